@@ -1,0 +1,132 @@
+/*
+ * qa_b200.h -- C-ABI of the B200-native int8 exhaustive k-NN path.
+ *
+ * Drop-in boundary for the reference package's kernel seam
+ * (quantann._backend, /root/reference/pkg/src/quantann/_backend.py:14-46).
+ * Each entry point names the reference routine it replaces.  All functions:
+ *
+ *   * are plain C (no C++/torch types), thread-safe (an internal mutex
+ *     serialises use of the per-device workspace);
+ *   * return QA_OK (0) or a nonzero QA_E* code; the message for the last
+ *     failure on the calling thread is available from qa_last_error();
+ *   * take DEVICE pointers unless the name ends in _host, and a CUDA stream
+ *     (cudaStream_t passed as void*, NULL = legacy default stream) on which
+ *     all work is enqueued.  Device variants are asynchronous except where
+ *     noted; _host variants are synchronous.
+ *
+ * Error mapping used by the Python shim (paper_2110_08919_b200/_lib.py):
+ *   QA_EINVAL       -> ValueError with the reference's message
+ *                      (_core.pyx:340-347, 357-358)
+ *   QA_EUNSUPPORTED -> NotImplementedError (shape outside this build's limits)
+ *   QA_ECUDA/ENOMEM -> RuntimeError
+ *
+ * Metric codes are the reference's (distances.py:22-27):
+ *   0 = INNER_PRODUCT (score = -dot), 1 = L2_SQUARED, 2 = ANGULAR (1 - cos).
+ */
+#ifndef QA_B200_H
+#define QA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    QA_OK = 0,
+    QA_EINVAL = 1,
+    QA_ECUDA = 2,
+    QA_ENOMEM = 3,
+    QA_EUNSUPPORTED = 4
+};
+
+/* Library identification. */
+int qa_version(void);
+const char *qa_last_error(void);
+/* Number of visible CUDA devices (0 when no driver/GPU); never fails. */
+int qa_device_count(void);
+/* Row stride (bytes) this build uses for int8 code matrices of width d:
+ * 32, 64 or a multiple of 128 -- the K granularity of the tcgen05 kind::i8
+ * MMA and the TMA swizzle width.  Pad columns are zero. */
+int64_t qa_code_stride(int64_t d);
+
+/* ---- calibration (quantizer.py:176-267; BASELINE min/max + symmetric) ----
+ * Per-dimension min and max of a float32 matrix x[n, ldx] (first d columns).
+ * Exact (order-free); NaN entries are ignored like numpy's fmin/fmax would
+ * NOT -- they propagate as in numpy min/max (result NaN for that column). */
+int qa_minmax_f32(const float *x, int64_t n, int64_t d, int64_t ldx,
+                  float *out_min, float *out_max, void *stream);
+
+/* ---- encode (quantizer.py:291-300 _quantize_matrix; 303-320 callers) ----
+ * codes[i, j] = Eq. 1 code of x[i, j] under per-dim window (k, sb, se) with
+ * `bits` in [1, 8], bit-exact with numpy's float32 evaluation order.  codes
+ * has row stride ldc >= d (bytes); columns [d, ldc) are written as zero.
+ * Optional (may be NULL) per-row outputs of the encoded vector:
+ *   sqnorm[i] = sum_j codes[i,j]^2 (int32), norm[i] = float(sqrt(double(sqnorm)))
+ * (_core.pyx:137-157 norms, int8 branch). */
+int qa_encode_i8(const float *x, int64_t n, int64_t d, int64_t ldx,
+                 const float *k, const float *sb, const float *se, int bits,
+                 int8_t *codes, int64_t ldc, int32_t *sqnorm, float *norm,
+                 void *stream);
+
+/* ---- norms (_core.pyx:137-157, int8 branch) ---- */
+int qa_norms_i8(const int8_t *codes, int64_t n, int64_t d, int64_t ldc,
+                int32_t *sqnorm, float *norm, void *stream);
+
+/* ---- exhaustive top-k (_core.pyx:301-365 scan_topk/_scan_i8) ----
+ * db[n, ldd] and q[nq, ldq] are int8 codes with ldd, ldq == qa_code_stride(d)
+ * (zero padded).  db_sqnorm/q_sqnorm (int32) are required for metric 1,
+ * db_norm/q_norm (float32, strictly positive) for metric 2; others may be
+ * NULL.  Writes keff = min(k, n) entries per query, ascending by
+ * (score, id): out_scores float64[nq, keff], out_ids int32[nq, keff] where
+ * id = row + id_offset.  Synchronises `stream` once at the end (overflow
+ * check of the candidate buffers). */
+int qa_scan_topk_i8(const int8_t *db, int64_t n, int64_t d, int64_t ldd,
+                    const int32_t *db_sqnorm, const float *db_norm,
+                    const int8_t *q, int64_t nq, int64_t ldq,
+                    const int32_t *q_sqnorm, const float *q_norm,
+                    int64_t k, int metric, int64_t id_offset,
+                    double *out_scores, int32_t *out_ids, void *stream);
+
+/* Host-buffer form of the reference call scan_topk(data, queries, k, metric,
+ * data_norms, query_norms) for int8 inputs: data[n, d] and queries[nq, d]
+ * C-contiguous int8 in HOST memory; data_norms/query_norms host float32
+ * (metric 2 only, may be NULL otherwise -- the device recomputes norms and
+ * uses the supplied ones only for validation of presence, like the
+ * reference).  Output host arrays sized nq*min(k,n).  Synchronous. */
+int qa_scan_topk_i8_host(const int8_t *data, int64_t n, int64_t d,
+                         const int8_t *queries, int64_t nq, int64_t k,
+                         int metric, const float *data_norms,
+                         const float *query_norms, double *out_scores,
+                         int32_t *out_ids);
+
+/* ---- multi-shard merge (row-sharded search, §8e) ----
+ * in_scores/in_ids: [G, nq, kin] per-shard sorted lists with GLOBAL ids;
+ * writes the first k of the (score, id)-merged list per query. */
+int qa_merge_topk(const double *in_scores, const int32_t *in_ids, int64_t G,
+                  int64_t nq, int64_t kin, int64_t k, double *out_scores,
+                  int32_t *out_ids, void *stream);
+
+/* ---- diagnostics (tests) ----
+ * Full int32 dot matrix out[nq, n] (row stride n) through one filter pass
+ * with the threshold disabled: impl 0 = the production tensor-core pass
+ * (tcgen05 kind::i8), impl 1 = the CUDA-core dp4a pass.  Used to validate
+ * the MMA path in isolation. */
+int qa_debug_dots_i8(const int8_t *db, int64_t n, const int8_t *q, int64_t nq,
+                     int64_t d, int impl, int32_t *out, void *stream);
+
+/* Per-call statistics of the last qa_scan_topk_i8 on this thread
+ * (rounds, candidates, kernel launches, overflow retries). */
+typedef struct {
+    int64_t rounds;
+    int64_t candidates;
+    int64_t launches;
+    int64_t retries;
+} qa_scan_stats;
+int qa_last_scan_stats(qa_scan_stats *out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QA_B200_H */

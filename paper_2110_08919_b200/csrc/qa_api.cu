@@ -1,0 +1,516 @@
+// qa_api.cu -- the C-ABI (include/qa_b200.h) and the search orchestration.
+//
+// Search algorithm for one query chunk (all of it stays on the device; the
+// only host synchronisation is the final overflow check):
+//
+//   round 0   rows [0, r0)          dense pass: every row is a candidate
+//   round i   rows [r_{i-1}, r_i)   filter pass with each query's current
+//                                   k-th score as threshold, r_i = ratio*r_{i-1}
+//   after every round: select (exact float64 scores, (score, id) sort, keep
+//   k, next threshold); at the end: finalize (scores + ids to the output).
+//
+// Any k rows' k-th best score bounds the final k-th best score, so a filter
+// pass never discards a row of the final top-k; rows whose threshold test
+// passes are re-scored exactly, so the output equals the reference's full
+// lexicographic sort truncated to keff (_core.pyx:301-330, 349).  Candidate
+// lists are bounded (cap per query); a query that overflows its list in any
+// round is recomputed with a larger cap.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/qa_b200.h"
+#include "qa_common.cuh"
+#include "qa_internal.h"
+
+namespace qa {
+
+namespace {
+
+thread_local std::string g_err;
+thread_local qa_scan_stats g_stats;
+
+int set_err(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_err(cudaError_t e, const char *what) {
+    if (e == cudaErrorNotSupported)
+        return set_err(QA_EUNSUPPORTED, "%s: shape not supported by this build", what);
+    if (e == cudaErrorMemoryAllocation) return set_err(QA_ENOMEM, "%s: out of device memory", what);
+    return set_err(QA_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define QA_TRY(expr, what)                         \
+    do {                                           \
+        cudaError_t _e = (expr);                   \
+        if (_e != cudaSuccess) return cuda_err(_e, what); \
+    } while (0)
+
+// Grow-only device buffers, one set per device, guarded by a mutex.
+struct Buf {
+    void *ptr = nullptr;
+    size_t bytes = 0;
+    cudaError_t reserve(size_t want) {
+        if (want <= bytes) return cudaSuccess;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+        size_t b = std::max(want, (size_t)256);
+        cudaError_t e = cudaMalloc(&ptr, b);
+        if (e == cudaSuccess) bytes = b;
+        return e;
+    }
+};
+
+struct Workspace {
+    std::mutex mu;
+    Buf state, state_cnt, thr, cand, ccount, ovf, flags, scratch;
+};
+
+constexpr int kMaxDevices = 64;
+Workspace g_ws[kMaxDevices];
+
+int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+
+bool use_simt_filter(int64_t kdim) {
+    static int forced = -1;
+    if (forced < 0) {
+        const char *v = getenv("QA_B200_FILTER");
+        forced = (v && strcmp(v, "simt") == 0) ? 1 : 0;
+    }
+    return forced == 1 || kdim > 1024;
+}
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+struct ScanPlan {
+    int64_t r0, ratio, cap, qchunk;
+};
+
+ScanPlan plan_scan(int64_t n, int64_t nq, int64_t keff, int64_t cap_min) {
+    ScanPlan p;
+    p.r0 = std::min(n, round_up(std::max<int64_t>(keff, 256), 128));
+    p.ratio = nq >= 256 ? 4 : 16;
+    p.cap = std::max<int64_t>({2048, p.r0, 2 * keff * p.ratio, cap_min});
+    const int64_t per_q = p.cap * (int64_t)sizeof(Cand) + keff * (int64_t)sizeof(Entry) + 64;
+    const int64_t budget = (int64_t)1 << 30;
+    p.qchunk = std::max<int64_t>(1, std::min<int64_t>(nq, budget / per_q));
+    p.qchunk = std::min<int64_t>(p.qchunk, 65535 * 16);
+    return p;
+}
+
+__global__ void gather_rows_kernel(const int8_t *__restrict__ src, int64_t ld,
+                                   const int32_t *__restrict__ idx, int64_t m,
+                                   int8_t *__restrict__ dst) {
+    int64_t r = blockIdx.x;
+    if (r >= m) return;
+    const int8_t *s = src + (int64_t)idx[r] * ld;
+    for (int64_t j = threadIdx.x; j < ld; j += blockDim.x) dst[r * ld + j] = s[j];
+}
+
+template <typename T>
+__global__ void gather_vals_kernel(const T *__restrict__ src, const int32_t *__restrict__ idx,
+                                   int64_t m, T *__restrict__ dst) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < m) dst[r] = src[idx[r]];
+}
+
+__global__ void scatter_results_kernel(const double *__restrict__ s, const int32_t *__restrict__ i,
+                                       const int32_t *__restrict__ idx, int64_t m, int64_t keff,
+                                       double *__restrict__ out_s, int32_t *__restrict__ out_i) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m * keff) return;
+    int64_t r = t / keff, j = t - r * keff;
+    out_s[(int64_t)idx[r] * keff + j] = s[t];
+    out_i[(int64_t)idx[r] * keff + j] = i[t];
+}
+
+// One complete search with a given minimum candidate capacity.  Returns
+// QA_OK; *overflowed receives the list of queries whose lists overflowed
+// (their output rows are invalid and must be recomputed).
+int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t ld, const int32_t *db_sqnorm,
+              const float *db_norm, const int8_t *q, int64_t nq, const int32_t *q_sqnorm,
+              const float *q_norm, int64_t keff, int metric, int64_t id_offset,
+              double *out_scores, int32_t *out_ids, int64_t cap_min, cudaStream_t st,
+              std::vector<int32_t> *overflowed) {
+    ScanPlan pl = plan_scan(n, nq, keff, cap_min);
+    const int64_t qc = pl.qchunk;
+    QA_TRY(ws.state.reserve((size_t)qc * keff * sizeof(Entry)), "workspace");
+    QA_TRY(ws.state_cnt.reserve((size_t)qc * 4), "workspace");
+    QA_TRY(ws.thr.reserve((size_t)qc * 4), "workspace");
+    QA_TRY(ws.cand.reserve((size_t)qc * pl.cap * sizeof(Cand)), "workspace");
+    QA_TRY(ws.ccount.reserve((size_t)qc * 4), "workspace");
+    QA_TRY(ws.ovf.reserve((size_t)nq * 4), "workspace");
+    QA_TRY(ws.flags.reserve(64), "workspace");
+    Entry *state = (Entry *)ws.state.ptr;
+    int32_t *state_cnt = (int32_t *)ws.state_cnt.ptr;
+    int32_t *thr = (int32_t *)ws.thr.ptr;
+    Cand *cand = (Cand *)ws.cand.ptr;
+    int32_t *ccount = (int32_t *)ws.ccount.ptr;
+    int32_t *ovf = (int32_t *)ws.ovf.ptr;
+    int32_t *flags = (int32_t *)ws.flags.ptr;  // [0] any overflow, [1] sched counter
+    QA_TRY(cudaMemsetAsync(ovf, 0, (size_t)nq * 4, st), "memset");
+    QA_TRY(cudaMemsetAsync(flags, 0, 64, st), "memset");
+    const bool simt = use_simt_filter(ld);
+
+    for (int64_t c0 = 0; c0 < nq; c0 += qc) {
+        const int64_t m = std::min(qc, nq - c0);
+        QA_TRY(launch_init_state(state_cnt, thr, m, metric, st), "init");
+        g_stats.launches += 1;
+        int64_t r_lo = 0, r_hi = pl.r0;
+        bool first = true;
+        for (;;) {
+            FilterArgs fa;
+            fa.db = db;
+            fa.ldd = ld;
+            fa.q = q + c0 * ld;
+            fa.ldq = ld;
+            fa.kdim = ld;
+            fa.nq = m;
+            fa.r_lo = r_lo;
+            fa.r_hi = r_hi;
+            fa.db_sqnorm = db_sqnorm;
+            fa.db_norm = db_norm;
+            fa.thr = thr;
+            fa.cand = cand;
+            fa.ccount = ccount;
+            fa.cap = pl.cap;
+            fa.metric = metric;
+            fa.mode = first ? 1 : 0;
+            fa.dots_out = nullptr;
+            fa.ld_dots = 0;
+            QA_TRY(launch_fill(ccount, m, first ? (int32_t)(r_hi - r_lo) : 0, st), "fill");
+            cudaError_t e = cudaErrorNotSupported;
+            if (!simt) e = launch_filter_tc(fa, flags + 1, st);
+            if (e == cudaErrorNotSupported) e = launch_filter_simt(fa, st);
+            QA_TRY(e, "filter");
+            SelectArgs sa;
+            sa.state = state;
+            sa.state_cnt = state_cnt;
+            sa.cand = cand;
+            sa.ccount = ccount;
+            sa.cap = pl.cap;
+            sa.nq = m;
+            sa.k = keff;
+            sa.metric = metric;
+            sa.db_sqnorm = db_sqnorm;
+            sa.db_norm = db_norm;
+            sa.q_sqnorm = q_sqnorm ? q_sqnorm + c0 : nullptr;
+            sa.q_norm = q_norm ? q_norm + c0 : nullptr;
+            sa.thr = thr;
+            sa.overflow = ovf + c0;
+            sa.any_overflow = flags;
+            QA_TRY(launch_select(sa, st), "select");
+            g_stats.launches += 3;
+            g_stats.rounds += 1;
+            if (r_hi >= n) break;
+            first = false;
+            r_lo = r_hi;
+            r_hi = std::min(n, round_up(r_hi * pl.ratio, 128));
+        }
+        QA_TRY(launch_finalize(state, state_cnt, m, keff, keff, metric, db_sqnorm, db_norm,
+                               q_sqnorm ? q_sqnorm + c0 : nullptr, q_norm ? q_norm + c0 : nullptr,
+                               id_offset, out_scores + c0 * keff, out_ids + c0 * keff, st),
+               "finalize");
+        g_stats.launches += 1;
+    }
+    int32_t any = 0;
+    QA_TRY(cudaMemcpyAsync(&any, flags, 4, cudaMemcpyDeviceToHost, st), "overflow check");
+    QA_TRY(cudaStreamSynchronize(st), "sync");
+    overflowed->clear();
+    if (any) {
+        std::vector<int32_t> h(nq);
+        QA_TRY(cudaMemcpy(h.data(), ovf, (size_t)nq * 4, cudaMemcpyDeviceToHost), "overflow list");
+        for (int64_t i = 0; i < nq; ++i)
+            if (h[i]) overflowed->push_back((int32_t)i);
+    }
+    return QA_OK;
+}
+
+int scan_entry(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_t *db_sqnorm,
+               const float *db_norm, const int8_t *q, int64_t nq, int64_t ldq,
+               const int32_t *q_sqnorm, const float *q_norm, int64_t k, int metric,
+               int64_t id_offset, double *out_scores, int32_t *out_ids, cudaStream_t st) {
+    g_stats = qa_scan_stats{0, 0, 0, 0};
+    if (metric < 0 || metric > 2) return set_err(QA_EINVAL, "unknown metric %d", metric);
+    if (k < 0) return set_err(QA_EINVAL, "k must be >= 0");
+    if (n < 0 || nq < 0 || d < 0) return set_err(QA_EINVAL, "negative shape");
+    const int64_t ld = qa_code_stride(d);
+    if (ldd != ld || ldq != ld)
+        return set_err(QA_EINVAL, "code row stride must be qa_code_stride(d)=%lld",
+                       (long long)ld);
+    const int64_t keff = std::min(k, n);
+    if (n == 0 || nq == 0 || keff == 0) return QA_OK;
+    if (metric == kAngular && (!db_norm || !q_norm))
+        return set_err(QA_EINVAL, "angular metric needs data and query norms");
+    if (metric == kL2 && (!db_sqnorm || !q_sqnorm))
+        return set_err(QA_EINVAL, "L2 metric needs data and query squared norms");
+    if (keff > kMaxK)
+        return set_err(QA_EUNSUPPORTED, "k=%lld above this build's limit %lld", (long long)keff,
+                       (long long)kMaxK);
+    // int32 exactness: |dot| <= d*128^2 and l2 <= d*255^2 must stay < 2^31
+    // (the reference accumulates in C int as well, _core.pyx:49-63).
+    if (d > 131071 || (metric == kL2 && d > 33025))
+        return set_err(QA_EUNSUPPORTED, "d=%lld exceeds the int32-exact range for this metric",
+                       (long long)d);
+    if (n > INT32_MAX) return set_err(QA_EUNSUPPORTED, "n exceeds int32 ids");
+    Workspace &ws = g_ws[current_device() % kMaxDevices];
+    std::lock_guard<std::mutex> lock(ws.mu);
+    std::vector<int32_t> ovf;
+    int rc = scan_impl(ws, db, n, ld, db_sqnorm, db_norm, q, nq, q_sqnorm, q_norm, keff, metric,
+                       id_offset, out_scores, out_ids, 0, st, &ovf);
+    if (rc != QA_OK) return rc;
+    int64_t cap = plan_scan(n, nq, keff, 0).cap;
+    while (!ovf.empty()) {
+        // Recompute the overflowed queries with 4x the candidate capacity;
+        // once cap >= n no list can overflow.
+        g_stats.retries += 1;
+        cap = std::min<int64_t>(cap * 4, std::max<int64_t>(n, 2048));
+        const int64_t m = (int64_t)ovf.size();
+        int32_t *idx = nullptr;
+        int8_t *qsub = nullptr;
+        int32_t *qsq = nullptr;
+        float *qn = nullptr;
+        double *s = nullptr;
+        int32_t *ids = nullptr;
+        QA_TRY(cudaMalloc(&idx, m * 4), "retry");
+        QA_TRY(cudaMalloc(&qsub, m * ld), "retry");
+        QA_TRY(cudaMalloc(&qsq, m * 4), "retry");
+        QA_TRY(cudaMalloc(&qn, m * 4), "retry");
+        QA_TRY(cudaMalloc(&s, m * keff * 8), "retry");
+        QA_TRY(cudaMalloc(&ids, m * keff * 4), "retry");
+        QA_TRY(cudaMemcpyAsync(idx, ovf.data(), m * 4, cudaMemcpyHostToDevice, st), "retry");
+        gather_rows_kernel<<<(unsigned)m, 128, 0, st>>>(q, ld, idx, m, qsub);
+        if (q_sqnorm)
+            gather_vals_kernel<int32_t><<<(unsigned)((m + 255) / 256), 256, 0, st>>>(q_sqnorm, idx,
+                                                                                   m, qsq);
+        if (q_norm)
+            gather_vals_kernel<float><<<(unsigned)((m + 255) / 256), 256, 0, st>>>(q_norm, idx, m,
+                                                                                 qn);
+        std::vector<int32_t> ovf2;
+        rc = scan_impl(ws, db, n, ld, db_sqnorm, db_norm, qsub, m, q_sqnorm ? qsq : nullptr,
+                       q_norm ? qn : nullptr, keff, metric, id_offset, s, ids, cap, st, &ovf2);
+        if (rc == QA_OK) {
+            scatter_results_kernel<<<(unsigned)((m * keff + 255) / 256), 256, 0, st>>>(
+                s, ids, idx, m, keff, out_scores, out_ids);
+            cudaError_t e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) rc = cuda_err(e, "retry");
+        }
+        // map second-level overflow indices back to original query ids
+        std::vector<int32_t> next;
+        for (int32_t i : ovf2) next.push_back(ovf[i]);
+        cudaFree(idx);
+        cudaFree(qsub);
+        cudaFree(qsq);
+        cudaFree(qn);
+        cudaFree(s);
+        cudaFree(ids);
+        if (rc != QA_OK) return rc;
+        ovf.swap(next);
+        if (cap >= n && !ovf.empty())
+            return set_err(QA_ECUDA, "internal: overflow at full capacity");
+    }
+    return QA_OK;
+}
+
+}  // namespace
+
+int num_sms() {
+    static int cached[kMaxDevices] = {0};
+    int dev = current_device() % kMaxDevices;
+    if (!cached[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = v > 0 ? v : 148;
+    }
+    return cached[dev];
+}
+
+}  // namespace qa
+
+using namespace qa;
+
+extern "C" {
+
+int qa_version(void) { return 1; }
+
+const char *qa_last_error(void) { return g_err.c_str(); }
+
+int qa_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return c;
+}
+
+int64_t qa_code_stride(int64_t d) {
+    if (d <= 32) return 32;
+    if (d <= 64) return 64;
+    return (d + 127) / 128 * 128;
+}
+
+int qa_last_scan_stats(qa_scan_stats *out) {
+    if (!out) return set_err(QA_EINVAL, "null stats pointer");
+    *out = g_stats;
+    return QA_OK;
+}
+
+int qa_minmax_f32(const float *x, int64_t n, int64_t d, int64_t ldx, float *out_min,
+                  float *out_max, void *stream) {
+    if (n < 0 || d < 1 || ldx < d) return set_err(QA_EINVAL, "bad shape");
+    cudaStream_t st = (cudaStream_t)stream;
+    Workspace &ws = g_ws[current_device() % kMaxDevices];
+    std::lock_guard<std::mutex> lock(ws.mu);
+    int64_t floats = (int64_t)num_sms() * 4 * 2 * d;
+    QA_TRY(ws.scratch.reserve((size_t)floats * 4), "workspace");
+    QA_TRY(launch_minmax(x, n, d, ldx, out_min, out_max, (float *)ws.scratch.ptr, floats, st),
+           "minmax");
+    return QA_OK;
+}
+
+int qa_encode_i8(const float *x, int64_t n, int64_t d, int64_t ldx, const float *k,
+                 const float *sb, const float *se, int bits, int8_t *codes, int64_t ldc,
+                 int32_t *sqnorm, float *norm, void *stream) {
+    if (bits < 1 || bits > 8) return set_err(QA_EINVAL, "bits must be between 1 and 8");
+    if (n < 0 || d < 0 || ldx < d || ldc < d) return set_err(QA_EINVAL, "bad shape");
+    QA_TRY(launch_encode(x, n, d, ldx, k, sb, se, bits, codes, ldc, sqnorm, norm,
+                         (cudaStream_t)stream),
+           "encode");
+    return QA_OK;
+}
+
+int qa_norms_i8(const int8_t *codes, int64_t n, int64_t d, int64_t ldc, int32_t *sqnorm,
+                float *norm, void *stream) {
+    if (n < 0 || d < 0 || ldc < d) return set_err(QA_EINVAL, "bad shape");
+    QA_TRY(launch_norms(codes, n, d, ldc, sqnorm, norm, (cudaStream_t)stream), "norms");
+    return QA_OK;
+}
+
+int qa_scan_topk_i8(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_t *db_sqnorm,
+                    const float *db_norm, const int8_t *q, int64_t nq, int64_t ldq,
+                    const int32_t *q_sqnorm, const float *q_norm, int64_t k, int metric,
+                    int64_t id_offset, double *out_scores, int32_t *out_ids, void *stream) {
+    return scan_entry(db, n, d, ldd, db_sqnorm, db_norm, q, nq, ldq, q_sqnorm, q_norm, k, metric,
+                      id_offset, out_scores, out_ids, (cudaStream_t)stream);
+}
+
+int qa_scan_topk_i8_host(const int8_t *data, int64_t n, int64_t d, const int8_t *queries,
+                         int64_t nq, int64_t k, int metric, const float *data_norms,
+                         const float *query_norms, double *out_scores, int32_t *out_ids) {
+    if (metric < 0 || metric > 2) return set_err(QA_EINVAL, "unknown metric %d", metric);
+    if (k < 0) return set_err(QA_EINVAL, "k must be >= 0");
+    if (n < 0 || nq < 0 || d < 0) return set_err(QA_EINVAL, "negative shape");
+    const int64_t keff = std::min(k, n);
+    if (n == 0 || nq == 0 || keff == 0) return QA_OK;
+    if (metric == kAngular && (!data_norms || !query_norms))
+        return set_err(QA_EINVAL, "angular metric needs data and query norms");
+    const int64_t ld = qa_code_stride(d);
+    cudaStream_t st = nullptr;
+    QA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+    int8_t *ddb = nullptr, *dq = nullptr;
+    int32_t *dsq = nullptr, *qsq = nullptr, *dids = nullptr;
+    float *dn = nullptr, *qn = nullptr;
+    double *ds = nullptr;
+    int rc = QA_OK;
+    auto fail = [&](cudaError_t e, const char *w) { rc = cuda_err(e, w); };
+    do {
+        cudaError_t e;
+        if ((e = cudaMalloc(&ddb, n * ld)) != cudaSuccess) { fail(e, "alloc"); break; }
+        if ((e = cudaMalloc(&dq, nq * ld)) != cudaSuccess) { fail(e, "alloc"); break; }
+        if ((e = cudaMalloc(&dsq, n * 4)) != cudaSuccess) { fail(e, "alloc"); break; }
+        if ((e = cudaMalloc(&qsq, nq * 4)) != cudaSuccess) { fail(e, "alloc"); break; }
+        if ((e = cudaMalloc(&dn, n * 4)) != cudaSuccess) { fail(e, "alloc"); break; }
+        if ((e = cudaMalloc(&qn, nq * 4)) != cudaSuccess) { fail(e, "alloc"); break; }
+        if ((e = cudaMalloc(&ds, nq * keff * 8)) != cudaSuccess) { fail(e, "alloc"); break; }
+        if ((e = cudaMalloc(&dids, nq * keff * 4)) != cudaSuccess) { fail(e, "alloc"); break; }
+        if (ld != d) {
+            cudaMemsetAsync(ddb, 0, n * ld, st);
+            cudaMemsetAsync(dq, 0, nq * ld, st);
+        }
+        if (d > 0) {
+            cudaMemcpy2DAsync(ddb, ld, data, d, d, n, cudaMemcpyHostToDevice, st);
+            cudaMemcpy2DAsync(dq, ld, queries, d, d, nq, cudaMemcpyHostToDevice, st);
+        }
+        launch_norms(ddb, n, d, ld, dsq, nullptr, st);
+        launch_norms(dq, nq, d, ld, qsq, nullptr, st);
+        if (metric == kAngular) {
+            cudaMemcpyAsync(dn, data_norms, n * 4, cudaMemcpyHostToDevice, st);
+            cudaMemcpyAsync(qn, query_norms, nq * 4, cudaMemcpyHostToDevice, st);
+        }
+        if ((e = cudaGetLastError()) != cudaSuccess) { fail(e, "upload"); break; }
+        rc = scan_entry(ddb, n, d, ld, dsq, dn, dq, nq, ld, qsq, qn, k, metric, 0, ds, dids, st);
+        if (rc != QA_OK) break;
+        cudaMemcpyAsync(out_scores, ds, nq * keff * 8, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(out_ids, dids, nq * keff * 4, cudaMemcpyDeviceToHost, st);
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { fail(e, "download"); break; }
+    } while (0);
+    cudaFree(ddb);
+    cudaFree(dq);
+    cudaFree(dsq);
+    cudaFree(qsq);
+    cudaFree(dn);
+    cudaFree(qn);
+    cudaFree(ds);
+    cudaFree(dids);
+    cudaStreamDestroy(st);
+    return rc;
+}
+
+int qa_merge_topk(const double *in_scores, const int32_t *in_ids, int64_t G, int64_t nq,
+                  int64_t kin, int64_t k, double *out_scores, int32_t *out_ids, void *stream) {
+    if (G < 1 || nq < 0 || kin < 0 || k < 0) return set_err(QA_EINVAL, "bad shape");
+    if (k > G * kin) return set_err(QA_EINVAL, "k exceeds the number of merged entries");
+    if (k > kMaxK) return set_err(QA_EUNSUPPORTED, "k above this build's limit");
+    QA_TRY(launch_merge(in_scores, in_ids, G, nq, kin, k, out_scores, out_ids,
+                        (cudaStream_t)stream),
+           "merge");
+    return QA_OK;
+}
+
+int qa_debug_dots_i8(const int8_t *db, int64_t n, const int8_t *q, int64_t nq, int64_t d,
+                     int impl, int32_t *out, void *stream) {
+    if (n < 1 || nq < 1 || d < 0) return set_err(QA_EINVAL, "bad shape");
+    const int64_t ld = qa_code_stride(d);
+    FilterArgs fa;
+    memset(&fa, 0, sizeof(fa));
+    fa.db = db;
+    fa.ldd = ld;
+    fa.q = q;
+    fa.ldq = ld;
+    fa.kdim = ld;
+    fa.nq = nq;
+    fa.r_lo = 0;
+    fa.r_hi = n;
+    fa.metric = kIP;
+    fa.mode = 2;
+    fa.dots_out = out;
+    fa.ld_dots = n;
+    cudaStream_t st = (cudaStream_t)stream;
+    Workspace &ws = g_ws[current_device() % kMaxDevices];
+    std::lock_guard<std::mutex> lock(ws.mu);
+    QA_TRY(ws.flags.reserve(64), "workspace");
+    cudaError_t e = impl == 0 ? launch_filter_tc(fa, (int32_t *)ws.flags.ptr + 1, st)
+                              : launch_filter_simt(fa, st);
+    QA_TRY(e, "debug dots");
+    return QA_OK;
+}
+
+}  // extern "C"

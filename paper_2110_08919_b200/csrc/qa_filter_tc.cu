@@ -1,0 +1,554 @@
+// qa_filter_tc.cu -- the fused tensor-core filter pass (sm_100a).
+//
+// One pass scores database rows [r_lo, r_hi) against a chunk of queries and
+// keeps only (query, row) pairs that can still enter the query's top-k:
+//
+//   * int8 x int8 -> int32 contraction on the 5th-gen tensor cores:
+//     tcgen05.mma.cta_group::1.kind::i8, M = 128 database rows, N = up to
+//     256 queries, K = 32 bytes per instruction, accumulator in TMEM
+//     (double-buffered: 2 x N columns of the 512);
+//   * operands staged by TMA (cp.async.bulk.tensor.2d) with the 32/64/128-byte
+//     swizzle matching the UMMA shared-memory descriptors; the query tile (B)
+//     is loaded once per work unit and stays resident while database tiles
+//     (A) stream through a multi-stage mbarrier ring;
+//   * the epilogue (8 warps) reads each accumulator with tcgen05.ld
+//     32x32b.x32, applies the metric's norm correction and compares against
+//     the per-query threshold with one predicate per element; survivors
+//     (rare) are staged in shared memory and flushed to the per-query global
+//     candidate lists with one atomic per (query, unit).  The int32 score
+//     matrix never reaches HBM.
+//
+// Warp roles (384 threads, 1 CTA per SM, persistent over an atomic work-unit
+// counter):  warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM allocator,
+// warp 3 idle, warps 4..11 epilogue.
+//
+// Reference semantics being accelerated: _core.pyx:301-330 (_scan_i8), the
+// pair kernel _core.pyx:49-96.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "qa_common.cuh"
+#include "qa_internal.h"
+
+namespace qa {
+
+namespace {
+
+constexpr int kBlockM = 128;
+constexpr int kThreads = 384;
+constexpr int kEpiWarp0 = 4;
+constexpr int kEpiThreads = 256;
+constexpr int kStageCap = 2048;  // survivors staged in smem per work unit
+constexpr int kEpiBarrier = 1;   // named barrier id for the epilogue warps
+
+// ------------------------------------------------------------------ PTX --
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t"
+        "}" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                            int32_t c0, int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)map) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
+        "}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32"
+        " {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15,"
+        " %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31},"
+        " [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+          "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void epi_barrier() {
+    asm volatile("bar.sync %0, %1;" ::"n"(kEpiBarrier), "n"(kEpiThreads) : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, swizzle SW bytes (32/64/128):
+// start>>4 [0,14), LBO>>4 [16,30) (unused for swizzled K-major: 1),
+// SBO>>4 [32,46) = 8 rows * SW bytes, version 1 at bit 46, layout type
+// [61,64): 128B=2, 64B=4, 32B=6.
+template <int SW>
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
+    constexpr uint64_t layout = SW == 128 ? 2 : (SW == 64 ? 4 : 6);
+    constexpr uint64_t sbo = (8 * SW) >> 4;
+    return (uint64_t)((saddr >> 4) & 0x3fff) | ((uint64_t)1 << 16) | (sbo << 32) |
+           ((uint64_t)1 << 46) | (layout << 61);
+}
+
+// Instruction descriptor for kind::i8: D=S32 (bits 4-5 = 2), A/B signed
+// int8 (bits 7-9, 10-12 = 1), both K-major, N>>3 at 17, M>>4 at 24.
+__host__ __device__ constexpr uint32_t make_idesc(int N) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(kBlockM >> 4) << 24);
+}
+
+struct Staged {
+    int32_t qloc;
+    int32_t sq;
+    int32_t row;
+    int32_t dot;
+};
+
+struct Params {
+    FilterArgs a;
+    int64_t n_tiles;        // 128-row tiles in [r_lo, r_hi)
+    int64_t tiles_per_unit;
+    int64_t n_qtiles;
+    int64_t n_units;
+    int kchunks;            // kdim / SW
+    int stages;
+    int *sched;
+};
+
+template <int SW, int N, int M>
+__global__ void __launch_bounds__(kThreads, 1)
+    filter_tc_kernel(const __grid_constant__ CUtensorMap tm_db,
+                     const __grid_constant__ CUtensorMap tm_q, const Params p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const FilterArgs &a = p.a;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    // ---- shared memory carve-up (1024-aligned operand buffers) ----
+    uintptr_t base = ((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023;
+    const uint32_t a_stage_bytes = kBlockM * SW;
+    const uint32_t b_bytes = (uint32_t)N * (uint32_t)a.kdim;
+    unsigned char *sA = (unsigned char *)base;
+    unsigned char *sB = sA + (size_t)p.stages * a_stage_bytes;
+    Staged *stage_buf = (Staged *)(sB + 2 * (size_t)b_bytes);
+    int32_t *thr_s = (int32_t *)(stage_buf + kStageCap);
+    int32_t *qcnt = thr_s + N;
+    int32_t *qbase = qcnt + N;
+    uint64_t *bars = (uint64_t *)(qbase + N);
+    uint64_t *a_full = bars;
+    uint64_t *a_empty = a_full + p.stages;
+    uint64_t *b_full = a_empty + p.stages;
+    uint64_t *b_empty = b_full + 2;
+    uint64_t *acc_full = b_empty + 2;
+    uint64_t *acc_empty = acc_full + 2;
+    uint64_t *unit_full = acc_empty + 2;
+    uint64_t *unit_empty = unit_full + 2;
+    int32_t *unit_id = (int32_t *)(unit_empty + 2);
+    uint32_t *tmem_base_s = (uint32_t *)(unit_id + 2);
+    int32_t *stage_n = (int32_t *)(tmem_base_s + 1);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < p.stages; ++s) {
+            mbar_init(a_full + s, 1);
+            mbar_init(a_empty + s, 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(b_full + s, 1);
+            mbar_init(b_empty + s, 1);
+            mbar_init(acc_full + s, 1);
+            mbar_init(acc_empty + s, kEpiThreads / 32);
+            mbar_init(unit_full + s, 1);
+            mbar_init(unit_empty + s, 2);
+        }
+        *stage_n = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tm_db);
+        prefetch_tmap(&tm_q);
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_base_s)),
+                     "n"(2 * N));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    for (int i = threadIdx.x; i < N; i += kThreads) qcnt[i] = 0;
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_base_s;
+
+    if (warp == 0) {
+        // =============================== TMA producer ===================
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t aph = 0;
+            for (int it = 0;; ++it) {
+                const int slot = it & 1;
+                const uint32_t ph = (it >> 1) & 1;
+                int64_t u = atomicAdd(p.sched, 1);
+                mbar_wait(unit_empty + slot, ph ^ 1);
+                unit_id[slot] = u < p.n_units ? (int32_t)u : -1;
+                mbar_arrive(unit_full + slot);
+                if (u >= p.n_units) break;
+                const int64_t t = u % p.n_qtiles, b = u / p.n_qtiles;
+                // resident query tile for this unit
+                mbar_wait(b_empty + slot, ph ^ 1);
+                mbar_arrive_expect_tx(b_full + slot, b_bytes);
+                unsigned char *dstB = sB + (size_t)slot * b_bytes;
+                for (int c = 0; c < p.kchunks; ++c)
+                    tma_load_2d(dstB + (size_t)c * N * SW, &tm_q, b_full + slot, c * SW,
+                                (int32_t)(t * N));
+                // streamed database tiles
+                const int64_t tile0 = b * p.tiles_per_unit;
+                const int64_t tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
+                for (int64_t tile = tile0; tile < tile1; ++tile) {
+                    const int32_t row0 = (int32_t)(a.r_lo + tile * kBlockM);
+                    for (int c = 0; c < p.kchunks; ++c) {
+                        mbar_wait(a_empty + stage, aph ^ 1);
+                        mbar_arrive_expect_tx(a_full + stage, a_stage_bytes);
+                        tma_load_2d(sA + (size_t)stage * a_stage_bytes, &tm_db, a_full + stage,
+                                    c * SW, row0);
+                        if (++stage == p.stages) {
+                            stage = 0;
+                            aph ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // =============================== MMA issuer =====================
+        constexpr uint32_t idesc = make_idesc(N);
+        int stage = 0;
+        uint32_t aph = 0;
+        int acc = 0;
+        uint32_t accph = 0;
+        for (int it = 0;; ++it) {
+            const int slot = it & 1;
+            const uint32_t ph = (it >> 1) & 1;
+            mbar_wait(unit_full + slot, ph);
+            const int32_t u = unit_id[slot];
+            __syncwarp();
+            if (u < 0) break;
+            const int64_t b = u / p.n_qtiles;
+            const int64_t tile0 = b * p.tiles_per_unit;
+            const int64_t tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
+            mbar_wait(b_full + slot, ph);
+            const uint32_t bbase = smem_u32(sB + (size_t)slot * b_bytes);
+            for (int64_t tile = tile0; tile < tile1; ++tile) {
+                mbar_wait(acc_empty + acc, accph ^ 1);
+                tc_fence_after();
+                const uint32_t tmem_d = tmem_base + (uint32_t)(acc * N);
+                for (int c = 0; c < p.kchunks; ++c) {
+                    mbar_wait(a_full + stage, aph);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t abase = smem_u32(sA + (size_t)stage * a_stage_bytes);
+                        const uint32_t bchunk = bbase + (uint32_t)(c * N * SW);
+#pragma unroll
+                        for (int kk = 0; kk < SW / 32; ++kk) {
+                            tc_mma_i8(tmem_d, make_desc<SW>(abase + kk * 32),
+                                      make_desc<SW>(bchunk + kk * 32), idesc,
+                                      (c | kk) != 0 ? 1u : 0u);
+                        }
+                        tc_commit(a_empty + stage);
+                    }
+                    __syncwarp();
+                    if (++stage == p.stages) {
+                        stage = 0;
+                        aph ^= 1;
+                    }
+                }
+                if (lane == 0) tc_commit(acc_full + acc);
+                __syncwarp();
+                if (++acc == 2) {
+                    acc = 0;
+                    accph ^= 1;
+                }
+            }
+            if (lane == 0) {
+                tc_commit(b_empty + slot);
+                mbar_arrive(unit_empty + slot);
+            }
+            __syncwarp();
+        }
+    } else if (warp >= kEpiWarp0) {
+        // =============================== epilogue =======================
+        const int ew = warp - kEpiWarp0;          // 0..7
+        const int quarter = warp & 3;             // TMEM lane quarter of this warp
+        const int half = ew >> 2;                 // column half
+        const int etid = threadIdx.x - kEpiWarp0 * 32;
+        int acc = 0;
+        uint32_t accph = 0;
+        for (int it = 0;; ++it) {
+            const int slot = it & 1;
+            const uint32_t ph = (it >> 1) & 1;
+            mbar_wait(unit_full + slot, ph);
+            const int32_t u = unit_id[slot];
+            epi_barrier();
+            if (etid == 0) mbar_arrive(unit_empty + slot);
+            if (u < 0) break;
+            const int64_t t = u % p.n_qtiles, b = u / p.n_qtiles;
+            const int64_t q0 = t * N;
+            const int nqt = (int)min((int64_t)N, a.nq - q0);
+            for (int i = etid; i < N && a.mode == 0; i += kEpiThreads) {
+                int32_t v;
+                if (i < nqt) {
+                    v = __ldg(a.thr + q0 + i);
+                } else {
+                    v = (M == kIP) ? INT32_MAX : (M == kL2 ? INT32_MIN : 0x7fc00000);
+                }
+                thr_s[i] = v;
+            }
+            epi_barrier();
+            const int64_t tile0 = b * p.tiles_per_unit;
+            const int64_t tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
+            for (int64_t tile = tile0; tile < tile1; ++tile) {
+                const int64_t row = a.r_lo + tile * kBlockM + quarter * 32 + lane;
+                const bool valid = row < a.r_hi;
+                int32_t xx = 0;
+                float inv_xn = 0.f;
+                if (valid) {
+                    if constexpr (M == kL2) xx = __ldg(a.db_sqnorm + row);
+                    if constexpr (M == kAngular) inv_xn = __frcp_rn(__ldg(a.db_norm + row));
+                }
+                mbar_wait(acc_full + acc, accph);
+                tc_fence_after();
+                const uint32_t tbase =
+                    tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * N);
+#pragma unroll 1
+                for (int c0 = half * (N / 2); c0 < (half + 1) * (N / 2) && c0 < nqt; c0 += 32) {
+                    int32_t v[32];
+                    tmem_ld32(tbase + (uint32_t)c0, v);
+                    if (a.mode == 0) {
+                        bool any = false;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            any |= passes<M>(v[j], thr_s[c0 + j], xx, inv_xn);
+                        if (any && valid) {
+                            for (int j = 0; j < 32; ++j) {
+                                if (!passes<M>(v[j], thr_s[c0 + j], xx, inv_xn)) continue;
+                                const int qloc = c0 + j;
+                                int e = atomicAdd(stage_n, 1);
+                                if (e < kStageCap) {
+                                    int sq = atomicAdd(qcnt + qloc, 1);
+                                    stage_buf[e] = Staged{qloc, sq, (int32_t)row, v[j]};
+                                } else {
+                                    // staging full: direct append (slow, rare)
+                                    int32_t s = atomicAdd(a.ccount + q0 + qloc, 1);
+                                    if (s < a.cap)
+                                        a.cand[(q0 + qloc) * a.cap + s] = Cand{(int32_t)row, v[j]};
+                                }
+                            }
+                        }
+                    } else if (valid) {
+#pragma unroll 4
+                        for (int j = 0; j < 32; ++j) {
+                            if (c0 + j >= nqt) break;
+                            const int64_t q = q0 + c0 + j;
+                            if (a.mode == 1)
+                                a.cand[q * a.cap + (row - a.r_lo)] = Cand{(int32_t)row, v[j]};
+                            else
+                                a.dots_out[q * a.ld_dots + row] = v[j];
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(acc_empty + acc);
+                if (++acc == 2) {
+                    acc = 0;
+                    accph ^= 1;
+                }
+            }
+            if (a.mode == 0) {
+                // ---- flush the unit's staged survivors ----
+                epi_barrier();
+                for (int i = etid; i < N; i += kEpiThreads) {
+                    int c = qcnt[i];
+                    if (c > 0) {
+                        qbase[i] = atomicAdd(a.ccount + q0 + i, c);
+                        qcnt[i] = 0;
+                    }
+                }
+                epi_barrier();
+                const int ns = min(*stage_n, kStageCap);
+                for (int e = etid; e < ns; e += kEpiThreads) {
+                    Staged s = stage_buf[e];
+                    int32_t dst = qbase[s.qloc] + s.sq;
+                    if (dst < a.cap) a.cand[(q0 + s.qloc) * a.cap + dst] = Cand{s.row, s.dot};
+                }
+                epi_barrier();
+                if (etid == 0) *stage_n = 0;
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "n"(2 * N));
+    }
+}
+
+// ------------------------------------------------------------- host side --
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)ptr;
+    }
+    return fn;
+}
+
+bool make_map(CUtensorMap *m, const int8_t *ptr, int64_t rows, int64_t cols, int64_t ld,
+              int box_rows, int sw) {
+    auto fn = get_encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld};
+    cuuint32_t box[2] = {(cuuint32_t)sw, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUtensorMapSwizzle swz = sw == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                       : (sw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                   : CU_TENSOR_MAP_SWIZZLE_32B);
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void *)ptr, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int SW, int N, int M>
+cudaError_t launch_t(const FilterArgs &a, int *sched, cudaStream_t st) {
+    CUtensorMap tm_db, tm_q;
+    if (!make_map(&tm_db, a.db, a.r_hi, a.kdim, a.ldd, kBlockM, SW)) return cudaErrorNotSupported;
+    if (!make_map(&tm_q, a.q, a.nq, a.kdim, a.ldq, N, SW)) return cudaErrorNotSupported;
+    Params p;
+    p.a = a;
+    p.n_tiles = (a.r_hi - a.r_lo + kBlockM - 1) / kBlockM;
+    p.n_qtiles = (a.nq + N - 1) / N;
+    p.kchunks = (int)(a.kdim / SW);
+    const int sms = num_sms();
+    int64_t tpu = (p.n_tiles * p.n_qtiles) / ((int64_t)sms * 4);
+    if (tpu < 1) tpu = 1;
+    if (tpu > 32) tpu = 32;
+    p.tiles_per_unit = tpu;
+    p.n_units = ((p.n_tiles + tpu - 1) / tpu) * p.n_qtiles;
+    p.sched = sched;
+    const size_t fixed = 1024 /*align slack*/ + 2 * (size_t)N * a.kdim +
+                         kStageCap * sizeof(Staged) + 3 * N * sizeof(int32_t) + 256;
+    const size_t budget = 227 * 1024;
+    const size_t stage_bytes = (size_t)kBlockM * SW;
+    if (fixed + 2 * stage_bytes > budget) return cudaErrorNotSupported;
+    int stages = (int)((budget - fixed) / stage_bytes);
+    if (stages > 8) stages = 8;
+    p.stages = stages;
+    const size_t smem = fixed + (size_t)stages * stage_bytes + (size_t)(2 * stages) * 8;
+    cudaError_t e = cudaFuncSetAttribute(filter_tc_kernel<SW, N, M>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(sched, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    int64_t grid = p.n_units < sms ? p.n_units : sms;
+    filter_tc_kernel<SW, N, M><<<(unsigned)grid, kThreads, smem, st>>>(tm_db, tm_q, p);
+    return cudaGetLastError();
+}
+
+template <int SW, int N>
+cudaError_t dispatch_metric(const FilterArgs &a, int *sched, cudaStream_t st) {
+    switch (a.metric) {
+        case kIP: return launch_t<SW, N, kIP>(a, sched, st);
+        case kL2: return launch_t<SW, N, kL2>(a, sched, st);
+        default: return launch_t<SW, N, kAngular>(a, sched, st);
+    }
+}
+
+template <int SW>
+cudaError_t dispatch_n(const FilterArgs &a, int *sched, cudaStream_t st) {
+    // Largest query tile whose double-buffered B fits (N * kdim <= 64 KiB),
+    // no larger than the query chunk needs.
+    int nmax = (int)(65536 / a.kdim);
+    if (a.nq > 128 && nmax >= 256) return dispatch_metric<SW, 256>(a, sched, st);
+    if (a.nq > 64 && nmax >= 128) return dispatch_metric<SW, 128>(a, sched, st);
+    if (nmax >= 64) return dispatch_metric<SW, 64>(a, sched, st);
+    return cudaErrorNotSupported;
+}
+
+}  // namespace
+
+cudaError_t launch_filter_tc(const FilterArgs &a, int *sched, cudaStream_t st) {
+    if (a.r_hi <= a.r_lo || a.nq == 0) return cudaSuccess;
+    if (a.kdim % 32 != 0 || a.kdim > 1024) return cudaErrorNotSupported;
+    if (a.ldd % 16 != 0 || a.ldq % 16 != 0) return cudaErrorNotSupported;
+    if (a.r_hi > INT32_MAX) return cudaErrorNotSupported;
+    if (a.kdim % 128 == 0) return dispatch_n<128>(a, sched, st);
+    if (a.kdim == 64) return dispatch_n<64>(a, sched, st);
+    if (a.kdim == 32) return dispatch_n<32>(a, sched, st);
+    return cudaErrorNotSupported;
+}
+
+}  // namespace qa

@@ -1,0 +1,92 @@
+// qa_internal.h -- launcher declarations shared between the translation units.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "qa_common.cuh"
+
+namespace qa {
+
+int num_sms();
+
+cudaError_t launch_encode(const float *x, int64_t n, int64_t d, int64_t ldx, const float *k,
+                          const float *sb, const float *se, int bits, int8_t *codes, int64_t ldc,
+                          int32_t *sqnorm, float *norm, cudaStream_t st);
+cudaError_t launch_norms(const int8_t *codes, int64_t n, int64_t d, int64_t ldc, int32_t *sqnorm,
+                         float *norm, cudaStream_t st);
+cudaError_t launch_minmax(const float *x, int64_t n, int64_t d, int64_t ldx, float *out_min,
+                          float *out_max, float *scratch, int64_t scratch_floats,
+                          cudaStream_t st);
+
+// Everything one filter pass needs.  Rows [r_lo, r_hi) of the database are
+// scored against queries [0, nq) of the current query chunk; every
+// (query, row) whose dot passes the query's threshold is appended to that
+// query's candidate list (capacity cap; count keeps counting past cap so
+// overflow is detectable).
+struct FilterArgs {
+    const int8_t *db;
+    int64_t ldd;
+    const int8_t *q;
+    int64_t ldq;
+    int64_t kdim;  // padded reduction length (== ldd == ldq, multiple of 32)
+    int64_t nq;
+    int64_t r_lo, r_hi;
+    const int32_t *db_sqnorm;
+    const float *db_norm;
+    const int32_t *thr;
+    Cand *cand;
+    int32_t *ccount;
+    int64_t cap;
+    int metric;
+    // 0 = filter (threshold test + append), 1 = dense (every row is a
+    // candidate: cand[q, row - r_lo]; the round-0 pass), 2 = diagnostics
+    // (every dot to dots_out[q, row]).
+    int mode;
+    int32_t *dots_out;
+    int64_t ld_dots;
+};
+
+// Tensor-core (tcgen05 kind::i8) filter pass.  Returns cudaErrorNotSupported
+// when the shape is outside what the kernel handles.
+cudaError_t launch_filter_tc(const FilterArgs &a, int *sched_counter, cudaStream_t st);
+// Plain CUDA-core (dp4a) filter pass, the bring-up path.
+cudaError_t launch_filter_simt(const FilterArgs &a, cudaStream_t st);
+
+struct SelectArgs {
+    Entry *state;        // [nq, k] sorted (score,row) prefix of length state_cnt[q]
+    int32_t *state_cnt;  // [nq]
+    const Cand *cand;    // [nq, cap]
+    const int32_t *ccount;
+    int64_t cap;
+    int64_t nq;
+    int64_t k;
+    int metric;
+    const int32_t *db_sqnorm;
+    const float *db_norm;
+    const int32_t *q_sqnorm;
+    const float *q_norm;
+    int32_t *thr;        // out: next-round threshold
+    int32_t *overflow;   // [nq] sticky per-query flag: candidate list overflowed
+    int32_t *any_overflow;
+};
+
+cudaError_t launch_select(const SelectArgs &a, cudaStream_t st);
+cudaError_t launch_init_state(int32_t *state_cnt, int32_t *thr, int64_t nq, int metric,
+                              cudaStream_t st);
+cudaError_t launch_fill(int32_t *p, int64_t n, int32_t v, cudaStream_t st);
+cudaError_t launch_finalize(const Entry *state, const int32_t *state_cnt, int64_t nq, int64_t k,
+                            int64_t keff, int metric, const int32_t *db_sqnorm,
+                            const float *db_norm, const int32_t *q_sqnorm, const float *q_norm,
+                            int64_t id_offset, double *out_scores, int32_t *out_ids,
+                            cudaStream_t st);
+cudaError_t launch_merge(const double *in_scores, const int32_t *in_ids, int64_t G, int64_t nq,
+                         int64_t kin, int64_t k, double *out_scores, int32_t *out_ids,
+                         cudaStream_t st);
+
+// Largest list the select kernel sorts in shared memory at once.
+constexpr int64_t kSortMax = 8192;
+// Largest k served (k + one candidate chunk must fit kSortMax).
+constexpr int64_t kMaxK = 2048;
+
+}  // namespace qa

@@ -1,0 +1,180 @@
+"""Device-resident data and the calls into libqa_b200 on torch-managed HBM.
+
+PyTorch supplies device memory and the current CUDA stream; every compute
+step is a kernel of libqa_b200.so reached through the C-ABI
+(include/qa_b200.h).  Layout in HBM:
+
+* codes   int8  [n, ld]  row stride ld = qa_code_stride(d) (32, 64 or a
+                          multiple of 128 bytes; pad columns are zero) -- the
+                          K granularity of the tcgen05 kind::i8 MMA and the
+                          TMA swizzle width;
+* sqnorm  int32 [n]      sum of squared codes (L2 epilogue correction);
+* norm    fp32  [n]      float32(sqrt(double(sqnorm))) (angular metric,
+                          reference _core.pyx:154-156).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, lib
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def default_device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2110_08919_b200 needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+@dataclass
+class DeviceCodes:
+    """int8 code matrix resident in HBM plus its per-row norms."""
+
+    codes: torch.Tensor    # int8 [n, ld]
+    d: int
+    sqnorm: torch.Tensor   # int32 [n]
+    norm: torch.Tensor     # float32 [n]
+
+    @property
+    def n(self) -> int:
+        return self.codes.shape[0]
+
+    @property
+    def ld(self) -> int:
+        return self.codes.shape[1]
+
+    @property
+    def device(self) -> torch.device:
+        return self.codes.device
+
+    @classmethod
+    def empty(cls, n: int, d: int, device=None) -> "DeviceCodes":
+        device = device or default_device()
+        ld = _lib.code_stride(d)
+        return cls(
+            codes=torch.empty((n, ld), dtype=torch.int8, device=device),
+            d=d,
+            sqnorm=torch.empty((n,), dtype=torch.int32, device=device),
+            norm=torch.empty((n,), dtype=torch.float32, device=device),
+        )
+
+    @classmethod
+    def from_host(cls, arr: np.ndarray, device=None) -> "DeviceCodes":
+        """Upload an int8 [n, d] host matrix and compute its norms on device."""
+        arr = np.ascontiguousarray(arr)
+        if arr.dtype != np.int8 or arr.ndim != 2:
+            raise ValueError("expected a 2-D int8 array")
+        n, d = arr.shape
+        out = cls.empty(n, d, device)
+        if n:
+            src = torch.from_numpy(arr.copy() if not arr.flags.writeable else arr)
+            if out.ld != d:
+                out.codes.zero_()
+            if d:
+                out.codes[:, :d].copy_(src, non_blocking=False)
+            elif out.ld:
+                out.codes.zero_()
+            norms_(out)
+        return out
+
+    def to_host(self) -> np.ndarray:
+        return self.codes[:, : self.d].cpu().numpy()
+
+    def slice_rows(self, lo: int, hi: int) -> "DeviceCodes":
+        return DeviceCodes(self.codes[lo:hi], self.d, self.sqnorm[lo:hi], self.norm[lo:hi])
+
+
+def norms_(dc: DeviceCodes) -> None:
+    """(Re)compute sqnorm/norm of a DeviceCodes in place (_core.pyx:137-157)."""
+    check(lib.qa_norms_i8(_p(dc.codes), dc.n, dc.d, dc.ld, _p(dc.sqnorm), _p(dc.norm), _stream()))
+
+
+def minmax(x: torch.Tensor):
+    """Per-dimension (min, max) of a float32 [n, d] device matrix, exact."""
+    if x.dtype != torch.float32 or x.dim() != 2 or not x.is_cuda:
+        raise ValueError("expected a float32 [n, d] CUDA tensor")
+    x = x if x.stride(1) == 1 else x.contiguous()
+    n, d = x.shape
+    mn = torch.empty(d, dtype=torch.float32, device=x.device)
+    mx = torch.empty(d, dtype=torch.float32, device=x.device)
+    check(lib.qa_minmax_f32(_p(x), n, d, x.stride(0), _p(mn), _p(mx), _stream()))
+    return mn, mx
+
+
+def encode(x: torch.Tensor, k: torch.Tensor, sb: torch.Tensor, se: torch.Tensor, bits: int,
+           out: DeviceCodes | None = None) -> DeviceCodes:
+    """Eq. 1 encode of a float32 [n, d] device matrix (quantizer.py:291-300),
+    fused with the code norms."""
+    if x.dtype != torch.float32 or x.dim() != 2 or not x.is_cuda:
+        raise ValueError("expected a float32 [n, d] CUDA tensor")
+    x = x if x.stride(1) == 1 else x.contiguous()
+    n, d = x.shape
+    for name, t in (("k", k), ("sb", sb), ("se", se)):
+        if t.dtype != torch.float32 or t.shape != (d,) or t.device != x.device:
+            raise ValueError(f"{name} must be float32[{d}] on {x.device}")
+    if out is None:
+        out = DeviceCodes.empty(n, d, x.device)
+    check(lib.qa_encode_i8(_p(x), n, d, x.stride(0), _p(k.contiguous()), _p(sb.contiguous()),
+                           _p(se.contiguous()), int(bits), _p(out.codes), out.ld,
+                           _p(out.sqnorm), _p(out.norm), _stream()))
+    return out
+
+
+def scan_topk(db: DeviceCodes, q: DeviceCodes, k: int, metric: int, db_norm=None, q_norm=None,
+              id_offset: int = 0, out=None):
+    """Exhaustive top-k of every query over the database (_core.pyx:333-365).
+
+    Returns (scores float64 [nq, keff], ids int32 [nq, keff]) on the device,
+    rows ascending by (score, id), keff = min(k, n).  For the angular metric
+    ``db_norm``/``q_norm`` (float32 device vectors) override the stored code
+    norms, as the reference takes them from the caller.
+    """
+    if db.d != q.d:
+        raise ValueError("dimension mismatch between data and queries")
+    if k < 0:
+        raise ValueError("k must be >= 0")
+    keff = min(k, db.n)
+    dev = db.device
+    if out is None:
+        scores = torch.empty((q.n, keff), dtype=torch.float64, device=dev)
+        ids = torch.empty((q.n, keff), dtype=torch.int32, device=dev)
+    else:
+        scores, ids = out
+    dn = db.norm if db_norm is None else db_norm
+    qn = q.norm if q_norm is None else q_norm
+    check(lib.qa_scan_topk_i8(_p(db.codes), db.n, db.d, db.ld, _p(db.sqnorm), _p(dn),
+                              _p(q.codes), q.n, q.ld, _p(q.sqnorm), _p(qn), int(k), int(metric),
+                              int(id_offset), _p(scores), _p(ids), _stream()))
+    return scores, ids
+
+
+def merge_topk(scores: torch.Tensor, ids: torch.Tensor, k: int):
+    """Merge G per-shard sorted lists [G, nq, kin] (global ids) into the
+    (score, id)-first k per query."""
+    G, nq, kin = scores.shape
+    out_s = torch.empty((nq, k), dtype=torch.float64, device=scores.device)
+    out_i = torch.empty((nq, k), dtype=torch.int32, device=scores.device)
+    check(lib.qa_merge_topk(_p(scores.contiguous()), _p(ids.contiguous()), G, nq, kin, k,
+                            _p(out_s), _p(out_i), _stream()))
+    return out_s, out_i
+
+
+def debug_dots(db: DeviceCodes, q: DeviceCodes, impl: int = 0) -> torch.Tensor:
+    """Full int32 dot matrix [nq, n] through one unfiltered pass
+    (impl 0 = tcgen05 tensor cores, 1 = dp4a CUDA cores)."""
+    out = torch.empty((q.n, db.n), dtype=torch.int32, device=db.device)
+    check(lib.qa_debug_dots_i8(_p(db.codes), db.n, _p(q.codes), q.n, db.d, int(impl), _p(out),
+                               _stream()))
+    return out

@@ -1,0 +1,159 @@
+"""Generate the golden fixtures in tests/golden/ from the REAL reference.
+
+Runs only in the dev container (needs /root/reference): imports the
+reference package from /root/reference/pkg/src (its numpy quantizer) and
+its compiled kernel module quantann._core built from the reference sources
+by ``make -C oracle ref``.  The outputs are small .npz files committed next
+to this script; the tests read them on any machine.
+
+    python tests/golden/make_golden.py
+"""
+
+from __future__ import annotations
+
+import importlib.util
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+OUT = Path(__file__).resolve().parent
+REF_SRC = Path("/root/reference/pkg/src")
+
+sys.path.insert(0, str(ROOT))
+
+
+def load_reference():
+    """The reference package (pure-numpy backend from the source tree) and
+    its compiled _core from oracle/_ref."""
+    sys.path.insert(0, str(REF_SRC))
+    import quantann  # noqa: E402  (reference, /root/reference/pkg/src)
+
+    spec = importlib.util.spec_from_file_location(
+        "quantann._core", next((ROOT / "oracle/_ref/quantann").glob("_core*.so")))
+    core = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(core)
+    assert core.BACKEND == "compiled"
+    return quantann, core
+
+
+def encode_cases(qa):
+    from quantann.quantizer import (QuantizerParams, QuantMode, estimate_stats, fit,
+                                    quantize_dataset)
+    from quantann import DenseDataset
+
+    cases = {}
+    # hand window of test_quantizer.py:_fit_window(-0.1, 0.1)
+    st = estimate_stats(DenseDataset(np.asarray([[-0.1], [0.1]], dtype=np.float32)))
+    p = fit(st, 8, QuantMode.SIGMA_CLAMP).params
+    x = np.asarray([[0.0], [0.05], [-0.1], [0.1], [0.5], [-0.2], [np.nan], [np.inf], [-np.inf]],
+                   dtype=np.float32)
+    cases["hand"] = (x, p, quantize_dataset(DenseDataset(x), p).data)
+    rng = np.random.default_rng(123)
+    for bits in range(1, 9):
+        for mode in (QuantMode.SIGMA_CLAMP, QuantMode.ABS_MAX, QuantMode.UNIFORM_SIGMA_CLAMP):
+            d = int(rng.integers(1, 70))
+            n = int(rng.integers(8, 300))
+            data = (rng.normal(0.0, rng.uniform(0.01, 3.0), size=(n, d))
+                    + rng.normal(0.0, 2.0, size=d)).astype(np.float32)
+            p = fit(estimate_stats(DenseDataset(data)), bits, mode).params
+            probe = data.copy()
+            probe[0] = p.sb
+            probe[1] = p.se
+            probe[2] = p.k
+            probe[3] = np.nextafter(p.sb, np.float32(-np.inf))
+            probe[4] = np.nextafter(p.se, np.float32(np.inf))
+            probe[5, : min(d, 4)] = [np.nan, np.inf, -np.inf, 1e-40][: min(d, 4)]
+            probe[6] = np.float32(1e-42)  # denormal
+            codes = quantize_dataset(DenseDataset(probe), p).data
+            cases[f"b{bits}_m{int(mode)}"] = (probe, p, codes)
+    arrays = {}
+    for name, (x, p, c) in cases.items():
+        arrays[f"{name}__x"] = x
+        arrays[f"{name}__k"] = p.k
+        arrays[f"{name}__sb"] = p.sb
+        arrays[f"{name}__se"] = p.se
+        arrays[f"{name}__bits"] = np.int64(p.bits)
+        arrays[f"{name}__codes"] = c
+    np.savez_compressed(OUT / "encode_cases.npz", **arrays)
+    return len(cases)
+
+
+def scan_cases(core):
+    arrays = {}
+    rng = np.random.default_rng(7)
+    count = 0
+    for i in range(36):
+        metric = i % 3
+        n = int(rng.integers(1, 700))
+        d = int(rng.integers(1, 48))
+        nq = int(rng.integers(1, 6))
+        lo, hi = (-127, 128) if i % 4 else (-3, 4)  # every 4th case: heavy ties
+        X = rng.integers(lo, hi, size=(n, d)).astype(np.int8)
+        Q = rng.integers(lo, hi, size=(nq, d)).astype(np.int8)
+        if metric == 2:
+            X[~X.any(axis=1), 0] = 1
+            Q[~Q.any(axis=1), 0] = 1
+        k = int(rng.choice([1, 10, 100, n, n + 1]))
+        xn, qn = core.norms(X), core.norms(Q)
+        sc, ids = core.scan_topk(X, Q, k, metric, xn, qn)
+        pre = f"c{i}"
+        arrays.update({f"{pre}__X": X, f"{pre}__Q": Q, f"{pre}__k": np.int64(k),
+                       f"{pre}__metric": np.int64(metric), f"{pre}__xn": xn,
+                       f"{pre}__qn": qn, f"{pre}__scores": sc, f"{pre}__ids": ids})
+        count += 1
+    np.savez_compressed(OUT / "scan_cases.npz", **arrays)
+    return count
+
+
+def cfg_minis(qa, core):
+    """BASELINE cfg0 (L2, min/max) and cfg1 (angular, symmetric) at reduced
+    size through the reference pipeline: constructed stats -> fit(ABS_MAX)
+    -> quantize_dataset -> compiled scan_topk."""
+    from paper_2110_08919_b200 import synth
+    from quantann import DenseDataset
+    from quantann.quantizer import DimensionStats, QuantMode, fit, quantize_dataset
+
+    arrays = {}
+    for cfg, (n, nq) in ((0, (6000, 24)), (1, (6000, 24)), (3, (6000, 24))):
+        X, Q = synth.generate(cfg, n=n, nq=nq)
+        mn = X.astype(np.float64).min(axis=0)
+        mx = X.astype(np.float64).max(axis=0)
+        if cfg == 1:
+            center = np.zeros_like(mn)
+            half = np.maximum(np.abs(mn), np.abs(mx))
+        else:
+            center = (mn + mx) / 2.0
+            half = (mx - mn) / 2.0
+        z = np.zeros_like(center)
+        stats = DimensionStats(mu=center, sigma=z, min=center - half, max=center + half,
+                               trimmed_absmax=half, pooled_mu=0.0, pooled_sigma=0.0, count=n)
+        p = fit(stats, 8, QuantMode.ABS_MAX).params
+        Xc = quantize_dataset(DenseDataset(X), p).data
+        Qc = quantize_dataset(DenseDataset(Q), p).data
+        metric = synth.CONFIGS[cfg]["metric"]
+        xn, qn = core.norms(Xc), core.norms(Qc)
+        sc, ids = core.scan_topk(Xc, Qc, 100, metric, xn, qn)
+        f_xn, f_qn = core.norms(X), core.norms(Q)
+        _, gt32 = core.scan_topk(X, Q, 100, metric, f_xn, f_qn)
+        pre = f"cfg{cfg}"
+        arrays.update({f"{pre}__k": p.k, f"{pre}__sb": p.sb, f"{pre}__se": p.se,
+                       f"{pre}__mn": mn, f"{pre}__mx": mx,
+                       f"{pre}__codes_sha": np.frombuffer(
+                           __import__("hashlib").sha256(Xc.tobytes()).digest(), np.uint8),
+                       f"{pre}__qcodes": Qc, f"{pre}__scores": sc, f"{pre}__ids": ids,
+                       f"{pre}__gt32": gt32})
+    np.savez_compressed(OUT / "cfg_minis.npz", **arrays)
+
+
+def main():
+    qa, core = load_reference()
+    ne = encode_cases(qa)
+    ns = scan_cases(core)
+    cfg_minis(qa, core)
+    print(f"wrote {ne} encode cases, {ns} scan cases, cfg minis to {OUT}")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,290 @@
+"""Parity of the CUDA path (through the C-ABI) with the CPU oracle.
+
+Bar: bit-exact codes, norms, int32 dots, top-k ids AND float64 scores for
+every metric -- the reference's own contract (_core.pyx:8-14).  Sizes here
+are ones the oracle finishes in seconds; full BASELINE sizes are covered by
+size-independent properties in test_gpu_scale.py.
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2110_08919_b200 as qa  # noqa: E402
+from paper_2110_08919_b200 import _backend, device as dev, synth  # noqa: E402
+
+
+def _rand_codes(rng, n, d, lo=-127, hi=128, nonzero=False):
+    X = rng.integers(lo, hi, size=(n, d)).astype(np.int8)
+    if nonzero:
+        X[~X.any(axis=1), 0] = 1
+    return X
+
+
+def _scan_gpu(X, Q, k, metric, xn=None, qn=None):
+    return _backend.scan_topk(X, Q, k, metric, xn, qn)
+
+
+def _scan_oracle(oracle, X, Q, k, metric):
+    return oracle.scan_topk_i8(X, Q, k, metric, oracle.norms_i8(X), oracle.norms_i8(Q))
+
+
+# ----------------------------------------------------------------- encode --
+
+def test_encode_golden(golden_encode):
+    for name, c in golden_encode.items():
+        x = torch.from_numpy(c["x"]).cuda()
+        k, sb, se = (torch.from_numpy(c[f]).cuda() for f in ("k", "sb", "se"))
+        codes = dev.encode(x, k, sb, se, int(c["bits"]))
+        np.testing.assert_array_equal(codes.to_host(), c["codes"], err_msg=name)
+        pad = codes.codes[:, codes.d:].cpu().numpy()
+        assert not pad.any(), name
+        w = c["codes"].astype(np.int64)
+        np.testing.assert_array_equal(codes.sqnorm.cpu().numpy(), (w * w).sum(1), err_msg=name)
+
+
+def test_encode_large_random_vs_oracle(oracle):
+    rng = np.random.default_rng(5)
+    for d in (1, 3, 100, 128, 257):
+        x = (rng.normal(size=(3001, d)) * rng.uniform(0.1, 10, size=d)).astype(np.float32)
+        x[::97, 0] = np.nan
+        x[1::89, -1] = np.float32(1e-41)
+        mn, mx = oracle.minmax(np.nan_to_num(x, nan=0.0))
+        k, sb, se = oracle.fit_range((mn + mx) / 2, (mx - mn) / 2 * 0.8)
+        for bits in (8, 5, 1):
+            want = oracle.encode(x, k, sb, se, bits)
+            got = dev.encode(torch.from_numpy(x).cuda(), *(torch.from_numpy(a).cuda()
+                                                             for a in (k, sb, se)), bits)
+            np.testing.assert_array_equal(got.to_host(), want, err_msg=f"d={d} bits={bits}")
+            np.testing.assert_array_equal(got.norm.cpu().numpy(), oracle.norms_i8(want))
+
+
+def test_minmax_exact(oracle):
+    rng = np.random.default_rng(6)
+    x = rng.normal(size=(50_001, 100)).astype(np.float32)
+    mn, mx = dev.minmax(torch.from_numpy(x).cuda())
+    omn, omx = oracle.minmax(x)
+    np.testing.assert_array_equal(mn.double().cpu().numpy(), omn)
+    np.testing.assert_array_equal(mx.double().cpu().numpy(), omx)
+
+
+def test_norms_vs_oracle(oracle):
+    rng = np.random.default_rng(7)
+    X = _rand_codes(rng, 777, 200, -128, 128)
+    np.testing.assert_array_equal(_backend.norms(X), oracle.norms_i8(X))
+
+
+# ------------------------------------------------------------------- dots --
+
+@pytest.mark.parametrize("d", [1, 16, 32, 33, 64, 100, 128, 200, 256, 512, 1024])
+def test_tensor_core_dots_exact(d):
+    rng = np.random.default_rng(d)
+    n, nq = 1000 + d, 300 + (d % 7)
+    X = _rand_codes(rng, n, d, -128, 128)
+    Q = _rand_codes(rng, nq, d, -128, 128)
+    want = Q.astype(np.int64) @ X.astype(np.int64).T
+    db = dev.DeviceCodes.from_host(X)
+    qs = dev.DeviceCodes.from_host(Q)
+    tc = dev.debug_dots(db, qs, impl=0).cpu().numpy()
+    np.testing.assert_array_equal(tc, want)
+    simt = dev.debug_dots(db, qs, impl=1).cpu().numpy()
+    np.testing.assert_array_equal(simt, want)
+
+
+@pytest.mark.parametrize("nq", [1, 7, 64, 65, 128, 129, 256, 300])
+def test_tensor_core_dots_query_tiles(nq):
+    rng = np.random.default_rng(100 + nq)
+    X = _rand_codes(rng, 4099, 128)
+    Q = _rand_codes(rng, nq, 128)
+    want = Q.astype(np.int64) @ X.astype(np.int64).T
+    got = dev.debug_dots(dev.DeviceCodes.from_host(X), dev.DeviceCodes.from_host(Q)).cpu().numpy()
+    np.testing.assert_array_equal(got, want)
+
+
+# ------------------------------------------------------------------- scan --
+
+def test_scan_golden(golden_scan):
+    for name, c in golden_scan.items():
+        sc, ids = _scan_gpu(c["X"], c["Q"], int(c["k"]), int(c["metric"]), c["xn"], c["qn"])
+        np.testing.assert_array_equal(ids, c["ids"], err_msg=name)
+        np.testing.assert_array_equal(sc, c["scores"], err_msg=name)
+
+
+def test_gate2_random_instances(oracle):
+    # test_acceptance.py:116-135 (int8 half): 200 instances, n<=1000, d<=32,
+    # all metrics, bit-exact ids and scores through exact_topk
+    for i in range(200):
+        rng = np.random.default_rng(1000 + i)
+        n, d = int(rng.integers(1, 1001)), int(rng.integers(1, 33))
+        metric = qa.Metric(i % 3)
+        X = _rand_codes(rng, n, d, nonzero=True)
+        q = _rand_codes(rng, 1, d, nonzero=True)[0]
+        k = min(int(rng.choice([1, 10, 100])), n)
+        res = qa.exact_topk(qa.DenseDataset(X), q, k, metric)
+        sc, ids = _scan_oracle(oracle, X, q[None], k, int(metric))
+        np.testing.assert_array_equal(res.ids, ids[0])
+        np.testing.assert_array_equal(res.scores, sc[0])
+
+
+def test_exact_hand_cases():
+    X = qa.DenseDataset(np.int8([[1], [2], [3]]))
+    res = qa.exact_topk(X, np.int8([4]), 1, qa.Metric.L2_SQUARED)
+    assert res.ids[0] == 2 and res.scores[0] == 1.0
+    ties = qa.DenseDataset(np.int8([[1, 0], [1, 0], [0, 0], [1, 0]]))
+    assert list(qa.exact_topk(ties, np.int8([1, 0]), 4, qa.Metric.L2_SQUARED).ids) == [0, 1, 3, 2]
+    full = qa.exact_topk(qa.DenseDataset(np.int8([[5], [1], [3]])), np.int8([0]), 10,
+                         qa.Metric.L2_SQUARED)
+    assert list(full.ids) == [1, 2, 0] and len(full) == 3
+    gt = qa.batch_ground_truth(qa.DenseDataset(np.int8([[1, 1]])),
+                               qa.DenseDataset(np.int8([[2, 2]])), 1, qa.Metric.L2_SQUARED)
+    np.testing.assert_array_equal(gt.ids, [[0]])
+    # inner product of zero vector scores -0.0 exactly like the reference
+    r = qa.exact_topk(qa.DenseDataset(np.int8([[0, 0], [1, 1]])), np.int8([0, 0]), 2,
+                      qa.Metric.INNER_PRODUCT)
+    assert np.signbit(r.scores[0]) and r.scores[0] == 0.0
+    with pytest.raises(qa.ZeroNorm):
+        qa.exact_topk(qa.DenseDataset(np.int8([[1, 0], [0, 0]])), np.int8([1, 0]), 1,
+                      qa.Metric.ANGULAR)
+
+
+def test_self_query_property():
+    rng = np.random.default_rng(4)
+    X = _rand_codes(rng, 3000, 24)
+    X = np.unique(X, axis=0)
+    gt = qa.batch_ground_truth(qa.DenseDataset(X), qa.DenseDataset(X), 1, qa.Metric.L2_SQUARED)
+    np.testing.assert_array_equal(gt.ids[:, 0], np.arange(X.shape[0]))
+
+
+@pytest.mark.parametrize("metric", [0, 1, 2])
+@pytest.mark.parametrize("k", [1, 10, 100, 1000])
+def test_scan_mid_size_vs_oracle(oracle, metric, k):
+    rng = np.random.default_rng(10 * metric + k)
+    X = _rand_codes(rng, 20_000, 96, nonzero=True)
+    Q = _rand_codes(rng, 70, 96, nonzero=True)
+    sc, ids = _scan_gpu(X, Q, k, metric, oracle.norms_i8(X), oracle.norms_i8(Q))
+    osc, oids = _scan_oracle(oracle, X, Q, k, metric)
+    np.testing.assert_array_equal(ids, oids)
+    np.testing.assert_array_equal(sc, osc)
+
+
+@pytest.mark.parametrize("metric", [0, 1, 2])
+def test_heavy_ties_exercise_overflow_retry(oracle, metric):
+    # narrow code range: thousands of rows share each score, so candidate
+    # lists overflow and the capacity-retry path must restore exactness.
+    rng = np.random.default_rng(77 + metric)
+    X = _rand_codes(rng, 60_000, 8, -2, 3, nonzero=True)
+    X[:20_000] = X[0]
+    Q = np.repeat(X[:1], 3, axis=0)
+    Q[1] = _rand_codes(rng, 1, 8, -2, 3, nonzero=True)[0]
+    sc, ids = _scan_gpu(X, Q, 100, metric, oracle.norms_i8(X), oracle.norms_i8(Q))
+    osc, oids = _scan_oracle(oracle, X, Q, 100, metric)
+    np.testing.assert_array_equal(ids, oids)
+    np.testing.assert_array_equal(sc, osc)
+
+
+def test_many_queries_and_edge_shapes(oracle):
+    rng = np.random.default_rng(9)
+    for n, nq, d, k in ((1, 5, 3, 1), (1, 5, 3, 10), (129, 513, 16, 128), (5000, 1500, 40, 30),
+                        (300, 2, 200, 300), (257, 3, 64, 2048)):
+        for metric in (0, 1, 2):
+            X = _rand_codes(rng, n, d, nonzero=True)
+            Q = _rand_codes(rng, nq, d, nonzero=True)
+            sc, ids = _scan_gpu(X, Q, k, metric, oracle.norms_i8(X), oracle.norms_i8(Q))
+            osc, oids = _scan_oracle(oracle, X, Q, k, metric)
+            np.testing.assert_array_equal(ids, oids, err_msg=f"{n} {nq} {d} {k} {metric}")
+            np.testing.assert_array_equal(sc, osc)
+
+
+def test_host_c_abi_entry(oracle):
+    import ctypes
+
+    from paper_2110_08919_b200._lib import check, lib
+
+    rng = np.random.default_rng(11)
+    X = _rand_codes(rng, 3000, 50, nonzero=True)
+    Q = _rand_codes(rng, 17, 50, nonzero=True)
+    for metric in (0, 1, 2):
+        xn, qn = oracle.norms_i8(X), oracle.norms_i8(Q)
+        out_s = np.empty((17, 100), np.float64)
+        out_i = np.empty((17, 100), np.int32)
+        p = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        check(lib.qa_scan_topk_i8_host(p(X), 3000, 50, p(Q), 17, 100, metric, p(xn), p(qn),
+                                       p(out_s), p(out_i)))
+        osc, oids = _scan_oracle(oracle, X, Q, 100, metric)
+        np.testing.assert_array_equal(out_i, oids)
+        np.testing.assert_array_equal(out_s, osc)
+
+
+# ------------------------------------------------- BASELINE configs (mini) --
+
+@pytest.mark.parametrize("cfg", [0, 1, 3])
+def test_cfg_minis_golden(golden_cfg, cfg):
+    g = golden_cfg[f"cfg{cfg}"]
+    X, Q = synth.generate(cfg, n=6000, nq=24)
+    c = synth.CONFIGS[cfg]
+    x = torch.from_numpy(X).cuda()
+    index = qa.Int8Index.build(x, qa.Metric(c["metric"]), c["calibration"])
+    np.testing.assert_array_equal(index.params.k, g["k"])
+    np.testing.assert_array_equal(index.params.sb, g["sb"])
+    np.testing.assert_array_equal(index.params.se, g["se"])
+    assert hashlib.sha256(index.codes.to_host().tobytes()).digest() == g["codes_sha"].tobytes()
+    qc = index.encode_queries(torch.from_numpy(Q).cuda())
+    np.testing.assert_array_equal(qc.to_host(), g["qcodes"])
+    sc, ids = index.search_codes(qc, 100)
+    np.testing.assert_array_equal(ids.cpu().numpy(), g["ids"])
+    np.testing.assert_array_equal(sc.cpu().numpy(), g["scores"])
+    r = qa.recall_at_k(qa.GroundTruth(g["gt32"]), ids.cpu().numpy(), 100)
+    r_ref = qa.recall_at_k(qa.GroundTruth(g["gt32"]), g["ids"], 100)
+    assert abs(r.mean - r_ref.mean) <= 0.001
+
+
+def test_cfg0_full_parity(oracle):
+    # BASELINE config 0 at full size: 100k x 128, 1000 queries, L2, min/max.
+    X, Q = synth.generate(0)
+    index = qa.Int8Index.build(torch.from_numpy(X).cuda(), qa.Metric.L2_SQUARED, "minmax")
+    mn, mx = oracle.minmax(X)
+    k, sb, se = oracle.fit_range((mn + mx) / 2.0, (mx - mn) / 2.0)
+    np.testing.assert_array_equal(index.params.sb, sb)
+    np.testing.assert_array_equal(index.params.se, se)
+    Xc = oracle.encode(X, k, sb, se, 8)
+    Qc = oracle.encode(Q, k, sb, se, 8)
+    np.testing.assert_array_equal(index.codes.to_host(), Xc)
+    sc, ids = index.search(torch.from_numpy(Q).cuda(), 100)
+    osc, oids = _scan_oracle(oracle, Xc, Qc, 100, 1)
+    np.testing.assert_array_equal(ids.cpu().numpy(), oids)
+    np.testing.assert_array_equal(sc.cpu().numpy(), osc)
+
+
+# ------------------------------------------------------------ sharding --
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_virtual_shards_merge_equals_full(oracle, G):
+    from paper_2110_08919_b200.sharded import pad_topk, shard_bounds
+
+    rng = np.random.default_rng(G)
+    X = _rand_codes(rng, 10_007, 32, -6, 7, nonzero=True)   # many ties across shards
+    Q = _rand_codes(rng, 40, 32, -6, 7, nonzero=True)
+    for metric in (0, 1, 2):
+        db = dev.DeviceCodes.from_host(X)
+        qs = dev.DeviceCodes.from_host(Q)
+        kin = min(100, -(-X.shape[0] // G))
+        parts_s, parts_i = [], []
+        for r in range(G):
+            lo, hi = shard_bounds(X.shape[0], G, r)
+            s, i = dev.scan_topk(db.slice_rows(lo, hi), qs, 100, metric, id_offset=lo)
+            s, i = pad_topk(s, i, kin)
+            parts_s.append(s)
+            parts_i.append(i)
+        ms, mi = dev.merge_topk(torch.stack(parts_s), torch.stack(parts_i), 100)
+        osc, oids = _scan_oracle(oracle, X, Q, 100, metric)
+        np.testing.assert_array_equal(mi.cpu().numpy(), oids)
+        np.testing.assert_array_equal(ms.cpu().numpy(), osc)
