@@ -77,12 +77,16 @@ int qa_norms_i8(const int8_t *codes, int64_t n, int64_t d, int64_t ldc,
  * db[n, ldd] and q[nq, ldq] are int8 codes with ldd, ldq == qa_code_stride(d)
  * (zero padded).  db_sqnorm/q_sqnorm (int32) are required for metric 1,
  * db_norm/q_norm (float32, strictly positive) for metric 2; others may be
- * NULL.  Writes keff = min(k, n) entries per query, ascending by
+ * NULL.  row_ids (optional, int32[n]) maps stored row -> reported id; it lets
+ * an index keep its rows in a different order (e.g. sorted by norm, see
+ * qa_order_rows_by_norm) and still report, and break ties by, the caller's
+ * ids.  Writes keff = min(k, n) entries per query, ascending by
  * (score, id): out_scores float64[nq, keff], out_ids int32[nq, keff] where
- * id = row + id_offset.  Synchronises `stream` once at the end (overflow
- * check of the candidate buffers). */
+ * id = (row_ids ? row_ids[row] : row) + id_offset.  Synchronises `stream`
+ * once at the end (overflow check of the candidate buffers). */
 int qa_scan_topk_i8(const int8_t *db, int64_t n, int64_t d, int64_t ldd,
                     const int32_t *db_sqnorm, const float *db_norm,
+                    const int32_t *row_ids,
                     const int8_t *q, int64_t nq, int64_t ldq,
                     const int32_t *q_sqnorm, const float *q_norm,
                     int64_t k, int metric, int64_t id_offset,
@@ -90,15 +94,24 @@ int qa_scan_topk_i8(const int8_t *db, int64_t n, int64_t d, int64_t ldd,
 
 /* Host-buffer form of the reference call scan_topk(data, queries, k, metric,
  * data_norms, query_norms) for int8 inputs: data[n, d] and queries[nq, d]
- * C-contiguous int8 in HOST memory; data_norms/query_norms host float32
- * (metric 2 only, may be NULL otherwise -- the device recomputes norms and
- * uses the supplied ones only for validation of presence, like the
- * reference).  Output host arrays sized nq*min(k,n).  Synchronous. */
+ * C-contiguous int8 in HOST memory; data_norms/query_norms host float32,
+ * required for metric 2 and used as given (the reference takes them from
+ * the caller too), ignored otherwise.  Output host arrays sized
+ * nq*min(k,n).  Synchronous. */
 int qa_scan_topk_i8_host(const int8_t *data, int64_t n, int64_t d,
                          const int8_t *queries, int64_t nq, int64_t k,
                          int metric, const float *data_norms,
                          const float *query_norms, double *out_scores,
                          int32_t *out_ids);
+
+/* ---- index layout ----
+ * perm = rows ordered by ascending squared norm (stable), and the gather
+ * that applies it to codes + norms (norm/norm_out may be NULL).  An index
+ * stored in this order gives the filter pass tight per-warp bounds. */
+int qa_order_rows_by_norm(const int32_t *sqnorm, int64_t n, int32_t *perm, void *stream);
+int qa_permute_rows_i8(const int8_t *codes, const int32_t *sqnorm, const float *norm,
+                       int64_t n, int64_t ldc, const int32_t *perm, int8_t *codes_out,
+                       int32_t *sqnorm_out, float *norm_out, void *stream);
 
 /* ---- multi-shard merge (row-sharded search, §8e) ----
  * in_scores/in_ids: [G, nq, kin] per-shard sorted lists with GLOBAL ids;
@@ -115,15 +128,24 @@ int qa_merge_topk(const double *in_scores, const int32_t *in_ids, int64_t G,
 int qa_debug_dots_i8(const int8_t *db, int64_t n, const int8_t *q, int64_t nq,
                      int64_t d, int impl, int32_t *out, void *stream);
 
-/* Per-call statistics of the last qa_scan_topk_i8 on this thread
- * (rounds, candidates, kernel launches, overflow retries). */
+/* Per-call statistics of the last qa_scan_topk_i8 on this thread: filter
+ * rounds, kernel launches, overflow retries, the algorithmic int8 ops of the
+ * filter passes (2 * queries * rows * d, unpadded d), and -- when profiling
+ * is enabled -- CUDA-event durations measured on the launch stream around
+ * every filter / select launch. */
 typedef struct {
     int64_t rounds;
     int64_t candidates;
     int64_t launches;
     int64_t retries;
+    int64_t filter_launches;
+    double filter_ops;
+    double filter_ms;
+    double select_ms;
 } qa_scan_stats;
 int qa_last_scan_stats(qa_scan_stats *out);
+/* Enable (1) / disable (0) event timing of filter and select launches. */
+int qa_set_profiling(int on);
 
 #ifdef __cplusplus
 }

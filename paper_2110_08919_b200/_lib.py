@@ -34,6 +34,10 @@ class ScanStats(ctypes.Structure):
         ("candidates", c_i64),
         ("launches", c_i64),
         ("retries", c_i64),
+        ("filter_launches", c_i64),
+        ("filter_ops", ctypes.c_double),
+        ("filter_ms", ctypes.c_double),
+        ("select_ms", ctypes.c_double),
     ]
 
 
@@ -51,9 +55,11 @@ SIGNATURES = {
     "qa_norms_i8": (c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "qa_scan_topk_i8": (
         c_int,
-        [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp,
+        [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp,
          c_i64, c_int, c_i64, c_vp, c_vp, c_vp],
     ),
+    "qa_order_rows_by_norm": (c_int, [c_vp, c_i64, c_vp, c_vp]),
+    "qa_permute_rows_i8": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "qa_scan_topk_i8_host": (
         c_int,
         [c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_int, c_vp, c_vp, c_vp, c_vp],
@@ -61,6 +67,7 @@ SIGNATURES = {
     "qa_merge_topk": (c_int, [c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "qa_debug_dots_i8": (c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_int, c_vp, c_vp]),
     "qa_last_scan_stats": (c_int, [ctypes.POINTER(ScanStats)]),
+    "qa_set_profiling": (c_int, [c_int]),
 }
 
 
@@ -104,5 +111,8 @@ def code_stride(d: int) -> int:
 def last_scan_stats() -> dict:
     s = ScanStats()
     check(lib.qa_last_scan_stats(ctypes.byref(s)))
-    return {"rounds": s.rounds, "candidates": s.candidates, "launches": s.launches,
-            "retries": s.retries}
+    return {name: getattr(s, name) for name, _ in ScanStats._fields_}
+
+
+def set_profiling(on: bool) -> None:
+    check(lib.qa_set_profiling(1 if on else 0))

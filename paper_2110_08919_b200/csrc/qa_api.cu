@@ -34,6 +34,48 @@ namespace {
 
 thread_local std::string g_err;
 thread_local qa_scan_stats g_stats;
+bool g_profiling = false;
+
+// Event pairs recorded around filter / select launches when profiling.
+struct EventTimer {
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::pair<int, int>> spans;  // (kind, index of start event)
+    size_t used = 0;
+    cudaEvent_t next() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+    void reset() {
+        used = 0;
+        spans.clear();
+    }
+    void begin(int kind, cudaStream_t st) {
+        if (!g_profiling) return;
+        spans.emplace_back(kind, (int)used);
+        cudaEventRecord(next(), st);
+    }
+    void end(cudaStream_t st) {
+        if (!g_profiling) return;
+        cudaEventRecord(next(), st);
+    }
+    // call after the stream is synchronised
+    void accumulate(qa_scan_stats &s) {
+        for (auto &sp : spans) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, pool[sp.second], pool[sp.second + 1]);
+            if (sp.first == 0)
+                s.filter_ms += ms;
+            else
+                s.select_ms += ms;
+        }
+        reset();
+    }
+};
+thread_local EventTimer g_timer;
 
 int set_err(int code, const char *fmt, ...) {
     char buf[512];
@@ -144,8 +186,10 @@ __global__ void scatter_results_kernel(const double *__restrict__ s, const int32
 // One complete search with a given minimum candidate capacity.  Returns
 // QA_OK; *overflowed receives the list of queries whose lists overflowed
 // (their output rows are invalid and must be recomputed).
-int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t ld, const int32_t *db_sqnorm,
-              const float *db_norm, const int8_t *q, int64_t nq, const int32_t *q_sqnorm,
+int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t ld,
+              const int32_t *db_sqnorm,
+              const float *db_norm, const int32_t *row_ids, const int8_t *q, int64_t nq,
+              const int32_t *q_sqnorm,
               const float *q_norm, int64_t keff, int metric, int64_t id_offset,
               double *out_scores, int32_t *out_ids, int64_t cap_min, cudaStream_t st,
               std::vector<int32_t> *overflowed) {
@@ -197,9 +241,13 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t ld, const int3
             fa.ld_dots = 0;
             QA_TRY(launch_fill(ccount, m, first ? (int32_t)(r_hi - r_lo) : 0, st), "fill");
             cudaError_t e = cudaErrorNotSupported;
+            g_timer.begin(0, st);
             if (!simt) e = launch_filter_tc(fa, flags + 1, st);
             if (e == cudaErrorNotSupported) e = launch_filter_simt(fa, st);
+            g_timer.end(st);
             QA_TRY(e, "filter");
+            g_stats.filter_launches += 1;
+            g_stats.filter_ops += 2.0 * (double)m * (double)(r_hi - r_lo) * (double)d_alg;
             SelectArgs sa;
             sa.state = state;
             sa.state_cnt = state_cnt;
@@ -213,10 +261,13 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t ld, const int3
             sa.db_norm = db_norm;
             sa.q_sqnorm = q_sqnorm ? q_sqnorm + c0 : nullptr;
             sa.q_norm = q_norm ? q_norm + c0 : nullptr;
+            sa.row_ids = row_ids;
             sa.thr = thr;
             sa.overflow = ovf + c0;
             sa.any_overflow = flags;
+            g_timer.begin(1, st);
             QA_TRY(launch_select(sa, st), "select");
+            g_timer.end(st);
             g_stats.launches += 3;
             g_stats.rounds += 1;
             if (r_hi >= n) break;
@@ -224,15 +275,15 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t ld, const int3
             r_lo = r_hi;
             r_hi = std::min(n, round_up(r_hi * pl.ratio, 128));
         }
-        QA_TRY(launch_finalize(state, state_cnt, m, keff, keff, metric, db_sqnorm, db_norm,
-                               q_sqnorm ? q_sqnorm + c0 : nullptr, q_norm ? q_norm + c0 : nullptr,
-                               id_offset, out_scores + c0 * keff, out_ids + c0 * keff, st),
+        QA_TRY(launch_finalize(state, m, keff, keff, metric, id_offset, out_scores + c0 * keff,
+                               out_ids + c0 * keff, st),
                "finalize");
         g_stats.launches += 1;
     }
     int32_t any = 0;
     QA_TRY(cudaMemcpyAsync(&any, flags, 4, cudaMemcpyDeviceToHost, st), "overflow check");
     QA_TRY(cudaStreamSynchronize(st), "sync");
+    g_timer.accumulate(g_stats);
     overflowed->clear();
     if (any) {
         std::vector<int32_t> h(nq);
@@ -244,10 +295,10 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t ld, const int3
 }
 
 int scan_entry(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_t *db_sqnorm,
-               const float *db_norm, const int8_t *q, int64_t nq, int64_t ldq,
+               const float *db_norm, const int32_t *row_ids, const int8_t *q, int64_t nq, int64_t ldq,
                const int32_t *q_sqnorm, const float *q_norm, int64_t k, int metric,
                int64_t id_offset, double *out_scores, int32_t *out_ids, cudaStream_t st) {
-    g_stats = qa_scan_stats{0, 0, 0, 0};
+    g_stats = qa_scan_stats{};
     if (metric < 0 || metric > 2) return set_err(QA_EINVAL, "unknown metric %d", metric);
     if (k < 0) return set_err(QA_EINVAL, "k must be >= 0");
     if (n < 0 || nq < 0 || d < 0) return set_err(QA_EINVAL, "negative shape");
@@ -273,7 +324,8 @@ int scan_entry(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_
     Workspace &ws = g_ws[current_device() % kMaxDevices];
     std::lock_guard<std::mutex> lock(ws.mu);
     std::vector<int32_t> ovf;
-    int rc = scan_impl(ws, db, n, ld, db_sqnorm, db_norm, q, nq, q_sqnorm, q_norm, keff, metric,
+    g_timer.reset();
+    int rc = scan_impl(ws, db, n, d, ld, db_sqnorm, db_norm, row_ids, q, nq, q_sqnorm, q_norm, keff, metric,
                        id_offset, out_scores, out_ids, 0, st, &ovf);
     if (rc != QA_OK) return rc;
     int64_t cap = plan_scan(n, nq, keff, 0).cap;
@@ -304,7 +356,7 @@ int scan_entry(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_
             gather_vals_kernel<float><<<(unsigned)((m + 255) / 256), 256, 0, st>>>(q_norm, idx, m,
                                                                                  qn);
         std::vector<int32_t> ovf2;
-        rc = scan_impl(ws, db, n, ld, db_sqnorm, db_norm, qsub, m, q_sqnorm ? qsq : nullptr,
+        rc = scan_impl(ws, db, n, d, ld, db_sqnorm, db_norm, row_ids, qsub, m, q_sqnorm ? qsq : nullptr,
                        q_norm ? qn : nullptr, keff, metric, id_offset, s, ids, cap, st, &ovf2);
         if (rc == QA_OK) {
             scatter_results_kernel<<<(unsigned)((m * keff + 255) / 256), 256, 0, st>>>(
@@ -367,6 +419,11 @@ int64_t qa_code_stride(int64_t d) {
     return (d + 127) / 128 * 128;
 }
 
+int qa_set_profiling(int on) {
+    g_profiling = on != 0;
+    return QA_OK;
+}
+
 int qa_last_scan_stats(qa_scan_stats *out) {
     if (!out) return set_err(QA_EINVAL, "null stats pointer");
     *out = g_stats;
@@ -405,10 +462,11 @@ int qa_norms_i8(const int8_t *codes, int64_t n, int64_t d, int64_t ldc, int32_t 
 }
 
 int qa_scan_topk_i8(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_t *db_sqnorm,
-                    const float *db_norm, const int8_t *q, int64_t nq, int64_t ldq,
+                    const float *db_norm, const int32_t *row_ids, const int8_t *q, int64_t nq,
+                    int64_t ldq,
                     const int32_t *q_sqnorm, const float *q_norm, int64_t k, int metric,
                     int64_t id_offset, double *out_scores, int32_t *out_ids, void *stream) {
-    return scan_entry(db, n, d, ldd, db_sqnorm, db_norm, q, nq, ldq, q_sqnorm, q_norm, k, metric,
+    return scan_entry(db, n, d, ldd, db_sqnorm, db_norm, row_ids, q, nq, ldq, q_sqnorm, q_norm, k, metric,
                       id_offset, out_scores, out_ids, (cudaStream_t)stream);
 }
 
@@ -456,7 +514,7 @@ int qa_scan_topk_i8_host(const int8_t *data, int64_t n, int64_t d, const int8_t 
             cudaMemcpyAsync(qn, query_norms, nq * 4, cudaMemcpyHostToDevice, st);
         }
         if ((e = cudaGetLastError()) != cudaSuccess) { fail(e, "upload"); break; }
-        rc = scan_entry(ddb, n, d, ld, dsq, dn, dq, nq, ld, qsq, qn, k, metric, 0, ds, dids, st);
+        rc = scan_entry(ddb, n, d, ld, dsq, dn, nullptr, dq, nq, ld, qsq, qn, k, metric, 0, ds, dids, st);
         if (rc != QA_OK) break;
         cudaMemcpyAsync(out_scores, ds, nq * keff * 8, cudaMemcpyDeviceToHost, st);
         cudaMemcpyAsync(out_ids, dids, nq * keff * 4, cudaMemcpyDeviceToHost, st);
@@ -472,6 +530,30 @@ int qa_scan_topk_i8_host(const int8_t *data, int64_t n, int64_t d, const int8_t 
     cudaFree(dids);
     cudaStreamDestroy(st);
     return rc;
+}
+
+int qa_order_rows_by_norm(const int32_t *sqnorm, int64_t n, int32_t *perm, void *stream) {
+    if (n < 0 || n > INT32_MAX) return set_err(QA_EINVAL, "bad shape");
+    if (n == 0) return QA_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    Workspace &ws = g_ws[current_device() % kMaxDevices];
+    std::lock_guard<std::mutex> lock(ws.mu);
+    size_t need = 0;
+    QA_TRY(launch_order_by_key(sqnorm, n, perm, nullptr, 0, &need, st), "order");
+    QA_TRY(ws.scratch.reserve(need), "workspace");
+    QA_TRY(launch_order_by_key(sqnorm, n, perm, ws.scratch.ptr, ws.scratch.bytes, &need, st),
+           "order");
+    return QA_OK;
+}
+
+int qa_permute_rows_i8(const int8_t *codes, const int32_t *sqnorm, const float *norm, int64_t n,
+                       int64_t ldc, const int32_t *perm, int8_t *codes_out, int32_t *sqnorm_out,
+                       float *norm_out, void *stream) {
+    if (n < 0 || ldc % 16 != 0) return set_err(QA_EINVAL, "bad shape");
+    QA_TRY(launch_permute_rows(codes, sqnorm, norm, n, ldc, perm, codes_out, sqnorm_out, norm_out,
+                               (cudaStream_t)stream),
+           "permute");
+    return QA_OK;
 }
 
 int qa_merge_topk(const double *in_scores, const int32_t *in_ids, int64_t G, int64_t nq,

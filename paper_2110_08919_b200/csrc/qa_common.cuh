@@ -16,19 +16,21 @@ namespace qa {
 
 enum Metric : int { kIP = 0, kL2 = 1, kAngular = 2 };
 
-// Candidate produced by a filter pass: database row (local to the search)
-// and the exact int32 dot product with the query.
+// Candidate produced by a filter pass: stored database row and the exact
+// int32 dot product with the query.
 struct Cand {
     int32_t row;
     int32_t dot;
 };
 
-// One retained neighbour: order key, row, dot.  skey orders exactly like the
-// float64 score (ties resolved by row).
+// One retained neighbour: order key, reported id (the row's position in the
+// caller's corpus -- differs from the stored row when the index keeps its
+// rows sorted by norm), stored row.  skey orders exactly like the float64
+// score; ties are resolved by id, the reference's rule.
 struct Entry {
     unsigned long long skey;
+    int32_t id;
     int32_t row;
-    int32_t dot;
 };
 
 // Order-preserving map of an int32 score to an unsigned key.
@@ -47,6 +49,16 @@ __host__ __device__ __forceinline__ unsigned long long skey_from_double(double s
     return b < 0 ? ~(unsigned long long)b : ((unsigned long long)b | 0x8000000000000000ull);
 }
 
+// Inverses of the maps above.
+__host__ __device__ __forceinline__ int32_t int_from_skey(unsigned long long k) {
+    return (int32_t)((uint32_t)k ^ 0x80000000u);
+}
+__device__ __forceinline__ double double_from_skey(unsigned long long k) {
+    long long b = (k & 0x8000000000000000ull) ? (long long)(k & 0x7fffffffffffffffull)
+                                              : (long long)~k;
+    return __longlong_as_double(b);
+}
+
 __device__ __forceinline__ double angular_score(int32_t dot, float qn, float xn) {
     // qn*xn is exact in float64 (24+24 significant bits); one correctly
     // rounded division and one correctly rounded subtraction, exactly as
@@ -56,7 +68,7 @@ __device__ __forceinline__ double angular_score(int32_t dot, float qn, float xn)
 }
 
 __device__ __forceinline__ bool entry_less(const Entry &a, const Entry &b) {
-    return a.skey < b.skey || (a.skey == b.skey && a.row < b.row);
+    return a.skey < b.skey || (a.skey == b.skey && a.id < b.id);
 }
 
 // Filter thresholds (one 32-bit word per query, meaning depends on metric):

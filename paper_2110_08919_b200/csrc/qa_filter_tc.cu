@@ -40,6 +40,8 @@ constexpr int kEpiWarp0 = 4;
 constexpr int kEpiThreads = 256;
 constexpr int kStageCap = 2048;  // survivors staged in smem per work unit
 constexpr int kEpiBarrier = 1;   // named barrier id for the epilogue warps
+constexpr int kVRow = 36;        // words per lane row of slow-path values (32 + pad: no
+                                 // bank conflicts for 16-byte stores)
 
 // ------------------------------------------------------------------ PTX --
 
@@ -113,6 +115,62 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint6
         : "memory");
 }
 
+__device__ __forceinline__ void tmem_wait() {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// tcgen05.ld without the wait: the registers are valid only after tmem_wait().
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, int32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32"
+        " {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15,"
+        " %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31},"
+        " [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+          "=r"(v[31])
+        : "r"(taddr)
+        : "memory");
+}
+
+__device__ __forceinline__ int4 lds128(uint32_t addr) {
+    int4 r;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "r"(addr));
+    return r;
+}
+
+__device__ __forceinline__ int32_t lds32(uint32_t addr) {
+    int32_t r;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(r) : "r"(addr));
+    return r;
+}
+
+__device__ __forceinline__ void sts32(uint32_t addr, int32_t v) {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void sts128(uint32_t addr, int32_t a, int32_t b, int32_t c, int32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+                 "r"(d)
+                 : "memory");
+}
+
+template <typename T, typename Op>
+__device__ __forceinline__ T warp_reduce(T v, Op op) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__device__ __forceinline__ int32_t clamp_i64(long long v) {
+    return v > INT32_MAX ? INT32_MAX : (v < INT32_MIN ? INT32_MIN : (int32_t)v);
+}
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32"
@@ -167,6 +225,7 @@ struct Params {
     int64_t n_units;
     int kchunks;            // kdim / SW
     int stages;
+    int b_slots;            // 1 or 2 query-tile buffers
     int *sched;
 };
 
@@ -185,11 +244,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t b_bytes = (uint32_t)N * (uint32_t)a.kdim;
     unsigned char *sA = (unsigned char *)base;
     unsigned char *sB = sA + (size_t)p.stages * a_stage_bytes;
-    Staged *stage_buf = (Staged *)(sB + 2 * (size_t)b_bytes);
+    // the query tile is double-buffered across work units when two copies fit
+    // in 64 KiB, else single-buffered (one MMA bubble per unit switch)
+    const int bslots = p.b_slots;
+    Staged *stage_buf = (Staged *)(sB + (size_t)bslots * b_bytes);
     int32_t *thr_s = (int32_t *)(stage_buf + kStageCap);
     int32_t *qcnt = thr_s + N;
     int32_t *qbase = qcnt + N;
-    uint64_t *bars = (uint64_t *)(qbase + N);
+    int32_t *bnd_s = qbase + N;  // [8 epilogue warps][N/2] per-warp column bounds
+    int32_t *vst_s = bnd_s + 4 * N;  // [8 warps][32 lanes][kVRow] slow-path value rows
+    uint64_t *bars = (uint64_t *)(vst_s + 8 * 32 * kVRow);
     uint64_t *a_full = bars;
     uint64_t *a_empty = a_full + p.stages;
     uint64_t *b_full = a_empty + p.stages;
@@ -249,11 +313,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (u >= p.n_units) break;
                 const int64_t t = u % p.n_qtiles, b = u / p.n_qtiles;
                 // resident query tile for this unit
-                mbar_wait(b_empty + slot, ph ^ 1);
-                mbar_arrive_expect_tx(b_full + slot, b_bytes);
-                unsigned char *dstB = sB + (size_t)slot * b_bytes;
+                const int bslot = it % bslots;
+                const uint32_t bph = (uint32_t)(it / bslots) & 1;
+                mbar_wait(b_empty + bslot, bph ^ 1);
+                mbar_arrive_expect_tx(b_full + bslot, b_bytes);
+                unsigned char *dstB = sB + (size_t)bslot * b_bytes;
                 for (int c = 0; c < p.kchunks; ++c)
-                    tma_load_2d(dstB + (size_t)c * N * SW, &tm_q, b_full + slot, c * SW,
+                    tma_load_2d(dstB + (size_t)c * N * SW, &tm_q, b_full + bslot, c * SW,
                                 (int32_t)(t * N));
                 // streamed database tiles
                 const int64_t tile0 = b * p.tiles_per_unit;
@@ -290,8 +356,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t b = u / p.n_qtiles;
             const int64_t tile0 = b * p.tiles_per_unit;
             const int64_t tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
-            mbar_wait(b_full + slot, ph);
-            const uint32_t bbase = smem_u32(sB + (size_t)slot * b_bytes);
+            const int bslot = it % bslots;
+            mbar_wait(b_full + bslot, (uint32_t)(it / bslots) & 1);
+            const uint32_t bbase = smem_u32(sB + (size_t)bslot * b_bytes);
             for (int64_t tile = tile0; tile < tile1; ++tile) {
                 mbar_wait(acc_empty + acc, accph ^ 1);
                 tc_fence_after();
@@ -324,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             if (lane == 0) {
-                tc_commit(b_empty + slot);
+                tc_commit(b_empty + bslot);
                 mbar_arrive(unit_empty + slot);
             }
             __syncwarp();
@@ -360,49 +427,140 @@ __global__ void __launch_bounds__(kThreads, 1)
             epi_barrier();
             const int64_t tile0 = b * p.tiles_per_unit;
             const int64_t tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
+            const int col_half = half * (N / 2);   // first column of this warp
+            const uint32_t thr_addr = smem_u32(thr_s);
+            // per-warp column bounds (IP uses the thresholds directly)
+            const uint32_t bnd_addr = (M == kIP) ? thr_addr + 4u * (uint32_t)col_half
+                                                 : smem_u32(bnd_s + ew * (N / 2));
+            const uint32_t vrow_addr = smem_u32(vst_s + (ew * 32 + lane) * kVRow);
+            // chunks of 32 columns this warp actually has queries for
+            const int nch = max(0, min(N / 64, (nqt - col_half + 31) / 32));
             for (int64_t tile = tile0; tile < tile1; ++tile) {
                 const int64_t row = a.r_lo + tile * kBlockM + quarter * 32 + lane;
                 const bool valid = row < a.r_hi;
                 int32_t xx = 0;
-                float inv_xn = 0.f;
+                float xn = 1.f, inv_xn = 0.f;
                 if (valid) {
                     if constexpr (M == kL2) xx = __ldg(a.db_sqnorm + row);
-                    if constexpr (M == kAngular) inv_xn = __frcp_rn(__ldg(a.db_norm + row));
+                    if constexpr (M == kAngular) {
+                        xn = __ldg(a.db_norm + row);
+                        inv_xn = __frcp_rn(xn);
+                    }
+                }
+                if (a.mode == 0 && M != kIP) {
+                    // Necessary integer condition per (warp rows, column):
+                    //   L2:      xx_i - 2 dot <= T  =>  dot >= ceil((min xx - T) / 2)
+                    //   angular: dot / xn_i >= P    =>  dot >= ceil(P * (P >= 0 ? min xn
+                    //                                                          : max xn))
+                    // (float*float is exact in double).  Rows sorted by norm at
+                    // index build make the warp's norm range, hence the bound,
+                    // tight; the exact per-row test runs on the rare survivors.
+                    if constexpr (M == kL2) {
+                        const int32_t xmin = warp_reduce(valid ? xx : INT32_MAX,
+                                                         [](int32_t x, int32_t y) { return min(x, y); });
+#pragma unroll
+                        for (int i = 0; i < N / 64; ++i) {
+                            const int c = i * 32 + lane;
+                            const int32_t T = lds32(thr_addr + 4u * (uint32_t)(col_half + c));
+                            const long long num = (long long)xmin - (long long)T;
+                            sts32(bnd_addr + 4u * (uint32_t)c, clamp_i64((num + 1) >> 1));
+                        }
+                    } else {
+                        const float nmin = warp_reduce(valid ? xn : INFINITY,
+                                                       [](float x, float y) { return fminf(x, y); });
+                        const float nmax = warp_reduce(valid ? xn : -INFINITY,
+                                                       [](float x, float y) { return fmaxf(x, y); });
+#pragma unroll
+                        for (int i = 0; i < N / 64; ++i) {
+                            const int c = i * 32 + lane;
+                            const float P = __int_as_float(lds32(thr_addr + 4u * (uint32_t)(col_half + c)));
+                            int32_t B;
+                            if (P != P || nmin == INFINITY) {
+                                B = INT32_MAX;  // padded column or no valid row
+                            } else {
+                                const double b = (double)P * (double)(P >= 0.f ? nmin : nmax);
+                                B = b > 2147483647.0 ? INT32_MAX
+                                                     : (b < -2147483648.0 ? INT32_MIN
+                                                                          : (int32_t)ceil(b));
+                            }
+                            sts32(bnd_addr + 4u * (uint32_t)c, B);
+                        }
+                    }
+                    __syncwarp();
                 }
                 mbar_wait(acc_full + acc, accph);
                 tc_fence_after();
-                const uint32_t tbase =
-                    tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * N);
-#pragma unroll 1
-                for (int c0 = half * (N / 2); c0 < (half + 1) * (N / 2) && c0 < nqt; c0 += 32) {
-                    int32_t v[32];
-                    tmem_ld32(tbase + (uint32_t)c0, v);
-                    if (a.mode == 0) {
+                const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) +
+                                       (uint32_t)(acc * N) + (uint32_t)col_half;
+                if (a.mode == 0) {
+                    int32_t va[32], vb[32];
+                    if (nch > 0) {
+                        tmem_ld32_async(tbase, va);
+                        tmem_wait();
+                    }
+#pragma unroll
+                    for (int ci = 0; ci < N / 64; ++ci) {
+                        if (ci >= nch) break;
+                        int32_t(&cur)[32] = (ci & 1) ? vb : va;
+                        int32_t(&nxt)[32] = (ci & 1) ? va : vb;
+                        if (ci + 1 < nch) tmem_ld32_async(tbase + (uint32_t)((ci + 1) * 32), nxt);
+                        // fast path: one integer compare per (row, query)
                         bool any = false;
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            any |= passes<M>(v[j], thr_s[c0 + j], xx, inv_xn);
+                        for (int g = 0; g < 8; ++g) {
+                            const int4 bb = lds128(bnd_addr + 4u * (uint32_t)(ci * 32 + 4 * g));
+                            any |= (cur[4 * g + 0] >= bb.x) | (cur[4 * g + 1] >= bb.y) |
+                                   (cur[4 * g + 2] >= bb.z) | (cur[4 * g + 3] >= bb.w);
+                        }
                         if (any && valid) {
-                            for (int j = 0; j < 32; ++j) {
-                                if (!passes<M>(v[j], thr_s[c0 + j], xx, inv_xn)) continue;
-                                const int qloc = c0 + j;
-                                int e = atomicAdd(stage_n, 1);
+                            // slow path (lanes with a candidate only): column mask,
+                            // values parked in this lane's smem row (no dynamic
+                            // register indexing), exact test per set bit.
+                            uint32_t mask = 0;
+#pragma unroll
+                            for (int g = 0; g < 8; ++g) {
+                                const int4 bb = lds128(bnd_addr + 4u * (uint32_t)(ci * 32 + 4 * g));
+                                mask |= ((uint32_t)(cur[4 * g + 0] >= bb.x) << (4 * g + 0)) |
+                                        ((uint32_t)(cur[4 * g + 1] >= bb.y) << (4 * g + 1)) |
+                                        ((uint32_t)(cur[4 * g + 2] >= bb.z) << (4 * g + 2)) |
+                                        ((uint32_t)(cur[4 * g + 3] >= bb.w) << (4 * g + 3));
+                                sts128(vrow_addr + 16u * (uint32_t)g, cur[4 * g], cur[4 * g + 1],
+                                       cur[4 * g + 2], cur[4 * g + 3]);
+                            }
+                            while (mask) {
+                                const int j = __ffs(mask) - 1;
+                                mask &= mask - 1;
+                                const int32_t v = lds32(vrow_addr + 4u * (uint32_t)j);
+                                const int qloc = col_half + ci * 32 + j;
+                                if constexpr (M != kIP) {
+                                    const int32_t T = lds32(thr_addr + 4u * (uint32_t)qloc);
+                                    if (!passes<M>(v, T, xx, inv_xn)) continue;
+                                }
+                                const int e = atomicAdd(stage_n, 1);
                                 if (e < kStageCap) {
-                                    int sq = atomicAdd(qcnt + qloc, 1);
-                                    stage_buf[e] = Staged{qloc, sq, (int32_t)row, v[j]};
+                                    const int sq = atomicAdd(qcnt + qloc, 1);
+                                    stage_buf[e] = Staged{qloc, sq, (int32_t)row, v};
                                 } else {
                                     // staging full: direct append (slow, rare)
-                                    int32_t s = atomicAdd(a.ccount + q0 + qloc, 1);
+                                    const int32_t s = atomicAdd(a.ccount + q0 + qloc, 1);
                                     if (s < a.cap)
-                                        a.cand[(q0 + qloc) * a.cap + s] = Cand{(int32_t)row, v[j]};
+                                        a.cand[(q0 + qloc) * a.cap + s] = Cand{(int32_t)row, v};
                                 }
                             }
                         }
-                    } else if (valid) {
-#pragma unroll 4
+                        if (ci + 1 < nch) tmem_wait();
+                    }
+                } else {
+#pragma unroll 1
+                    for (int ci = 0; ci < nch; ++ci) {
+                        int32_t v[32];
+                        tmem_ld32(tbase + (uint32_t)(ci * 32), v);
+                        if (!valid) continue;
+#pragma unroll
                         for (int j = 0; j < 32; ++j) {
-                            if (c0 + j >= nqt) break;
-                            const int64_t q = q0 + c0 + j;
+                            const int c = col_half + ci * 32 + j;
+                            if (c >= nqt) continue;
+                            const int64_t q = q0 + c;
                             if (a.mode == 1)
                                 a.cand[q * a.cap + (row - a.r_lo)] = Cand{(int32_t)row, v[j]};
                             else
@@ -499,15 +657,18 @@ cudaError_t launch_t(const FilterArgs &a, int *sched, cudaStream_t st) {
     p.tiles_per_unit = tpu;
     p.n_units = ((p.n_tiles + tpu - 1) / tpu) * p.n_qtiles;
     p.sched = sched;
-    const size_t fixed = 1024 /*align slack*/ + 2 * (size_t)N * a.kdim +
-                         kStageCap * sizeof(Staged) + 3 * N * sizeof(int32_t) + 256;
+    p.b_slots = (2 * (size_t)N * a.kdim <= 65536) ? 2 : 1;
+    const size_t fixed = 1024 /*align slack*/ + (size_t)p.b_slots * N * a.kdim +
+                         kStageCap * sizeof(Staged) + 7 * N * sizeof(int32_t) +
+                         8 * 32 * kVRow * sizeof(int32_t) + 256;
     const size_t budget = 227 * 1024;
     const size_t stage_bytes = (size_t)kBlockM * SW;
-    if (fixed + 2 * stage_bytes > budget) return cudaErrorNotSupported;
-    int stages = (int)((budget - fixed) / stage_bytes);
+    // each stage also costs two 8-byte mbarriers
+    if (fixed + 2 * (stage_bytes + 16) > budget) return cudaErrorNotSupported;
+    int stages = (int)((budget - fixed) / (stage_bytes + 16));
     if (stages > 8) stages = 8;
     p.stages = stages;
-    const size_t smem = fixed + (size_t)stages * stage_bytes + (size_t)(2 * stages) * 8;
+    const size_t smem = fixed + (size_t)stages * (stage_bytes + 16);
     cudaError_t e = cudaFuncSetAttribute(filter_tc_kernel<SW, N, M>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

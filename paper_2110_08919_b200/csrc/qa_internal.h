@@ -66,6 +66,7 @@ struct SelectArgs {
     const float *db_norm;
     const int32_t *q_sqnorm;
     const float *q_norm;
+    const int32_t *row_ids;  // stored row -> reported id (NULL: identity)
     int32_t *thr;        // out: next-round threshold
     int32_t *overflow;   // [nq] sticky per-query flag: candidate list overflowed
     int32_t *any_overflow;
@@ -75,11 +76,15 @@ cudaError_t launch_select(const SelectArgs &a, cudaStream_t st);
 cudaError_t launch_init_state(int32_t *state_cnt, int32_t *thr, int64_t nq, int metric,
                               cudaStream_t st);
 cudaError_t launch_fill(int32_t *p, int64_t n, int32_t v, cudaStream_t st);
-cudaError_t launch_finalize(const Entry *state, const int32_t *state_cnt, int64_t nq, int64_t k,
-                            int64_t keff, int metric, const int32_t *db_sqnorm,
-                            const float *db_norm, const int32_t *q_sqnorm, const float *q_norm,
+cudaError_t launch_finalize(const Entry *state, int64_t nq, int64_t k, int64_t keff, int metric,
                             int64_t id_offset, double *out_scores, int32_t *out_ids,
                             cudaStream_t st);
+// stable ascending order of rows by int32 key (CUB radix sort); perm[i] = row
+cudaError_t launch_order_by_key(const int32_t *key, int64_t n, int32_t *perm, void *scratch,
+                                size_t scratch_bytes, size_t *needed, cudaStream_t st);
+cudaError_t launch_permute_rows(const int8_t *src, const int32_t *sq_in, const float *n_in,
+                                int64_t n, int64_t ld, const int32_t *perm, int8_t *dst,
+                                int32_t *sq_out, float *n_out, cudaStream_t st);
 cudaError_t launch_merge(const double *in_scores, const int32_t *in_ids, int64_t G, int64_t nq,
                          int64_t kin, int64_t k, double *out_scores, int32_t *out_ids,
                          cudaStream_t st);

@@ -1,0 +1,112 @@
+// qa_layout.cu -- index layout: rows ordered by code norm.
+//
+// The filter epilogue derives one integer bound per (warp of 32 rows,
+// query) from the smallest / largest norm among those rows (qa_filter_tc.cu).
+// Storing the index rows in ascending-norm order makes every warp's norm
+// range narrow, so the bound is nearly the exact per-row test.  The order is
+// a stable radix sort on the int32 squared norm (CUB, part of the CUDA
+// toolkit); reported ids stay the caller's row positions through the
+// row_ids map passed to the scan.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "qa_internal.h"
+
+namespace qa {
+
+namespace {
+
+// Tile interleave: stored tile t <- sorted tile (t * step) mod T (step
+// coprime to T), so every prefix of stored rows samples the whole norm range
+// -- the search rounds scan row prefixes and need representative samples --
+// while each 128-row tile still holds rows of nearly equal norm.  A partial
+// last tile stays last.
+__global__ void interleave_tiles_kernel(const int32_t *__restrict__ sorted, int64_t n,
+                                        int64_t tile, int64_t full_tiles, int64_t step,
+                                        int32_t *__restrict__ perm) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t t = i / tile;
+    const int64_t src_t = t < full_tiles ? (t * step) % full_tiles : t;
+    perm[i] = sorted[src_t * tile + (i - t * tile)];
+}
+
+__global__ void iota_kernel(int32_t *p, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = (int32_t)i;
+}
+
+// one warp per destination row, 16-byte vector copies (ld is a multiple of 32)
+__global__ void permute_rows_kernel(const int8_t *__restrict__ src, const int32_t *__restrict__ sq_in,
+                                    const float *__restrict__ n_in, int64_t n, int64_t ld,
+                                    const int32_t *__restrict__ perm, int8_t *__restrict__ dst,
+                                    int32_t *__restrict__ sq_out, float *__restrict__ n_out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < n; r += nwarps) {
+        const int64_t s = perm[r];
+        const int4 *sp = reinterpret_cast<const int4 *>(src + s * ld);
+        int4 *dp = reinterpret_cast<int4 *>(dst + r * ld);
+        for (int64_t j = lane; j < ld / 16; j += 32) dp[j] = __ldg(sp + j);
+        if (lane == 0) {
+            if (sq_out) sq_out[r] = sq_in[s];
+            if (n_out) n_out[r] = n_in[s];
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_order_by_key(const int32_t *key, int64_t n, int32_t *perm, void *scratch,
+                                size_t scratch_bytes, size_t *needed, cudaStream_t st) {
+    // layout of scratch: [keys_out n*4][vals_in n*4][cub temp]
+    size_t temp = 0;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, temp, (const uint32_t *)nullptr,
+                                                    (uint32_t *)nullptr, (const int32_t *)nullptr,
+                                                    (int32_t *)nullptr, (int)n, 0, 32, st);
+    if (e != cudaSuccess) return e;
+    const size_t off = ((size_t)n * 12 + 255) / 256 * 256;
+    *needed = off + temp;
+    if (!scratch || scratch_bytes < *needed) return cudaSuccess;  // size query
+    uint32_t *keys_out = (uint32_t *)scratch;
+    int32_t *vals_in = (int32_t *)((char *)scratch + (size_t)n * 4);
+    int32_t *sorted = (int32_t *)((char *)scratch + (size_t)n * 8);
+    iota_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(vals_in, n);
+    // squared norms are >= 0, so their uint32 order is their int32 order
+    e = cub::DeviceRadixSort::SortPairs((char *)scratch + off, temp, (const uint32_t *)key,
+                                        keys_out, vals_in, sorted, (int)n, 0, 32, st);
+    if (e != cudaSuccess) return e;
+    const int64_t tile = 128, full = n / tile;
+    int64_t step = 1;
+    if (full > 1) {
+        // a step near T/phi, coprime to T: spreads consecutive stored tiles
+        // across the sorted order
+        step = (int64_t)((double)full * 0.6180339887) | 1;
+        auto gcd = [](int64_t x, int64_t y) {
+            while (y) {
+                int64_t t = x % y;
+                x = y;
+                y = t;
+            }
+            return x;
+        };
+        while (gcd(step, full) != 1) step += 2;
+    }
+    interleave_tiles_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sorted, n, tile, full,
+                                                                         step, perm);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_permute_rows(const int8_t *src, const int32_t *sq_in, const float *n_in,
+                                int64_t n, int64_t ld, const int32_t *perm, int8_t *dst,
+                                int32_t *sq_out, float *n_out, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    int64_t blocks = (n + 7) / 8;
+    int64_t cap = (int64_t)num_sms() * 8;
+    if (blocks > cap) blocks = cap;
+    permute_rows_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, sq_in, n_in, n, ld, perm, dst, sq_out,
+                                                          n_out);
+    return cudaGetLastError();
+}
+
+}  // namespace qa

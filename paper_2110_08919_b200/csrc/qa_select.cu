@@ -6,7 +6,14 @@
 // pass only discards rows that provably cannot enter that prefix; this file
 // turns the surviving candidates into the exact prefix: exact float64 scores
 // (angular: one correctly rounded division + subtraction, _core.pyx:96),
-// lexicographic sort, truncation to k, and the next pass's threshold.
+// (score, id) order, truncation to k, and the next pass's threshold.
+//
+// select: one WARP per query.  The retained list T (sorted, <= k entries)
+// lives in shared memory; candidates arrive in chunks of kChunk: they are
+// scored exactly, entries already worse than T's k-th are dropped (warp
+// ballot compaction), the rest are bitonic-sorted in shared memory and
+// merged into T by merge path (each element's output rank = its own index +
+// a binary-search count in the other list).
 #include <cfloat>
 
 #include "qa_common.cuh"
@@ -16,17 +23,45 @@ namespace qa {
 
 namespace {
 
+constexpr int kChunk = 256;  // candidates sorted per merge step
+constexpr int kWarpsMax = 8;
+
+__device__ __forceinline__ int next_pow2(int v) {
+    int p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+template <typename T, typename Less>
+__device__ void warp_bitonic_sort(T *buf, int P, Less less) {
+    const int lane = threadIdx.x & 31;
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = lane; t < (P >> 1); t += 32) {
+                const int i = 2 * t - (t & (stride - 1));
+                const int j = i + stride;
+                const bool up = ((i & size) == 0);
+                T a = buf[i], b = buf[j];
+                if (up ? less(b, a) : less(a, b)) {
+                    buf[i] = b;
+                    buf[j] = a;
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
 template <typename T, typename Less>
 __device__ void block_bitonic_sort(T *buf, int P, Less less) {
     for (int size = 2; size <= P; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
             for (int t = threadIdx.x; t < (P >> 1); t += blockDim.x) {
-                int i = 2 * t - (t & (stride - 1));
-                int j = i + stride;
-                bool up = ((i & size) == 0);
+                const int i = 2 * t - (t & (stride - 1));
+                const int j = i + stride;
+                const bool up = ((i & size) == 0);
                 T a = buf[i], b = buf[j];
-                bool swap = up ? less(b, a) : less(a, b);
-                if (swap) {
+                if (up ? less(b, a) : less(a, b)) {
                     buf[i] = b;
                     buf[j] = a;
                 }
@@ -36,23 +71,31 @@ __device__ void block_bitonic_sort(T *buf, int P, Less less) {
     }
 }
 
-__device__ __forceinline__ int next_pow2(int v) {
-    int p = 1;
-    while (p < v) p <<= 1;
-    return p;
-}
-
 struct EntryLess {
     __device__ bool operator()(const Entry &a, const Entry &b) const { return entry_less(a, b); }
 };
 
+// number of entries of sorted list L[0, len) strictly less than x
+__device__ __forceinline__ int count_less(const Entry *L, int len, const Entry &x) {
+    int lo = 0, hi = len;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (entry_less(L[mid], x))
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
 template <int M>
 __device__ __forceinline__ Entry make_entry(Cand c, int32_t qq, float qn,
                                             const int32_t *__restrict__ db_sqnorm,
-                                            const float *__restrict__ db_norm) {
+                                            const float *__restrict__ db_norm,
+                                            const int32_t *__restrict__ row_ids) {
     Entry e;
     e.row = c.row;
-    e.dot = c.dot;
+    e.id = row_ids ? __ldg(row_ids + c.row) : c.row;
     if constexpr (M == kIP) {
         e.skey = skey_from_int((int32_t)(0u - (uint32_t)c.dot));
     } else if constexpr (M == kL2) {
@@ -64,35 +107,38 @@ __device__ __forceinline__ Entry make_entry(Cand c, int32_t qq, float qn,
     return e;
 }
 
+// Next-pass threshold from the k-th retained entry (see qa_common.cuh).
 template <int M>
-__device__ __forceinline__ int32_t threshold_of(const Entry &e, int32_t qq,
-                                                const float *__restrict__ db_norm) {
+__device__ __forceinline__ int32_t threshold_of(const Entry &e, int32_t qq, float qn) {
     if constexpr (M == kIP) {
-        return e.dot;  // candidate iff dot >= dot_k (ties may win on id)
+        return (int32_t)(0u - (uint32_t)int_from_skey(e.skey));  // dot_k; ties may win on id
     } else if constexpr (M == kL2) {
-        int32_t s = (int32_t)((uint32_t)(e.skey & 0xffffffffull) ^ 0x80000000u);
-        return (int32_t)((uint32_t)s - (uint32_t)qq);  // xx - 2dot <= l2_k - qq
+        return (int32_t)((uint32_t)int_from_skey(e.skey) - (uint32_t)qq);  // l2_k - qq
     } else {
-        // c_k = dot_k / xn_k; the float proxy float(dot)*rcp(xn) is within
-        // 3 * 2^-24 relative of dot/xn, and rows that tie the k-th score
-        // after float64 rounding differ from c_k by < 2^-51 relative; a
-        // 2^-20 relative band (plus an absolute 2^-40) covers both.
-        double c = __ddiv_rn((double)e.dot, (double)__ldg(db_norm + e.row));
-        double p = c - fabs(c) * 0x1p-20 - 0x1p-40;
+        // Rows with score <= score_k have c = dot/xn >= qn*(1 - score_k) - qn*2^-50
+        // (two float64 roundings).  The float proxy float(dot)*rcp(xn) is
+        // within 3*2^-24 relative of c; a 2^-20 relative band plus qn*2^-40
+        // absolute covers both, so no such row is ever filtered out.
+        const double c = (1.0 - double_from_skey(e.skey)) * (double)qn;
+        const double p = c - fabs(c) * 0x1p-20 - (double)qn * 0x1p-40;
         return __float_as_int(__double2float_rd(p));
     }
 }
 
 template <int M>
-__global__ void __launch_bounds__(256) select_kernel(SelectArgs a, int sz) {
+__global__ void __launch_bounds__(kWarpsMax * 32) select_kernel(SelectArgs a, int kpad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    Entry *buf = reinterpret_cast<Entry *>(smem_raw);
-    const int64_t q = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     if (q >= a.nq) return;
-    const int32_t total_cands = a.ccount[q];
-    if (total_cands == 0) return;  // nothing new: state and threshold unchanged
-    const int m = (int)min((int64_t)total_cands, a.cap);
-    if (total_cands > a.cap && threadIdx.x == 0) {
+    const int32_t total = a.ccount[q];
+    if (total == 0) return;  // nothing new: state and threshold unchanged
+    Entry *T = reinterpret_cast<Entry *>(smem_raw) + (size_t)warp * (2 * kpad + kChunk);
+    Entry *O = T + kpad;
+    Entry *S = O + kpad;
+    const int k = (int)a.k;
+    const int m = (int)min((int64_t)total, a.cap);
+    if (total > a.cap && lane == 0) {
         a.overflow[q] = 1;
         atomicExch(a.any_overflow, 1);
     }
@@ -101,28 +147,56 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs a, int sz) {
     Entry *st = a.state + q * a.k;
     const Cand *cd = a.cand + q * a.cap;
     int cur = a.state_cnt[q];
-    for (int i = threadIdx.x; i < cur; i += blockDim.x) buf[i] = st[i];
-    int pos = 0;
-    while (pos < m) {
-        const int take = min(m - pos, sz - cur);
-        for (int i = threadIdx.x; i < take; i += blockDim.x)
-            buf[cur + i] = make_entry<M>(cd[pos + i], qq, qn, a.db_sqnorm, a.db_norm);
-        const int tot = cur + take;
-        const int P = next_pow2(tot);
-        for (int i = tot + threadIdx.x; i < P; i += blockDim.x) {
-            buf[i].skey = ~0ull;
-            buf[i].row = INT32_MAX;
-            buf[i].dot = 0;
+    for (int i = lane; i < cur; i += 32) T[i] = st[i];
+    __syncwarp();
+    for (int pos = 0; pos < m; pos += kChunk) {
+        const int take = min(kChunk, m - pos);
+        // score the chunk; drop entries that cannot beat the current k-th
+        const bool full = (cur == k);
+        Entry kth;
+        if (full) kth = T[k - 1];
+        int ns = 0;
+        for (int base = 0; base < take; base += 32) {
+            const int i = base + lane;
+            Entry e;
+            bool keep = false;
+            if (i < take) {
+                e = make_entry<M>(cd[pos + i], qq, qn, a.db_sqnorm, a.db_norm, a.row_ids);
+                keep = !full || entry_less(e, kth);
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) S[ns + __popc(bal & ((1u << lane) - 1))] = e;
+            ns += __popc(bal);
         }
-        __syncthreads();
-        block_bitonic_sort(buf, P, EntryLess());
-        cur = (int)min((int64_t)tot, a.k);
-        pos += take;
+        if (ns == 0) continue;
+        const int P = next_pow2(max(ns, 2));
+        for (int i = ns + lane; i < P; i += 32) {
+            S[i].skey = ~0ull;
+            S[i].id = INT32_MAX;
+            S[i].row = -1;
+        }
+        __syncwarp();
+        warp_bitonic_sort(S, P, EntryLess());
+        // merge T[0, cur) and S[0, ns) -> O[0, newcur)
+        const int newcur = min(k, cur + ns);
+        for (int i = lane; i < cur; i += 32) {
+            const int r = i + count_less(S, ns, T[i]);
+            if (r < newcur) O[r] = T[i];
+        }
+        for (int i = lane; i < ns; i += 32) {
+            const int r = i + count_less(T, cur, S[i]);
+            if (r < newcur) O[r] = S[i];
+        }
+        __syncwarp();
+        Entry *tmp = T;
+        T = O;
+        O = tmp;
+        cur = newcur;
     }
-    for (int i = threadIdx.x; i < cur; i += blockDim.x) st[i] = buf[i];
-    if (threadIdx.x == 0) {
+    for (int i = lane; i < cur; i += 32) st[i] = T[i];
+    if (lane == 0) {
         a.state_cnt[q] = cur;
-        if (cur == a.k) a.thr[q] = threshold_of<M>(buf[cur - 1], qq, a.db_norm);
+        if (cur == k) a.thr[q] = threshold_of<M>(T[k - 1], qq, qn);
     }
 }
 
@@ -142,26 +216,23 @@ __global__ void init_state_kernel(int32_t *state_cnt, int32_t *thr, int64_t nq,
 
 template <int M>
 __global__ void finalize_kernel(const Entry *__restrict__ state, int64_t nq, int64_t k,
-                                int64_t keff, const int32_t *__restrict__ db_sqnorm,
-                                const float *__restrict__ db_norm,
-                                const int32_t *__restrict__ q_sqnorm,
-                                const float *__restrict__ q_norm, int64_t id_offset,
-                                double *__restrict__ out_scores, int32_t *__restrict__ out_ids) {
+                                int64_t keff, int64_t id_offset, double *__restrict__ out_scores,
+                                int32_t *__restrict__ out_ids) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nq * keff) return;
     int64_t q = t / keff, j = t - q * keff;
     Entry e = state[q * k + j];
     double s;
     if constexpr (M == kIP) {
-        s = -(double)e.dot;  // dot == 0 gives -0.0, exactly as _core.pyx:95
+        const int32_t v = int_from_skey(e.skey);  // = -dot
+        s = v == 0 ? -0.0 : (double)v;            // -(double)0 is -0.0 in _core.pyx:95
     } else if constexpr (M == kL2) {
-        uint32_t v = (uint32_t)q_sqnorm[q] + (uint32_t)db_sqnorm[e.row] - 2u * (uint32_t)e.dot;
-        s = (double)(int32_t)v;
+        s = (double)int_from_skey(e.skey);
     } else {
-        s = angular_score(e.dot, q_norm[q], db_norm[e.row]);
+        s = double_from_skey(e.skey);
     }
     out_scores[t] = s;
-    out_ids[t] = (int32_t)(e.row + id_offset);
+    out_ids[t] = (int32_t)(e.id + id_offset);
 }
 
 struct MEntry {
@@ -224,33 +295,30 @@ int pow2_at_least(int64_t v, int64_t cap) {
     return (int)p;
 }
 
+template <int M>
+cudaError_t launch_select_t(const SelectArgs &a, cudaStream_t st) {
+    const int kpad = (int)((a.k + 31) / 32 * 32);
+    const size_t per_warp = (size_t)(2 * kpad + kChunk) * sizeof(Entry);
+    int warps = (int)std::min<size_t>(kWarpsMax, (160 * 1024) / per_warp);
+    if (warps < 1) warps = 1;
+    const size_t smem = per_warp * warps;
+    cudaError_t e = cudaFuncSetAttribute(select_kernel<M>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const unsigned grid = (unsigned)((a.nq + warps - 1) / warps);
+    select_kernel<M><<<grid, warps * 32, smem, st>>>(a, kpad);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t launch_select(const SelectArgs &a, cudaStream_t st) {
     if (a.nq == 0) return cudaSuccess;
-    const int sz = pow2_at_least(a.k + a.cap, kSortMax);
-    const size_t smem = (size_t)sz * sizeof(Entry);
-    cudaError_t e = cudaSuccess;
     switch (a.metric) {
-        case kIP:
-            e = cudaFuncSetAttribute(select_kernel<kIP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem);
-            if (e == cudaSuccess) select_kernel<kIP><<<(unsigned)a.nq, 256, smem, st>>>(a, sz);
-            break;
-        case kL2:
-            e = cudaFuncSetAttribute(select_kernel<kL2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem);
-            if (e == cudaSuccess) select_kernel<kL2><<<(unsigned)a.nq, 256, smem, st>>>(a, sz);
-            break;
-        default:
-            e = cudaFuncSetAttribute(select_kernel<kAngular>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e == cudaSuccess)
-                select_kernel<kAngular><<<(unsigned)a.nq, 256, smem, st>>>(a, sz);
-            break;
+        case kIP: return launch_select_t<kIP>(a, st);
+        case kL2: return launch_select_t<kL2>(a, st);
+        default: return launch_select_t<kAngular>(a, st);
     }
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
 }
 
 cudaError_t launch_fill(int32_t *p, int64_t n, int32_t v, cudaStream_t st) {
@@ -268,29 +336,23 @@ cudaError_t launch_init_state(int32_t *state_cnt, int32_t *thr, int64_t nq, int 
     return cudaGetLastError();
 }
 
-cudaError_t launch_finalize(const Entry *state, const int32_t *state_cnt, int64_t nq, int64_t k,
-                            int64_t keff, int metric, const int32_t *db_sqnorm,
-                            const float *db_norm, const int32_t *q_sqnorm, const float *q_norm,
+cudaError_t launch_finalize(const Entry *state, int64_t nq, int64_t k, int64_t keff, int metric,
                             int64_t id_offset, double *out_scores, int32_t *out_ids,
                             cudaStream_t st) {
-    (void)state_cnt;
     int64_t total = nq * keff;
     if (total == 0) return cudaSuccess;
     unsigned grid = (unsigned)((total + 255) / 256);
     switch (metric) {
         case kIP:
-            finalize_kernel<kIP><<<grid, 256, 0, st>>>(state, nq, k, keff, db_sqnorm, db_norm,
-                                                       q_sqnorm, q_norm, id_offset, out_scores,
+            finalize_kernel<kIP><<<grid, 256, 0, st>>>(state, nq, k, keff, id_offset, out_scores,
                                                        out_ids);
             break;
         case kL2:
-            finalize_kernel<kL2><<<grid, 256, 0, st>>>(state, nq, k, keff, db_sqnorm, db_norm,
-                                                       q_sqnorm, q_norm, id_offset, out_scores,
+            finalize_kernel<kL2><<<grid, 256, 0, st>>>(state, nq, k, keff, id_offset, out_scores,
                                                        out_ids);
             break;
         default:
-            finalize_kernel<kAngular><<<grid, 256, 0, st>>>(state, nq, k, keff, db_sqnorm,
-                                                            db_norm, q_sqnorm, q_norm, id_offset,
+            finalize_kernel<kAngular><<<grid, 256, 0, st>>>(state, nq, k, keff, id_offset,
                                                             out_scores, out_ids);
     }
     return cudaGetLastError();

@@ -46,6 +46,7 @@ class DeviceCodes:
     d: int
     sqnorm: torch.Tensor   # int32 [n]
     norm: torch.Tensor     # float32 [n]
+    ids: torch.Tensor | None = None  # int32 [n]: stored row -> reported id (None: identity)
 
     @property
     def n(self) -> int:
@@ -93,7 +94,21 @@ class DeviceCodes:
         return self.codes[:, : self.d].cpu().numpy()
 
     def slice_rows(self, lo: int, hi: int) -> "DeviceCodes":
-        return DeviceCodes(self.codes[lo:hi], self.d, self.sqnorm[lo:hi], self.norm[lo:hi])
+        ids = None if self.ids is None else self.ids[lo:hi]
+        return DeviceCodes(self.codes[lo:hi], self.d, self.sqnorm[lo:hi], self.norm[lo:hi], ids)
+
+    def sorted_by_norm(self) -> "DeviceCodes":
+        """Copy with rows in ascending-norm order (stable) and ``ids`` mapping
+        each stored row back to its position in this matrix.  The scan's
+        per-warp bounds are tight on such a layout (qa_layout.cu)."""
+        perm = torch.empty((self.n,), dtype=torch.int32, device=self.device)
+        check(lib.qa_order_rows_by_norm(_p(self.sqnorm), self.n, _p(perm), _stream()))
+        out = DeviceCodes.empty(self.n, self.d, self.device)
+        check(lib.qa_permute_rows_i8(_p(self.codes), _p(self.sqnorm), _p(self.norm), self.n,
+                                     self.ld, _p(perm), _p(out.codes), _p(out.sqnorm),
+                                     _p(out.norm), _stream()))
+        out.ids = perm if self.ids is None else self.ids[perm.long()]
+        return out
 
 
 def norms_(dc: DeviceCodes) -> None:
@@ -155,7 +170,7 @@ def scan_topk(db: DeviceCodes, q: DeviceCodes, k: int, metric: int, db_norm=None
     dn = db.norm if db_norm is None else db_norm
     qn = q.norm if q_norm is None else q_norm
     check(lib.qa_scan_topk_i8(_p(db.codes), db.n, db.d, db.ld, _p(db.sqnorm), _p(dn),
-                              _p(q.codes), q.n, q.ld, _p(q.sqnorm), _p(qn), int(k), int(metric),
+                              _p(db.ids), _p(q.codes), q.n, q.ld, _p(q.sqnorm), _p(qn), int(k), int(metric),
                               int(id_offset), _p(scores), _p(ids), _stream()))
     return scores, ids
 

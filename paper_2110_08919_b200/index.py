@@ -40,12 +40,26 @@ class Int8Index:
 
     @classmethod
     def from_params(cls, x: torch.Tensor, params: QuantizerParams, metric: Metric,
-                    id_offset: int = 0) -> "Int8Index":
+                    id_offset: int = 0, sort_rows: bool = True) -> "Int8Index":
+        """Encode ``x`` with ``params``.  For L2 and angular the stored rows
+        are ordered by code norm (ids still report positions in ``x``), which
+        keeps the scan's per-warp filter bounds tight."""
         device = x.device
         k, sb, se = (torch.from_numpy(np.array(a, dtype=np.float32)).to(device)
                      for a in (params.k, params.sb, params.se))
         codes = dev.encode(x, k, sb, se, params.bits)
+        if sort_rows and Metric(metric) != Metric.INNER_PRODUCT:
+            codes = codes.sorted_by_norm()
         return cls(params, Metric(metric), codes, k, sb, se, id_offset)
+
+    def codes_in_input_order(self) -> np.ndarray:
+        """int8 codes [n, d] in the order of the encoded input rows."""
+        host = self.codes.to_host()
+        if self.codes.ids is None:
+            return host
+        out = np.empty_like(host)
+        out[self.codes.ids.cpu().numpy()] = host
+        return out
 
     @classmethod
     def build(cls, x: torch.Tensor, metric: Metric, calibration: str = "minmax",

@@ -236,7 +236,7 @@ def test_cfg_minis_golden(golden_cfg, cfg):
     np.testing.assert_array_equal(index.params.k, g["k"])
     np.testing.assert_array_equal(index.params.sb, g["sb"])
     np.testing.assert_array_equal(index.params.se, g["se"])
-    assert hashlib.sha256(index.codes.to_host().tobytes()).digest() == g["codes_sha"].tobytes()
+    assert hashlib.sha256(index.codes_in_input_order().tobytes()).digest() == g["codes_sha"].tobytes()
     qc = index.encode_queries(torch.from_numpy(Q).cuda())
     np.testing.assert_array_equal(qc.to_host(), g["qcodes"])
     sc, ids = index.search_codes(qc, 100)
@@ -257,7 +257,7 @@ def test_cfg0_full_parity(oracle):
     np.testing.assert_array_equal(index.params.se, se)
     Xc = oracle.encode(X, k, sb, se, 8)
     Qc = oracle.encode(Q, k, sb, se, 8)
-    np.testing.assert_array_equal(index.codes.to_host(), Xc)
+    np.testing.assert_array_equal(index.codes_in_input_order(), Xc)
     sc, ids = index.search(torch.from_numpy(Q).cuda(), 100)
     osc, oids = _scan_oracle(oracle, Xc, Qc, 100, 1)
     np.testing.assert_array_equal(ids.cpu().numpy(), oids)
@@ -288,3 +288,29 @@ def test_virtual_shards_merge_equals_full(oracle, G):
         osc, oids = _scan_oracle(oracle, X, Q, 100, metric)
         np.testing.assert_array_equal(mi.cpu().numpy(), oids)
         np.testing.assert_array_equal(ms.cpu().numpy(), osc)
+
+
+@pytest.mark.parametrize("metric", [0, 1, 2])
+def test_norm_sorted_index_equals_unsorted(oracle, metric):
+    # The index stores rows sorted by norm (tight per-warp filter bounds) and
+    # reports/tie-breaks by the caller's ids via row_ids: results must be
+    # identical to the unsorted layout and to the oracle.
+    rng = np.random.default_rng(31 + metric)
+    X = _rand_codes(rng, 30_011, 64, -20, 21, nonzero=True)
+    Q = _rand_codes(rng, 300, 64, -20, 21, nonzero=True)
+    db = dev.DeviceCodes.from_host(X)
+    qs = dev.DeviceCodes.from_host(Q)
+    srt = db.sorted_by_norm()
+    ids = srt.ids.cpu().numpy()
+    assert sorted(ids.tolist()) == list(range(X.shape[0]))
+    sq = srt.sqnorm.cpu().numpy()
+    full = (sq.shape[0] // 128) * 128
+    assert (np.diff(sq[:full].reshape(-1, 128), axis=1) >= 0).all()  # sorted within tiles
+    np.testing.assert_array_equal(srt.to_host(), X[ids])
+    a = dev.scan_topk(db, qs, 100, metric)
+    b = dev.scan_topk(srt, qs, 100, metric, id_offset=7)
+    np.testing.assert_array_equal(a[1].cpu().numpy() + 7, b[1].cpu().numpy())
+    np.testing.assert_array_equal(a[0].cpu().numpy(), b[0].cpu().numpy())
+    osc, oids = _scan_oracle(oracle, X, Q, 100, metric)
+    np.testing.assert_array_equal(a[1].cpu().numpy(), oids)
+    np.testing.assert_array_equal(a[0].cpu().numpy(), osc)

@@ -44,28 +44,28 @@ def test_invalid_arguments_map_to_reference_errors():
     L = _lib.lib
     # unknown metric / negative k -> ValueError (_core.pyx:340-347)
     with pytest.raises(ValueError, match="metric"):
-        _lib.check(L.qa_scan_topk_i8(None, 10, 4, 32, None, None, None, 1, 32, None, None, 5, 7,
+        _lib.check(L.qa_scan_topk_i8(None, 10, 4, 32, None, None, None, None, 1, 32, None, None, 5, 7,
                                      0, None, None, None))
     with pytest.raises(ValueError, match="k must be >= 0"):
-        _lib.check(L.qa_scan_topk_i8(None, 10, 4, 32, None, None, None, 1, 32, None, None, -1, 0,
+        _lib.check(L.qa_scan_topk_i8(None, 10, 4, 32, None, None, None, None, 1, 32, None, None, -1, 0,
                                      0, None, None, None))
     with pytest.raises(ValueError, match="angular metric needs data and query norms"):
-        _lib.check(L.qa_scan_topk_i8(None, 10, 4, 32, None, None, None, 1, 32, None, None, 5, 2,
+        _lib.check(L.qa_scan_topk_i8(None, 10, 4, 32, None, None, None, None, 1, 32, None, None, 5, 2,
                                      0, None, None, None))
     with pytest.raises(ValueError, match="stride"):
-        _lib.check(L.qa_scan_topk_i8(None, 10, 4, 16, None, None, None, 1, 32, None, None, 5, 0,
+        _lib.check(L.qa_scan_topk_i8(None, 10, 4, 16, None, None, None, None, 1, 32, None, None, 5, 0,
                                      0, None, None, None))
     with pytest.raises(ValueError, match="bits must be between 1 and 8"):
         _lib.check(L.qa_encode_i8(None, 1, 1, 1, None, None, None, 9, None, 32, None, None, None))
     with pytest.raises(ValueError, match="k exceeds"):
         _lib.check(L.qa_merge_topk(None, None, 2, 1, 3, 7, None, None, None))
     with pytest.raises(NotImplementedError):
-        _lib.check(L.qa_scan_topk_i8(None, 10_000, 8, 32, None, None, None, 1, 32, None, None,
+        _lib.check(L.qa_scan_topk_i8(None, 10_000, 8, 32, None, None, None, None, 1, 32, None, None,
                                      5000, 0, 0, None, None, None))
     # empty problems are valid no-ops (_core.pyx:352-353)
-    _lib.check(L.qa_scan_topk_i8(None, 0, 4, 32, None, None, None, 3, 32, None, None, 5, 0, 0,
+    _lib.check(L.qa_scan_topk_i8(None, 0, 4, 32, None, None, None, None, 3, 32, None, None, 5, 0, 0,
                                  None, None, None))
-    _lib.check(L.qa_scan_topk_i8(None, 10, 4, 32, None, None, None, 0, 32, None, None, 5, 0, 0,
+    _lib.check(L.qa_scan_topk_i8(None, 10, 4, 32, None, None, None, None, 0, 32, None, None, 5, 0, 0,
                                  None, None, None))
 
 
