@@ -118,7 +118,7 @@ struct Buf {
 
 struct Workspace {
     std::mutex mu;
-    Buf state, state_cnt, thr, cand, ccount, ovf, flags, scratch;
+    Buf state, state_cnt, thr, cand, ccount, ovf, flags, scratch, grp;
 };
 
 constexpr int kMaxDevices = 64;
@@ -149,6 +149,7 @@ ScanPlan plan_scan(int64_t n, int64_t nq, int64_t keff, int64_t cap_min) {
     ScanPlan p;
     p.r0 = std::min(n, round_up(std::max<int64_t>(keff, 256), 128));
     p.ratio = nq >= 256 ? 4 : 16;
+    if (const char *v = getenv("QA_B200_RATIO")) p.ratio = std::max(2, atoi(v));
     p.cap = std::max<int64_t>({2048, p.r0, 2 * keff * p.ratio, cap_min});
     const int64_t per_q = p.cap * (int64_t)sizeof(Cand) + keff * (int64_t)sizeof(Entry) + 64;
     const int64_t budget = (int64_t)1 << 30;
@@ -212,6 +213,13 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
     QA_TRY(cudaMemsetAsync(ovf, 0, (size_t)nq * 4, st), "memset");
     QA_TRY(cudaMemsetAsync(flags, 0, 64, st), "memset");
     const bool simt = use_simt_filter(ld);
+    // norm range of every 32-row group (per-warp filter bounds), padded to
+    // whole 128-row tiles
+    const int64_t groups = (n + 127) / 128 * 4;
+    QA_TRY(ws.grp.reserve((size_t)groups * 8), "workspace");
+    int32_t *grp_lo = (int32_t *)ws.grp.ptr, *grp_hi = grp_lo + groups;
+    QA_TRY(launch_group_ranges(metric, db_sqnorm, db_norm, n, grp_lo, grp_hi, groups, st),
+           "group ranges");
 
     for (int64_t c0 = 0; c0 < nq; c0 += qc) {
         const int64_t m = std::min(qc, nq - c0);
@@ -231,6 +239,8 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             fa.r_hi = r_hi;
             fa.db_sqnorm = db_sqnorm;
             fa.db_norm = db_norm;
+            fa.grp_lo = grp_lo;
+            fa.grp_hi = grp_hi;
             fa.thr = thr;
             fa.cand = cand;
             fa.ccount = ccount;

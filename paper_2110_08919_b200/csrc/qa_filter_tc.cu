@@ -35,13 +35,11 @@ namespace qa {
 namespace {
 
 constexpr int kBlockM = 128;
-constexpr int kThreads = 384;
+constexpr int kThreads = 640;
 constexpr int kEpiWarp0 = 4;
-constexpr int kEpiThreads = 256;
+constexpr int kEpiThreads = 512;
 constexpr int kStageCap = 2048;  // survivors staged in smem per work unit
 constexpr int kEpiBarrier = 1;   // named barrier id for the epilogue warps
-constexpr int kVRow = 36;        // words per lane row of slow-path values (32 + pad: no
-                                 // bank conflicts for 16-byte stores)
 
 // ------------------------------------------------------------------ PTX --
 
@@ -134,6 +132,26 @@ __device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, int32_t (&v)[32]
           "=r"(v[31])
         : "r"(taddr)
         : "memory");
+}
+
+// tcgen05.ld of C (16 or 32) consecutive accumulator columns of this warp's
+// 32 TMEM lanes; valid after tmem_wait().
+template <int C>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, int32_t (&v)[C]) {
+    if constexpr (C == 32) {
+        tmem_ld32_async(taddr, v);
+    } else {
+        static_assert(C == 16, "16 or 32 columns");
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32"
+            " {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15},"
+            " [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr)
+            : "memory");
+    }
 }
 
 __device__ __forceinline__ int4 lds128(uint32_t addr) {
@@ -252,8 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int32_t *qcnt = thr_s + N;
     int32_t *qbase = qcnt + N;
     int32_t *bnd_s = qbase + N;  // [8 epilogue warps][N/2] per-warp column bounds
-    int32_t *vst_s = bnd_s + 4 * N;  // [8 warps][32 lanes][kVRow] slow-path value rows
-    uint64_t *bars = (uint64_t *)(vst_s + 8 * 32 * kVRow);
+    uint64_t *bars = (uint64_t *)(bnd_s + 4 * N);
     uint64_t *a_full = bars;
     uint64_t *a_empty = a_full + p.stages;
     uint64_t *b_full = a_empty + p.stages;
@@ -398,9 +415,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= kEpiWarp0) {
         // =============================== epilogue =======================
-        const int ew = warp - kEpiWarp0;          // 0..7
-        const int quarter = warp & 3;             // TMEM lane quarter of this warp
-        const int half = ew >> 2;                 // column half
+        // 16 warps: warp w reads TMEM lane quarter (w % 4) -- its 32 database
+        // rows -- and column block (w - 4) / 4 of kCB = N/4 queries.
+        constexpr int kCB = N / 4;                 // columns per warp
+        constexpr int kC = kCB < 32 ? kCB : 32;    // columns per TMEM load
+        const int ew = warp - kEpiWarp0;           // 0..15
+        const int quarter = warp & 3;
+        const int cblk = ew >> 2;
+        const int col0 = cblk * kCB;               // first column of this warp
         const int etid = threadIdx.x - kEpiWarp0 * 32;
         int acc = 0;
         uint32_t accph = 0;
@@ -427,62 +449,50 @@ __global__ void __launch_bounds__(kThreads, 1)
             epi_barrier();
             const int64_t tile0 = b * p.tiles_per_unit;
             const int64_t tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
-            const int col_half = half * (N / 2);   // first column of this warp
             const uint32_t thr_addr = smem_u32(thr_s);
             // per-warp column bounds (IP uses the thresholds directly)
-            const uint32_t bnd_addr = (M == kIP) ? thr_addr + 4u * (uint32_t)col_half
-                                                 : smem_u32(bnd_s + ew * (N / 2));
-            const uint32_t vrow_addr = smem_u32(vst_s + (ew * 32 + lane) * kVRow);
-            // chunks of 32 columns this warp actually has queries for
-            const int nch = max(0, min(N / 64, (nqt - col_half + 31) / 32));
+            const uint32_t bnd_addr = (M == kIP) ? thr_addr + 4u * (uint32_t)col0
+                                                 : smem_u32(bnd_s + ew * kCB);
+            // column chunks this warp actually has queries for
+            const int nch = max(0, min(kCB / kC, (nqt - col0 + kC - 1) / kC));
             for (int64_t tile = tile0; tile < tile1; ++tile) {
                 const int64_t row = a.r_lo + tile * kBlockM + quarter * 32 + lane;
                 const bool valid = row < a.r_hi;
                 int32_t xx = 0;
-                float xn = 1.f, inv_xn = 0.f;
+                float inv_xn = 0.f;
                 if (valid) {
                     if constexpr (M == kL2) xx = __ldg(a.db_sqnorm + row);
-                    if constexpr (M == kAngular) {
-                        xn = __ldg(a.db_norm + row);
-                        inv_xn = __frcp_rn(xn);
-                    }
+                    if constexpr (M == kAngular) inv_xn = __frcp_rn(__ldg(a.db_norm + row));
                 }
-                if (a.mode == 0 && M != kIP) {
+                if (a.mode == 0 && M != kIP && nch > 0) {
                     // Necessary integer condition per (warp rows, column):
                     //   L2:      xx_i - 2 dot <= T  =>  dot >= ceil((min xx - T) / 2)
                     //   angular: dot / xn_i >= P    =>  dot >= ceil(P * (P >= 0 ? min xn
                     //                                                          : max xn))
-                    // (float*float is exact in double).  Rows sorted by norm at
-                    // index build make the warp's norm range, hence the bound,
+                    // with the product rounded toward -inf (conservative).  The
+                    // norm range of the warp's 32 rows comes precomputed (a
+                    // superset range when rows past r_hi share the group).  Rows
+                    // sorted by norm at index build make it, hence the bound,
                     // tight; the exact per-row test runs on the rare survivors.
+                    const int64_t grp = (a.r_lo + tile * kBlockM + quarter * 32) >> 5;
                     if constexpr (M == kL2) {
-                        const int32_t xmin = warp_reduce(valid ? xx : INT32_MAX,
-                                                         [](int32_t x, int32_t y) { return min(x, y); });
+                        const int32_t xmin = __ldg(a.grp_lo + grp);
 #pragma unroll
-                        for (int i = 0; i < N / 64; ++i) {
-                            const int c = i * 32 + lane;
-                            const int32_t T = lds32(thr_addr + 4u * (uint32_t)(col_half + c));
+                        for (int c = lane; c < kCB; c += 32) {
+                            const int32_t T = lds32(thr_addr + 4u * (uint32_t)(col0 + c));
                             const long long num = (long long)xmin - (long long)T;
                             sts32(bnd_addr + 4u * (uint32_t)c, clamp_i64((num + 1) >> 1));
                         }
                     } else {
-                        const float nmin = warp_reduce(valid ? xn : INFINITY,
-                                                       [](float x, float y) { return fminf(x, y); });
-                        const float nmax = warp_reduce(valid ? xn : -INFINITY,
-                                                       [](float x, float y) { return fmaxf(x, y); });
+                        const float nmin = __int_as_float(__ldg(a.grp_lo + grp));
+                        const float nmax = __int_as_float(__ldg(a.grp_hi + grp));
 #pragma unroll
-                        for (int i = 0; i < N / 64; ++i) {
-                            const int c = i * 32 + lane;
-                            const float P = __int_as_float(lds32(thr_addr + 4u * (uint32_t)(col_half + c)));
-                            int32_t B;
-                            if (P != P || nmin == INFINITY) {
-                                B = INT32_MAX;  // padded column or no valid row
-                            } else {
-                                const double b = (double)P * (double)(P >= 0.f ? nmin : nmax);
-                                B = b > 2147483647.0 ? INT32_MAX
-                                                     : (b < -2147483648.0 ? INT32_MIN
-                                                                          : (int32_t)ceil(b));
-                            }
+                        for (int c = lane; c < kCB; c += 32) {
+                            const float P = __int_as_float(lds32(thr_addr + 4u * (uint32_t)(col0 + c)));
+                            // cvt.rpi saturates (+-inf -> INT_MAX/INT_MIN); NaN marks
+                            // a padded column
+                            const int32_t B = (P != P) ? INT32_MAX
+                                                       : __float2int_ru(__fmul_rd(P, P >= 0.f ? nmin : nmax));
                             sts32(bnd_addr + 4u * (uint32_t)c, B);
                         }
                     }
@@ -491,80 +501,77 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(acc_full + acc, accph);
                 tc_fence_after();
                 const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) +
-                                       (uint32_t)(acc * N) + (uint32_t)col_half;
-                if (a.mode == 0) {
-                    int32_t va[32], vb[32];
-                    if (nch > 0) {
-                        tmem_ld32_async(tbase, va);
-                        tmem_wait();
-                    }
-#pragma unroll
-                    for (int ci = 0; ci < N / 64; ++ci) {
-                        if (ci >= nch) break;
-                        int32_t(&cur)[32] = (ci & 1) ? vb : va;
-                        int32_t(&nxt)[32] = (ci & 1) ? va : vb;
-                        if (ci + 1 < nch) tmem_ld32_async(tbase + (uint32_t)((ci + 1) * 32), nxt);
-                        // fast path: one integer compare per (row, query)
-                        bool any = false;
-#pragma unroll
-                        for (int g = 0; g < 8; ++g) {
-                            const int4 bb = lds128(bnd_addr + 4u * (uint32_t)(ci * 32 + 4 * g));
-                            any |= (cur[4 * g + 0] >= bb.x) | (cur[4 * g + 1] >= bb.y) |
-                                   (cur[4 * g + 2] >= bb.z) | (cur[4 * g + 3] >= bb.w);
-                        }
-                        if (any && valid) {
-                            // slow path (lanes with a candidate only): column mask,
-                            // values parked in this lane's smem row (no dynamic
-                            // register indexing), exact test per set bit.
-                            uint32_t mask = 0;
-#pragma unroll
-                            for (int g = 0; g < 8; ++g) {
-                                const int4 bb = lds128(bnd_addr + 4u * (uint32_t)(ci * 32 + 4 * g));
-                                mask |= ((uint32_t)(cur[4 * g + 0] >= bb.x) << (4 * g + 0)) |
-                                        ((uint32_t)(cur[4 * g + 1] >= bb.y) << (4 * g + 1)) |
-                                        ((uint32_t)(cur[4 * g + 2] >= bb.z) << (4 * g + 2)) |
-                                        ((uint32_t)(cur[4 * g + 3] >= bb.w) << (4 * g + 3));
-                                sts128(vrow_addr + 16u * (uint32_t)g, cur[4 * g], cur[4 * g + 1],
-                                       cur[4 * g + 2], cur[4 * g + 3]);
-                            }
-                            while (mask) {
-                                const int j = __ffs(mask) - 1;
-                                mask &= mask - 1;
-                                const int32_t v = lds32(vrow_addr + 4u * (uint32_t)j);
-                                const int qloc = col_half + ci * 32 + j;
-                                if constexpr (M != kIP) {
-                                    const int32_t T = lds32(thr_addr + 4u * (uint32_t)qloc);
-                                    if (!passes<M>(v, T, xx, inv_xn)) continue;
-                                }
-                                const int e = atomicAdd(stage_n, 1);
-                                if (e < kStageCap) {
-                                    const int sq = atomicAdd(qcnt + qloc, 1);
-                                    stage_buf[e] = Staged{qloc, sq, (int32_t)row, v};
-                                } else {
-                                    // staging full: direct append (slow, rare)
-                                    const int32_t s = atomicAdd(a.ccount + q0 + qloc, 1);
-                                    if (s < a.cap)
-                                        a.cand[(q0 + qloc) * a.cap + s] = Cand{(int32_t)row, v};
-                                }
-                            }
-                        }
-                        if (ci + 1 < nch) tmem_wait();
-                    }
-                } else {
+                                       (uint32_t)(acc * N) + (uint32_t)col0;
 #pragma unroll 1
-                    for (int ci = 0; ci < nch; ++ci) {
-                        int32_t v[32];
-                        tmem_ld32(tbase + (uint32_t)(ci * 32), v);
+                for (int ci = 0; ci < nch; ++ci) {
+                    int32_t cur[kC];
+                    tmem_ld_cols<kC>(tbase + (uint32_t)(ci * kC), cur);
+                    tmem_wait();
+                    if (a.mode != 0) {
                         if (!valid) continue;
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const int c = col_half + ci * 32 + j;
+                        for (int j = 0; j < kC; ++j) {
+                            const int c = col0 + ci * kC + j;
                             if (c >= nqt) continue;
                             const int64_t q = q0 + c;
                             if (a.mode == 1)
-                                a.cand[q * a.cap + (row - a.r_lo)] = Cand{(int32_t)row, v[j]};
+                                a.cand[q * a.cap + (row - a.r_lo)] = Cand{(int32_t)row, cur[j]};
                             else
-                                a.dots_out[q * a.ld_dots + row] = v[j];
+                                a.dots_out[q * a.ld_dots + row] = cur[j];
+                        }
+                        continue;
+                    }
+                    // fast path: one integer compare per (row, query), one
+                    // accumulated predicate per group of 8 columns
+                    bool hit[kC / 8];
+#pragma unroll
+                    for (int h = 0; h < kC / 8; ++h) {
+                        const int4 b0 = lds128(bnd_addr + 4u * (uint32_t)(ci * kC + 8 * h));
+                        const int4 b1 = lds128(bnd_addr + 4u * (uint32_t)(ci * kC + 8 * h + 4));
+                        const int32_t *c8 = cur + 8 * h;
+                        hit[h] = (c8[0] >= b0.x) | (c8[1] >= b0.y) | (c8[2] >= b0.z) |
+                                 (c8[3] >= b0.w) | (c8[4] >= b1.x) | (c8[5] >= b1.y) |
+                                 (c8[6] >= b1.z) | (c8[7] >= b1.w);
+                    }
+                    bool anyhit = false;
+#pragma unroll
+                    for (int h = 0; h < kC / 8; ++h) anyhit |= hit[h];
+                    if (!(anyhit && valid)) continue;
+                    // slow path (lanes with a candidate only): per hit group an
+                    // 8-bit column mask; the value of a set bit is picked with a
+                    // select chain (no dynamic register indexing); exact test.
+#pragma unroll
+                    for (int h = 0; h < kC / 8; ++h) {
+                        if (!hit[h]) continue;
+                        const int32_t *c8 = cur + 8 * h;
+                        const int4 b0 = lds128(bnd_addr + 4u * (uint32_t)(ci * kC + 8 * h));
+                        const int4 b1 = lds128(bnd_addr + 4u * (uint32_t)(ci * kC + 8 * h + 4));
+                        uint32_t m8 =
+                            ((uint32_t)(c8[0] >= b0.x) << 0) | ((uint32_t)(c8[1] >= b0.y) << 1) |
+                            ((uint32_t)(c8[2] >= b0.z) << 2) | ((uint32_t)(c8[3] >= b0.w) << 3) |
+                            ((uint32_t)(c8[4] >= b1.x) << 4) | ((uint32_t)(c8[5] >= b1.y) << 5) |
+                            ((uint32_t)(c8[6] >= b1.z) << 6) | ((uint32_t)(c8[7] >= b1.w) << 7);
+                        while (m8) {
+                            const int j = __ffs(m8) - 1;
+                            m8 &= m8 - 1;
+                            int32_t v = c8[0];
+#pragma unroll
+                            for (int jj = 1; jj < 8; ++jj) v = (j == jj) ? c8[jj] : v;
+                            const int qloc = col0 + ci * kC + 8 * h + j;
+                            if constexpr (M != kIP) {
+                                const int32_t T = lds32(thr_addr + 4u * (uint32_t)qloc);
+                                if (!passes<M>(v, T, xx, inv_xn)) continue;
+                            }
+                            const int e = atomicAdd(stage_n, 1);
+                            if (e < kStageCap) {
+                                const int sq = atomicAdd(qcnt + qloc, 1);
+                                stage_buf[e] = Staged{qloc, sq, (int32_t)row, v};
+                            } else {
+                                // staging full: direct append (slow, rare)
+                                const int32_t s = atomicAdd(a.ccount + q0 + qloc, 1);
+                                if (s < a.cap)
+                                    a.cand[(q0 + qloc) * a.cap + s] = Cand{(int32_t)row, v};
+                            }
                         }
                     }
                 }
@@ -598,7 +605,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     }
-
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {
@@ -660,7 +666,7 @@ cudaError_t launch_t(const FilterArgs &a, int *sched, cudaStream_t st) {
     p.b_slots = (2 * (size_t)N * a.kdim <= 65536) ? 2 : 1;
     const size_t fixed = 1024 /*align slack*/ + (size_t)p.b_slots * N * a.kdim +
                          kStageCap * sizeof(Staged) + 7 * N * sizeof(int32_t) +
-                         8 * 32 * kVRow * sizeof(int32_t) + 256;
+                         256;
     const size_t budget = 227 * 1024;
     const size_t stage_bytes = (size_t)kBlockM * SW;
     // each stage also costs two 8-byte mbarriers

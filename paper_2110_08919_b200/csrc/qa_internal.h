@@ -34,6 +34,10 @@ struct FilterArgs {
     int64_t r_lo, r_hi;
     const int32_t *db_sqnorm;
     const float *db_norm;
+    // per 32-row group norm range (launch_group_ranges): L2 grp_lo = min
+    // sqnorm; angular grp_lo/grp_hi = float bits of min/max norm
+    const int32_t *grp_lo;
+    const int32_t *grp_hi;
     const int32_t *thr;
     Cand *cand;
     int32_t *ccount;
@@ -79,6 +83,10 @@ cudaError_t launch_fill(int32_t *p, int64_t n, int32_t v, cudaStream_t st);
 cudaError_t launch_finalize(const Entry *state, int64_t nq, int64_t k, int64_t keff, int metric,
                             int64_t id_offset, double *out_scores, int32_t *out_ids,
                             cudaStream_t st);
+// Norm range of every 32-row group, padded to `groups` entries (groups past
+// n never pass a filter bound).
+cudaError_t launch_group_ranges(int metric, const int32_t *sqnorm, const float *norm, int64_t n,
+                                int32_t *lo, int32_t *hi, int64_t groups, cudaStream_t st);
 // stable ascending order of rows by int32 key (CUB radix sort); perm[i] = row
 cudaError_t launch_order_by_key(const int32_t *key, int64_t n, int32_t *perm, void *scratch,
                                 size_t scratch_bytes, size_t *needed, cudaStream_t st);

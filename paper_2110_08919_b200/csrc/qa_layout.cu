@@ -55,7 +55,42 @@ __global__ void permute_rows_kernel(const int8_t *__restrict__ src, const int32_
     }
 }
 
+// one warp per 32-row group
+__global__ void group_ranges_kernel(int metric, const int32_t *__restrict__ sqnorm,
+                                    const float *__restrict__ norm, int64_t n,
+                                    int32_t *__restrict__ lo, int32_t *__restrict__ hi,
+                                    int64_t groups) {
+    const int lane = threadIdx.x & 31;
+    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (g >= groups) return;
+    const int64_t r = g * 32 + lane;
+    const bool ok = r < n;
+    if (metric == 1) {
+        int32_t v = ok ? sqnorm[r] : INT32_MAX;
+        for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (lane == 0) lo[g] = v;
+    } else {
+        float vmin = ok ? norm[r] : INFINITY, vmax = ok ? norm[r] : -INFINITY;
+        for (int o = 16; o; o >>= 1) {
+            vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+            vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+        }
+        if (lane == 0) {
+            lo[g] = __float_as_int(vmin);
+            hi[g] = __float_as_int(vmax);
+        }
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_group_ranges(int metric, const int32_t *sqnorm, const float *norm, int64_t n,
+                                int32_t *lo, int32_t *hi, int64_t groups, cudaStream_t st) {
+    if (groups == 0 || metric == 0) return cudaSuccess;
+    group_ranges_kernel<<<(unsigned)((groups * 32 + 255) / 256), 256, 0, st>>>(metric, sqnorm, norm,
+                                                                              n, lo, hi, groups);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_order_by_key(const int32_t *key, int64_t n, int32_t *perm, void *scratch,
                                 size_t scratch_bytes, size_t *needed, cudaStream_t st) {

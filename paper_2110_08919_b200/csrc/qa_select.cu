@@ -200,6 +200,196 @@ __global__ void __launch_bounds__(kWarpsMax * 32) select_kernel(SelectArgs a, in
     }
 }
 
+// ------------------------------------------------ register select (k<=128) --
+//
+// The retained list T (<= 128 entries) and a chunk S of 128 candidates live in
+// registers, 4 per lane, element index i = e*32 + lane.  S is bitonic-sorted
+// (strides < 32 cross lanes by shuffles, 32/64 swap registers), reversed,
+// and [T asc | S desc] -- a bitonic sequence of 256 -- is merged: one
+// compare at stride 128 leaves the 128 smallest in T's registers, seven more
+// stages sort them.  No shared memory, no barriers.
+//
+// Keys: IP / L2 scores are int32, so (score, id) packs into one u64; angular
+// keeps the u64 float64 order key plus the id.
+struct RKey64 {
+    unsigned long long k;
+};
+struct RKey96 {
+    unsigned long long k;
+    int32_t id;
+};
+
+__device__ __forceinline__ bool rlt(const RKey64 &a, const RKey64 &b) { return a.k < b.k; }
+__device__ __forceinline__ bool rlt(const RKey96 &a, const RKey96 &b) {
+    return a.k < b.k || (a.k == b.k && a.id < b.id);
+}
+__device__ __forceinline__ RKey64 rshfl(const RKey64 &a, int m) {
+    return RKey64{__shfl_xor_sync(0xffffffffu, a.k, m)};
+}
+__device__ __forceinline__ RKey96 rshfl(const RKey96 &a, int m) {
+    return RKey96{__shfl_xor_sync(0xffffffffu, a.k, m), __shfl_xor_sync(0xffffffffu, a.id, m)};
+}
+__device__ __forceinline__ void rsentinel(RKey64 &a) { a.k = ~0ull; }
+__device__ __forceinline__ void rsentinel(RKey96 &a) {
+    a.k = ~0ull;
+    a.id = INT32_MAX;
+}
+
+// Entry <-> register key
+template <int M>
+__device__ __forceinline__ void to_key(const Entry &e, RKey64 &r) {
+    r.k = ((unsigned long long)(uint32_t)e.skey << 32) | (uint32_t)e.id;
+}
+template <int M>
+__device__ __forceinline__ void to_key(const Entry &e, RKey96 &r) {
+    r.k = e.skey;
+    r.id = e.id;
+}
+__device__ __forceinline__ Entry from_key(const RKey64 &r) {
+    Entry e;
+    e.skey = r.k >> 32;
+    e.id = (int32_t)(uint32_t)r.k;
+    e.row = 0;
+    return e;
+}
+__device__ __forceinline__ Entry from_key(const RKey96 &r) {
+    Entry e;
+    e.skey = r.k;
+    e.id = r.id;
+    e.row = 0;
+    return e;
+}
+
+__device__ __forceinline__ RKey64 rbcast(const RKey64 &a, int src) {
+    return RKey64{__shfl_sync(0xffffffffu, a.k, src)};
+}
+__device__ __forceinline__ RKey96 rbcast(const RKey96 &a, int src) {
+    return RKey96{__shfl_sync(0xffffffffu, a.k, src), __shfl_sync(0xffffffffu, a.id, src)};
+}
+
+// element i of x[4] (i = e*32 + lane), broadcast to the whole warp
+template <typename K>
+__device__ __forceinline__ K rget(const K (&x)[4], int i) {
+    K v = x[0];
+#pragma unroll
+    for (int e = 1; e < 4; ++e)
+        if ((i >> 5) == e) v = x[e];
+    return rbcast(v, i & 31);
+}
+
+// one compare-exchange stage over x[4] (i = e*32 + lane) for (size, stride)
+template <typename K>
+__device__ __forceinline__ void rstage(K (&x)[4], int size, int stride) {
+    const int lane = threadIdx.x & 31;
+    if (stride >= 32) {
+        const int es = stride >> 5;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int p = e ^ es;
+            if (p > e) {
+                const bool up = (((e * 32 + lane) & size) == 0);
+                if (up ? rlt(x[p], x[e]) : rlt(x[e], x[p])) {
+                    K t = x[e];
+                    x[e] = x[p];
+                    x[p] = t;
+                }
+            }
+        }
+    } else {
+        const bool lower = (lane & stride) == 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const bool up = (((e * 32 + lane) & size) == 0);
+            const K o = rshfl(x[e], stride);
+            // the lower index of an ascending pair keeps the min
+            const bool take = (lower == up) ? rlt(o, x[e]) : rlt(x[e], o);
+            if (take) x[e] = o;
+        }
+    }
+}
+
+template <typename K>
+__device__ __forceinline__ void rsort128(K (&x)[4]) {
+#pragma unroll
+    for (int size = 2; size <= 128; size <<= 1)
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) rstage(x, size, stride);
+}
+
+template <int M, typename K>
+__global__ void __launch_bounds__(256) select_reg_kernel(SelectArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (q >= a.nq) return;
+    const int32_t total = a.ccount[q];
+    if (total == 0) return;
+    const int k = (int)a.k;
+    const int m = (int)min((int64_t)total, a.cap);
+    if (total > a.cap && lane == 0) {
+        a.overflow[q] = 1;
+        atomicExch(a.any_overflow, 1);
+    }
+    const int32_t qq = (M == kL2) ? a.q_sqnorm[q] : 0;
+    const float qn = (M == kAngular) ? a.q_norm[q] : 1.0f;
+    Entry *st = a.state + q * a.k;
+    const Cand *cd = a.cand + q * a.cap;
+    int cur = a.state_cnt[q];
+    K t[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int i = e * 32 + lane;
+        if (i < cur)
+            to_key<M>(st[i], t[e]);
+        else
+            rsentinel(t[e]);
+    }
+    for (int pos = 0; pos < m; pos += 128) {
+        // k-th retained key (sentinel while fewer than k): candidates not
+        // below it cannot enter
+        const K kth = rget(t, k - 1);
+        K s[4];
+        int ns = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int i = pos + e * 32 + lane;
+            bool keep = false;
+            if (i < m) {
+                const Entry en = make_entry<M>(cd[i], qq, qn, a.db_sqnorm, a.db_norm, a.row_ids);
+                to_key<M>(en, s[e]);
+                keep = rlt(s[e], kth);
+            }
+            if (!keep) rsentinel(s[e]);
+            ns += __popc(__ballot_sync(0xffffffffu, keep));
+        }
+        if (ns == 0) continue;
+        rsort128(s);
+        // reverse S (i -> 127 - i): lane -> 31 - lane, e -> 3 - e
+        K r[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) r[e] = rshfl(s[3 - e], 31);
+        // stride-128 step of the bitonic merge: T keeps the 128 smallest
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (rlt(r[e], t[e])) t[e] = r[e];
+        // t is bitonic now: finish the merge with strides 64..1 (size 128,
+        // ascending everywhere)
+#pragma unroll
+        for (int stride = 64; stride > 0; stride >>= 1) rstage(t, 256, stride);
+        cur = min(k, cur + ns);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int i = e * 32 + lane;
+        if (i < cur) st[i] = from_key(t[e]);
+    }
+    // threshold from the k-th entry
+    if (cur == k) {
+        const K v = rget(t, k - 1);
+        if (lane == 0) a.thr[q] = threshold_of<M>(from_key(v), qq, qn);
+    }
+    if (lane == 0) a.state_cnt[q] = cur;
+}
+
 __global__ void reset_kernel(int32_t *p, int64_t n, int32_t v) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -297,6 +487,14 @@ int pow2_at_least(int64_t v, int64_t cap) {
 
 template <int M>
 cudaError_t launch_select_t(const SelectArgs &a, cudaStream_t st) {
+    if (a.k <= 128) {
+        const unsigned grid = (unsigned)((a.nq + 7) / 8);
+        if constexpr (M == kAngular)
+            select_reg_kernel<M, RKey96><<<grid, 256, 0, st>>>(a);
+        else
+            select_reg_kernel<M, RKey64><<<grid, 256, 0, st>>>(a);
+        return cudaGetLastError();
+    }
     const int kpad = (int)((a.k + 31) / 32 * 32);
     const size_t per_warp = (size_t)(2 * kpad + kChunk) * sizeof(Entry);
     int warps = (int)std::min<size_t>(kWarpsMax, (160 * 1024) / per_warp);

@@ -25,8 +25,10 @@ for row in det[1:]:
 raw = list(csv.reader(io.StringIO(run("--page", "raw", "--csv"))))
 names, vals = raw[0], raw[2] if len(raw) > 2 else raw[1]
 for n, v in zip(names, vals):
-    if any(k in n for k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "sm__pipe_tensor",
-                            "sm__inst_executed_pipe_tc", "tensor_op")) and "pct" not in n[:3]:
+    if n in ("dram__bytes_read.sum", "dram__bytes_write.sum",
+             "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
+             "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+             "sm__pipe_tensor_op_imma_cycles_active.avg.pct_of_peak_sustained_active"):
         print(f"{n:70s} {v}")
 rows = list(csv.reader(io.StringIO(run("--page", "source", "--csv", "--print-source", "sass"))))
 h = rows[1]
