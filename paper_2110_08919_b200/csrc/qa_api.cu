@@ -148,7 +148,9 @@ struct ScanPlan {
 ScanPlan plan_scan(int64_t n, int64_t nq, int64_t keff, int64_t cap_min) {
     ScanPlan p;
     p.r0 = std::min(n, round_up(std::max<int64_t>(keff, 256), 128));
-    p.ratio = nq >= 256 ? 4 : 16;
+    // Row growth per round: every round adds ~k*(ratio-1) survivors per query;
+    // small ratios cost more rounds (launches), large ones more survivors.
+    p.ratio = nq >= 256 ? 2 : 16;
     if (const char *v = getenv("QA_B200_RATIO")) p.ratio = std::max(2, atoi(v));
     p.cap = std::max<int64_t>({2048, p.r0, 2 * keff * p.ratio, cap_min});
     const int64_t per_q = p.cap * (int64_t)sizeof(Cand) + keff * (int64_t)sizeof(Entry) + 64;

@@ -40,6 +40,10 @@ constexpr int kEpiWarp0 = 4;
 constexpr int kEpiThreads = 512;
 constexpr int kStageCap = 2048;  // survivors staged in smem per work unit
 constexpr int kEpiBarrier = 1;   // named barrier id for the epilogue warps
+// try_wait suspend-time hint: a waiting warp sleeps (instead of spinning and
+// stealing issue slots from the epilogue) until the phase completes or this
+// many ns pass
+constexpr int kWaitHintNs = 20000;
 
 // ------------------------------------------------------------------ PTX --
 
@@ -67,11 +71,37 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "{\n\t"
         ".reg .pred p;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n\t"
         "}" ::"r"(addr),
-        "r"(parity)
+        "r"(parity), "n"(kWaitHintNs)
         : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t"
+        "}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+// Wait with nanosleep backoff: for the single-thread producer / MMA roles,
+// which otherwise spin and steal issue slots from the epilogue warps that
+// share their SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    if (mbar_try(bar, parity)) return;
+    uint32_t ns = 32;
+    while (!mbar_try(bar, parity)) {
+        __nanosleep(ns);
+        ns = ns < 256 ? ns * 2 : 256;
+    }
 }
 
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar,
@@ -324,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int slot = it & 1;
                 const uint32_t ph = (it >> 1) & 1;
                 int64_t u = atomicAdd(p.sched, 1);
-                mbar_wait(unit_empty + slot, ph ^ 1);
+                mbar_wait_sleep(unit_empty + slot, ph ^ 1);
                 unit_id[slot] = u < p.n_units ? (int32_t)u : -1;
                 mbar_arrive(unit_full + slot);
                 if (u >= p.n_units) break;
@@ -332,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // resident query tile for this unit
                 const int bslot = it % bslots;
                 const uint32_t bph = (uint32_t)(it / bslots) & 1;
-                mbar_wait(b_empty + bslot, bph ^ 1);
+                mbar_wait_sleep(b_empty + bslot, bph ^ 1);
                 mbar_arrive_expect_tx(b_full + bslot, b_bytes);
                 unsigned char *dstB = sB + (size_t)bslot * b_bytes;
                 for (int c = 0; c < p.kchunks; ++c)
@@ -344,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int64_t tile = tile0; tile < tile1; ++tile) {
                     const int32_t row0 = (int32_t)(a.r_lo + tile * kBlockM);
                     for (int c = 0; c < p.kchunks; ++c) {
-                        mbar_wait(a_empty + stage, aph ^ 1);
+                        mbar_wait_sleep(a_empty + stage, aph ^ 1);
                         mbar_arrive_expect_tx(a_full + stage, a_stage_bytes);
                         tma_load_2d(sA + (size_t)stage * a_stage_bytes, &tm_db, a_full + stage,
                                     c * SW, row0);
@@ -366,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int it = 0;; ++it) {
             const int slot = it & 1;
             const uint32_t ph = (it >> 1) & 1;
-            mbar_wait(unit_full + slot, ph);
+            mbar_wait_sleep(unit_full + slot, ph);
             const int32_t u = unit_id[slot];
             __syncwarp();
             if (u < 0) break;
@@ -374,14 +404,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t tile0 = b * p.tiles_per_unit;
             const int64_t tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
             const int bslot = it % bslots;
-            mbar_wait(b_full + bslot, (uint32_t)(it / bslots) & 1);
+            mbar_wait_sleep(b_full + bslot, (uint32_t)(it / bslots) & 1);
             const uint32_t bbase = smem_u32(sB + (size_t)bslot * b_bytes);
             for (int64_t tile = tile0; tile < tile1; ++tile) {
-                mbar_wait(acc_empty + acc, accph ^ 1);
+                mbar_wait_sleep(acc_empty + acc, accph ^ 1);
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + (uint32_t)(acc * N);
                 for (int c = 0; c < p.kchunks; ++c) {
-                    mbar_wait(a_full + stage, aph);
+                    mbar_wait_sleep(a_full + stage, aph);
                     tc_fence_after();
                     if (lane == 0) {
                         const uint32_t abase = smem_u32(sA + (size_t)stage * a_stage_bytes);
@@ -455,16 +485,86 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                  : smem_u32(bnd_s + ew * kCB);
             // column chunks this warp actually has queries for
             const int nch = max(0, min(kCB / kC, (nqt - col0 + kC - 1) / kC));
-            for (int64_t tile = tile0; tile < tile1; ++tile) {
-                const int64_t row = a.r_lo + tile * kBlockM + quarter * 32 + lane;
-                const bool valid = row < a.r_hi;
-                int32_t xx = 0;
-                float inv_xn = 0.f;
-                if (valid) {
-                    if constexpr (M == kL2) xx = __ldg(a.db_sqnorm + row);
-                    if constexpr (M == kAngular) inv_xn = __frcp_rn(__ldg(a.db_norm + row));
+            // 32-bit row arithmetic (n <= INT32_MAX is enforced on the host)
+            const int32_t r_hi = (int32_t)a.r_hi;
+            int32_t wrow0 = (int32_t)(a.r_lo + tile0 * kBlockM) + quarter * 32;
+            const int ntl = (int)(tile1 - tile0);
+            if (a.mode != 0) {
+                // dense / diagnostic passes: every dot is written out
+                for (int ti = 0; ti < ntl; ++ti, wrow0 += kBlockM) {
+                    const int32_t row = wrow0 + lane;
+                    mbar_wait(acc_full + acc, accph);
+                    tc_fence_after();
+                    const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) +
+                                           (uint32_t)(acc * N) + (uint32_t)col0;
+                    for (int ci = 0; ci < nch; ++ci) {
+                        int32_t cur[kC];
+                        tmem_ld_cols<kC>(tbase + (uint32_t)(ci * kC), cur);
+                        tmem_wait();
+                        if (row >= r_hi) continue;
+#pragma unroll
+                        for (int j = 0; j < kC; ++j) {
+                            const int c = col0 + ci * kC + j;
+                            if (c >= nqt) continue;
+                            const int64_t q = q0 + c;
+                            if (a.mode == 1)
+                                a.cand[q * a.cap + (row - (int32_t)a.r_lo)] = Cand{row, cur[j]};
+                            else
+                                a.dots_out[q * a.ld_dots + row] = cur[j];
+                        }
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(acc_empty + acc);
+                    if (++acc == 2) {
+                        acc = 0;
+                        accph ^= 1;
+                    }
                 }
-                if (a.mode == 0 && M != kIP && nch > 0) {
+                continue;
+            }
+            // Per-unit column constants in registers (this lane's kCB/32
+            // columns): thresholds; for angular the NaN of padded columns
+            // becomes +inf (bound INT_MAX) and the sign picks min/max norm.
+            constexpr int kPL = (kCB + 31) / 32;
+            int32_t thr_r[kPL];
+#pragma unroll
+            for (int i = 0; i < kPL; ++i) {
+                const int c = i * 32 + lane;
+                thr_r[i] = c < kCB ? lds32(thr_addr + 4u * (uint32_t)(col0 + c)) : 0;
+                if constexpr (M == kAngular)
+                    if (__int_as_float(thr_r[i]) != __int_as_float(thr_r[i]))
+                        thr_r[i] = 0x7f800000;  // +inf
+            }
+            // prefetch of the first tile's per-row / per-group scalars
+            int32_t nx_a = 0, nx_lo = 0, nx_hi = 0;
+            if (ntl > 0) {
+                const int32_t row = wrow0 + lane;
+                if constexpr (M == kL2) {
+                    nx_a = row < r_hi ? __ldg(a.db_sqnorm + row) : 0;
+                    nx_lo = __ldg(a.grp_lo + (wrow0 >> 5));
+                } else if constexpr (M == kAngular) {
+                    nx_a = row < r_hi ? __float_as_int(__ldg(a.db_norm + row)) : 0;
+                    nx_lo = __ldg(a.grp_lo + (wrow0 >> 5));
+                    nx_hi = __ldg(a.grp_hi + (wrow0 >> 5));
+                }
+            }
+            for (int ti = 0; ti < ntl; ++ti, wrow0 += kBlockM) {
+                const int32_t row = wrow0 + lane;
+                const bool valid = row < r_hi;
+                const int32_t rv = nx_a, glo = nx_lo, ghi = nx_hi;
+                if (ti + 1 < ntl) {  // prefetch the next tile's scalars
+                    const int32_t nrow = row + kBlockM;
+                    if constexpr (M == kL2) {
+                        nx_a = nrow < r_hi ? __ldg(a.db_sqnorm + nrow) : 0;
+                        nx_lo = __ldg(a.grp_lo + ((wrow0 + kBlockM) >> 5));
+                    } else if constexpr (M == kAngular) {
+                        nx_a = nrow < r_hi ? __float_as_int(__ldg(a.db_norm + nrow)) : 0;
+                        nx_lo = __ldg(a.grp_lo + ((wrow0 + kBlockM) >> 5));
+                        nx_hi = __ldg(a.grp_hi + ((wrow0 + kBlockM) >> 5));
+                    }
+                }
+                if constexpr (M != kIP) {
                     // Necessary integer condition per (warp rows, column):
                     //   L2:      xx_i - 2 dot <= T  =>  dot >= ceil((min xx - T) / 2)
                     //   angular: dot / xn_i >= P    =>  dot >= ceil(P * (P >= 0 ? min xn
@@ -474,27 +574,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // superset range when rows past r_hi share the group).  Rows
                     // sorted by norm at index build make it, hence the bound,
                     // tight; the exact per-row test runs on the rare survivors.
-                    const int64_t grp = (a.r_lo + tile * kBlockM + quarter * 32) >> 5;
-                    if constexpr (M == kL2) {
-                        const int32_t xmin = __ldg(a.grp_lo + grp);
 #pragma unroll
-                        for (int c = lane; c < kCB; c += 32) {
-                            const int32_t T = lds32(thr_addr + 4u * (uint32_t)(col0 + c));
-                            const long long num = (long long)xmin - (long long)T;
-                            sts32(bnd_addr + 4u * (uint32_t)c, clamp_i64((num + 1) >> 1));
+                    for (int i = 0; i < kPL; ++i) {
+                        int32_t B;
+                        if constexpr (M == kL2) {
+                            const long long num = (long long)glo - (long long)thr_r[i];
+                            B = clamp_i64((num + 1) >> 1);
+                        } else {
+                            const float P = __int_as_float(thr_r[i]);
+                            B = __float2int_ru(__fmul_rd(P, P >= 0.f ? __int_as_float(glo)
+                                                                     : __int_as_float(ghi)));
                         }
-                    } else {
-                        const float nmin = __int_as_float(__ldg(a.grp_lo + grp));
-                        const float nmax = __int_as_float(__ldg(a.grp_hi + grp));
-#pragma unroll
-                        for (int c = lane; c < kCB; c += 32) {
-                            const float P = __int_as_float(lds32(thr_addr + 4u * (uint32_t)(col0 + c)));
-                            // cvt.rpi saturates (+-inf -> INT_MAX/INT_MIN); NaN marks
-                            // a padded column
-                            const int32_t B = (P != P) ? INT32_MAX
-                                                       : __float2int_ru(__fmul_rd(P, P >= 0.f ? nmin : nmax));
-                            sts32(bnd_addr + 4u * (uint32_t)c, B);
-                        }
+                        if (i * 32 + lane < kCB) sts32(bnd_addr + 4u * (uint32_t)(i * 32 + lane), B);
                     }
                     __syncwarp();
                 }
@@ -507,20 +598,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     int32_t cur[kC];
                     tmem_ld_cols<kC>(tbase + (uint32_t)(ci * kC), cur);
                     tmem_wait();
-                    if (a.mode != 0) {
-                        if (!valid) continue;
-#pragma unroll
-                        for (int j = 0; j < kC; ++j) {
-                            const int c = col0 + ci * kC + j;
-                            if (c >= nqt) continue;
-                            const int64_t q = q0 + c;
-                            if (a.mode == 1)
-                                a.cand[q * a.cap + (row - a.r_lo)] = Cand{(int32_t)row, cur[j]};
-                            else
-                                a.dots_out[q * a.ld_dots + row] = cur[j];
-                        }
-                        continue;
-                    }
                     // fast path: one integer compare per (row, query), one
                     // accumulated predicate per group of 8 columns
                     bool hit[kC / 8];
@@ -540,6 +617,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // slow path (lanes with a candidate only): per hit group an
                     // 8-bit column mask; the value of a set bit is picked with a
                     // select chain (no dynamic register indexing); exact test.
+                    const int32_t xx = (M == kL2) ? rv : 0;
+                    const float inv_xn = (M == kAngular) ? __frcp_rn(__int_as_float(rv)) : 0.f;
 #pragma unroll
                     for (int h = 0; h < kC / 8; ++h) {
                         if (!hit[h]) continue;
@@ -565,12 +644,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const int e = atomicAdd(stage_n, 1);
                             if (e < kStageCap) {
                                 const int sq = atomicAdd(qcnt + qloc, 1);
-                                stage_buf[e] = Staged{qloc, sq, (int32_t)row, v};
+                                stage_buf[e] = Staged{qloc, sq, row, v};
                             } else {
                                 // staging full: direct append (slow, rare)
                                 const int32_t s = atomicAdd(a.ccount + q0 + qloc, 1);
                                 if (s < a.cap)
-                                    a.cand[(q0 + qloc) * a.cap + s] = Cand{(int32_t)row, v};
+                                    a.cand[(q0 + qloc) * a.cap + s] = Cand{row, v};
                             }
                         }
                     }
@@ -583,7 +662,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     accph ^= 1;
                 }
             }
-            if (a.mode == 0) {
+            {
                 // ---- flush the unit's staged survivors ----
                 epi_barrier();
                 for (int i = etid; i < N; i += kEpiThreads) {
