@@ -147,7 +147,12 @@ struct ScanPlan {
 
 ScanPlan plan_scan(int64_t n, int64_t nq, int64_t keff, int64_t cap_min) {
     ScanPlan p;
-    p.r0 = std::min(n, round_up(std::max<int64_t>(keff, 256), 128));
+    // a power of two >= 256: with ratio 2 every round boundary >= 4096 is a
+    // multiple of the index's 4096-row norm blocks (qa_layout.cu)
+    int64_t r0 = 256;
+    if (const char *v = getenv("QA_B200_R0")) r0 = std::max<int64_t>(128, atoll(v));
+    while (r0 < keff) r0 *= 2;
+    p.r0 = std::min(n, r0);
     // Row growth per round: every round adds ~k*(ratio-1) survivors per query;
     // small ratios cost more rounds (launches), large ones more survivors.
     p.ratio = nq >= 256 ? 2 : 16;
@@ -215,9 +220,8 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
     QA_TRY(cudaMemsetAsync(ovf, 0, (size_t)nq * 4, st), "memset");
     QA_TRY(cudaMemsetAsync(flags, 0, 64, st), "memset");
     const bool simt = use_simt_filter(ld);
-    // norm range of every 32-row group (per-warp filter bounds), padded to
-    // whole 128-row tiles
-    const int64_t groups = (n + 127) / 128 * 4;
+    // norm range of every 128-row tile (per-unit filter bounds)
+    const int64_t groups = (n + 127) / 128;
     QA_TRY(ws.grp.reserve((size_t)groups * 8), "workspace");
     int32_t *grp_lo = (int32_t *)ws.grp.ptr, *grp_hi = grp_lo + groups;
     QA_TRY(launch_group_ranges(metric, db_sqnorm, db_norm, n, grp_lo, grp_hi, groups, st),
@@ -248,10 +252,15 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             fa.ccount = ccount;
             fa.cap = pl.cap;
             fa.metric = metric;
-            fa.mode = first ? 1 : 0;
+            // round 0: dense (every row); survivor-dense early rounds whose
+            // rows fit the candidate list: masked dense (no atomics); then the
+            // filter with staged survivors
+            const bool masked = !first && (r_hi - r_lo) <= std::min<int64_t>(pl.cap, 2048);
+            const int mode = first ? 1 : (masked ? 3 : 0);
+            fa.mode = mode;
             fa.dots_out = nullptr;
             fa.ld_dots = 0;
-            QA_TRY(launch_fill(ccount, m, first ? (int32_t)(r_hi - r_lo) : 0, st), "fill");
+            QA_TRY(launch_fill(ccount, m, mode != 0 ? (int32_t)(r_hi - r_lo) : 0, st), "fill");
             cudaError_t e = cudaErrorNotSupported;
             g_timer.begin(0, st);
             if (!simt) e = launch_filter_tc(fa, flags + 1, st);

@@ -48,6 +48,11 @@ __global__ void __launch_bounds__(kRows) filter_simt_kernel(FilterArgs a) {
             a.cand[q * a.cap + (row - a.r_lo)] = Cand{(int32_t)row, acc};
             continue;
         }
+        if (a.mode == 3) {  // masked dense: slot per row, row = -1 when filtered out
+            a.cand[q * a.cap + (row - a.r_lo)] =
+                passes<M>(acc, __ldg(a.thr + q), xx, inv_xn) ? Cand{(int32_t)row, acc} : Cand{-1, 0};
+            continue;
+        }
         if (passes<M>(acc, __ldg(a.thr + q), xx, inv_xn)) {
             int32_t slot = atomicAdd(a.ccount + q, 1);
             if (slot < a.cap) a.cand[q * a.cap + slot] = Cand{(int32_t)row, acc};

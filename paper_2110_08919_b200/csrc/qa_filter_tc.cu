@@ -1,31 +1,48 @@
 // qa_filter_tc.cu -- the fused tensor-core filter pass (sm_100a).
 //
 // One pass scores database rows [r_lo, r_hi) against a chunk of queries and
-// keeps only (query, row) pairs that can still enter the query's top-k:
+// keeps only the (query, row) pairs that can still enter the query's top-k:
 //
 //   * int8 x int8 -> int32 contraction on the 5th-gen tensor cores:
-//     tcgen05.mma.cta_group::1.kind::i8, M = 128 database rows, N = up to
-//     256 queries, K = 32 bytes per instruction, accumulator in TMEM
-//     (double-buffered: 2 x N columns of the 512);
-//   * operands staged by TMA (cp.async.bulk.tensor.2d) with the 32/64/128-byte
-//     swizzle matching the UMMA shared-memory descriptors; the query tile (B)
-//     is loaded once per work unit and stays resident while database tiles
-//     (A) stream through a multi-stage mbarrier ring;
-//   * the epilogue (8 warps) reads each accumulator with tcgen05.ld
-//     32x32b.x32, applies the metric's norm correction and compares against
-//     the per-query threshold with one predicate per element; survivors
-//     (rare) are staged in shared memory and flushed to the per-query global
-//     candidate lists with one atomic per (query, unit).  The int32 score
-//     matrix never reaches HBM.
+//     tcgen05.mma.cta_group::1.kind::i8, M = 128 database rows, N = up to 256
+//     queries, K = 32 bytes per instruction, accumulator in TMEM (double
+//     buffered: 2 x N of the 512 columns);
+//   * operands staged by TMA (cp.async.bulk.tensor.2d) in the 32/64/128-byte
+//     swizzle the UMMA shared-memory descriptors expect; the query tile (B)
+//     is loaded once per work unit, database tiles (A) stream through a
+//     multi-stage mbarrier ring;
+//   * the per-query filter bound is folded INTO the accumulator: one extra
+//     K=32 MMA per tile multiplies a constant A tile (all 127) by a per-unit
+//     B tile of int8 "bias digits", adding bias_q = 127 * sum(digits) >= -B_q
+//     to every dot of query q.  A row can pass the bound only if its biased
+//     value is >= 0, so the epilogue's fast path is a sign test: a 3-input
+//     LOP3 AND-reduction of 32 accumulators (~0.5 instruction per element);
+//   * the rare lanes with a non-negative value run the exact per-row test
+//     and stage survivors in shared memory; each work unit flushes them to
+//     the per-query global candidate lists with one atomic per query.  The
+//     int32 score matrix never reaches HBM.
 //
-// Warp roles (384 threads, 1 CTA per SM, persistent over an atomic work-unit
-// counter):  warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM allocator,
-// warp 3 idle, warps 4..11 epilogue.
+// Bounds (necessary conditions on the dot product, per query and per work
+// unit of <= 32 consecutive tiles; units lie inside one norm-sorted block of
+// the index, so the unit's norm range is narrow):
+//   IP       dot >= D                      (D = k-th dot so far)
+//   L2       xx - 2 dot <= T          =>   dot >= ceil((min xx - T) / 2)
+//   angular  dot / xn >= P            =>   dot >= ceil(P * (P >= 0 ? min xn : max xn))
+// A bound beyond the bias range is clamped conservatively, or -- if it would
+// need a bias above the maximum -- its 32-column chunk is flagged
+// "exceptional" and every element of the chunk takes the exact test.
 //
-// Reference semantics being accelerated: _core.pyx:301-330 (_scan_i8), the
-// pair kernel _core.pyx:49-96.
+// Warp roles (640 threads, 1 CTA per SM, persistent over an atomic counter):
+//   warp 0  TMA producer          warp 1  MMA issuer (one lane)
+//   warp 2  TMEM allocator        warp 3  bias builder (per work unit)
+//   warps 4-19  epilogue (warp w: TMEM lanes 32*(w%4).., N/4 query columns)
+//
+// Reference semantics being accelerated: _core.pyx:301-330 (_scan_i8), pair
+// kernel _core.pyx:49-96.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+
+#include <cstdlib>
 
 #include "qa_common.cuh"
 #include "qa_internal.h"
@@ -36,13 +53,16 @@ namespace {
 
 constexpr int kBlockM = 128;
 constexpr int kThreads = 640;
+constexpr int kBiasWarp = 3;
 constexpr int kEpiWarp0 = 4;
 constexpr int kEpiThreads = 512;
 constexpr int kStageCap = 2048;  // survivors staged in smem per work unit
 constexpr int kEpiBarrier = 1;   // named barrier id for the epilogue warps
-// try_wait suspend-time hint: a waiting warp sleeps (instead of spinning and
-// stealing issue slots from the epilogue) until the phase completes or this
-// many ns pass
+constexpr int kBiasK = 32;       // K of the bias MMA (int8 columns)
+constexpr int kBiasA = 127;      // constant of the bias A tile
+constexpr int kSMin = -128 * kBiasK;  // digit-sum range
+constexpr int kSMax = 127 * kBiasK;
+// try_wait suspend-time hint for the epilogue warps' waits (ns)
 constexpr int kWaitHintNs = 20000;
 
 // ------------------------------------------------------------------ PTX --
@@ -92,15 +112,21 @@ __device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity) {
     return ok != 0;
 }
 
-// Wait with nanosleep backoff: for the single-thread producer / MMA roles,
-// which otherwise spin and steal issue slots from the epilogue warps that
-// share their SM sub-partition.
+// Wait with nanosleep backoff, for the single-thread roles (producer, MMA,
+// bias), which would otherwise spin and steal issue slots from the epilogue
+// warps sharing their SM sub-partition.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
     if (mbar_try(bar, parity)) return;
-    uint32_t ns = 32;
+    uint32_t ns = 16;
     while (!mbar_try(bar, parity)) {
         __nanosleep(ns);
-        ns = ns < 256 ? ns * 2 : 256;
+        ns = ns < 64 ? ns * 2 : 64;
+    }
+}
+
+// Pure polling wait for the latency-critical MMA issuer.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
+    while (!mbar_try(bar, parity)) {
     }
 }
 
@@ -122,6 +148,11 @@ __device__ __forceinline__ void tc_fence_before() {
 }
 __device__ __forceinline__ void tc_fence_after() {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// generic-proxy smem writes -> visible to the tensor core (async proxy)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 __device__ __forceinline__ void tc_commit(uint64_t *bar) {
@@ -147,29 +178,24 @@ __device__ __forceinline__ void tmem_wait() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// tcgen05.ld without the wait: the registers are valid only after tmem_wait().
-__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, int32_t (&v)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32"
-        " {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15,"
-        " %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31},"
-        " [%32];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
-          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
-          "=r"(v[31])
-        : "r"(taddr)
-        : "memory");
-}
-
 // tcgen05.ld of C (16 or 32) consecutive accumulator columns of this warp's
-// 32 TMEM lanes; valid after tmem_wait().
+// 32 TMEM lanes; the registers are valid after tmem_wait().
 template <int C>
 __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, int32_t (&v)[C]) {
     if constexpr (C == 32) {
-        tmem_ld32_async(taddr, v);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32"
+            " {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15,"
+            " %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31},"
+            " [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+              "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+              "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]),
+              "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+              "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr)
+            : "memory");
     } else {
         static_assert(C == 16, "16 or 32 columns");
         asm volatile(
@@ -184,55 +210,10 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, int32_t (&v)[C]) {
     }
 }
 
-__device__ __forceinline__ int4 lds128(uint32_t addr) {
-    int4 r;
-    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "r"(addr));
-    return r;
-}
-
 __device__ __forceinline__ int32_t lds32(uint32_t addr) {
     int32_t r;
     asm volatile("ld.shared.b32 %0, [%1];" : "=r"(r) : "r"(addr));
     return r;
-}
-
-__device__ __forceinline__ void sts32(uint32_t addr, int32_t v) {
-    asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ void sts128(uint32_t addr, int32_t a, int32_t b, int32_t c, int32_t d) {
-    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
-                 "r"(d)
-                 : "memory");
-}
-
-template <typename T, typename Op>
-__device__ __forceinline__ T warp_reduce(T v, Op op) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
-
-__device__ __forceinline__ int32_t clamp_i64(long long v) {
-    return v > INT32_MAX ? INT32_MAX : (v < INT32_MIN ? INT32_MIN : (int32_t)v);
-}
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32"
-        " {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15,"
-        " %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31},"
-        " [%32];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
-          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
-          "=r"(v[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
 __device__ __forceinline__ void epi_barrier() {
@@ -258,6 +239,23 @@ __host__ __device__ constexpr uint32_t make_idesc(int N) {
            ((uint32_t)(kBlockM >> 4) << 24);
 }
 
+__device__ __forceinline__ int32_t clamp_i64(long long v) {
+    return v > INT32_MAX ? INT32_MAX : (v < INT32_MIN ? INT32_MIN : (int32_t)v);
+}
+
+// 1 when any of v[0..C) is >= 0: sign bit of the AND of all values
+template <int C>
+__device__ __forceinline__ bool any_nonneg(const int32_t (&v)[C]) {
+    int32_t r[C / 2];
+#pragma unroll
+    for (int i = 0; i < C / 2; ++i) r[i] = v[2 * i] & v[2 * i + 1];
+#pragma unroll
+    for (int w = C / 2; w > 1; w >>= 1)
+#pragma unroll
+        for (int i = 0; i < w / 2; ++i) r[i] = r[2 * i] & r[2 * i + 1];
+    return r[0] >= 0;
+}
+
 struct Staged {
     int32_t qloc;
     int32_t sq;
@@ -274,6 +272,7 @@ struct Params {
     int kchunks;            // kdim / SW
     int stages;
     int b_slots;            // 1 or 2 query-tile buffers
+    int experiment;         // diagnostics only (QA_B200_EXPERIMENT); 0 in production
     int *sched;
 };
 
@@ -295,12 +294,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the query tile is double-buffered across work units when two copies fit
     // in 64 KiB, else single-buffered (one MMA bubble per unit switch)
     const int bslots = p.b_slots;
-    Staged *stage_buf = (Staged *)(sB + (size_t)bslots * b_bytes);
-    int32_t *thr_s = (int32_t *)(stage_buf + kStageCap);
-    int32_t *qcnt = thr_s + N;
-    int32_t *qbase = qcnt + N;
-    int32_t *bnd_s = qbase + N;  // [8 epilogue warps][N/2] per-warp column bounds
-    uint64_t *bars = (uint64_t *)(bnd_s + 4 * N);
+    unsigned char *sAbias = sB + (size_t)bslots * b_bytes;          // [128][32] = 127
+    unsigned char *sBbias = sAbias + kBlockM * kBiasK;              // [2][N][32] digits
+    Staged *stage_all = (Staged *)(sBbias + 2 * N * kBiasK);        // [2][kStageCap]
+    int32_t *thr_all = (int32_t *)(stage_all + 2 * kStageCap);      // [2][N] thresholds
+    int32_t *bias_s = thr_all + 2 * N;                              // [2][N] bias_q
+    int32_t *exc_s = bias_s + 2 * N;                                // [2][N/32] flags
+    int32_t *qcnt_all = exc_s + 2 * (N / 32);                       // [2][N] staged per query
+    int32_t *qbase = qcnt_all + 2 * N;                              // [N] (flush warp)
+    uint64_t *bars = (uint64_t *)(qbase + N);
     uint64_t *a_full = bars;
     uint64_t *a_empty = a_full + p.stages;
     uint64_t *b_full = a_empty + p.stages;
@@ -309,9 +311,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *acc_empty = acc_full + 2;
     uint64_t *unit_full = acc_empty + 2;
     uint64_t *unit_empty = unit_full + 2;
-    int32_t *unit_id = (int32_t *)(unit_empty + 2);
+    uint64_t *bias_full = unit_empty + 2;
+    uint64_t *bias_empty = bias_full + 2;
+    uint64_t *stage_full = bias_empty + 2;
+    uint64_t *stage_free = stage_full + 2;
+    int32_t *unit_id = (int32_t *)(stage_free + 2);
     uint32_t *tmem_base_s = (uint32_t *)(unit_id + 2);
-    int32_t *stage_n = (int32_t *)(tmem_base_s + 1);
+    int32_t *stage_n_all = (int32_t *)(tmem_base_s + 1);  // [2]
+    constexpr int kEpiWarps = kEpiThreads / 32;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
@@ -322,11 +329,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(b_full + s, 1);
             mbar_init(b_empty + s, 1);
             mbar_init(acc_full + s, 1);
-            mbar_init(acc_empty + s, kEpiThreads / 32);
+            mbar_init(acc_empty + s, kEpiWarps);
             mbar_init(unit_full + s, 1);
-            mbar_init(unit_empty + s, 2);
+            // MMA, bias warp, flush warp and every epilogue warp read unit_id
+            mbar_init(unit_empty + s, 3 + kEpiWarps);
+            mbar_init(bias_full + s, 1);
+            mbar_init(bias_empty + s, 1 + kEpiWarps);  // MMA commit + epilogue warps
+            mbar_init(stage_full + s, kEpiWarps);
+            mbar_init(stage_free + s, 1);               // flush warp
+            stage_n_all[s] = 0;
         }
-        *stage_n = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0 && lane == 0) {
@@ -339,7 +351,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                      "n"(2 * N));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    for (int i = threadIdx.x; i < N; i += kThreads) qcnt[i] = 0;
+    // constant bias A tile (every byte 127: any K-major layout reads the same)
+    for (int i = threadIdx.x; i < kBlockM * kBiasK / 4; i += kThreads)
+        reinterpret_cast<int32_t *>(sAbias)[i] = 0x7f7f7f7f;
+    for (int i = threadIdx.x; i < 2 * N; i += kThreads) qcnt_all[i] = 0;
+    fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -389,6 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         // =============================== MMA issuer =====================
         constexpr uint32_t idesc = make_idesc(N);
+        const uint32_t abias = smem_u32(sAbias);
         int stage = 0;
         uint32_t aph = 0;
         int acc = 0;
@@ -396,22 +413,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int it = 0;; ++it) {
             const int slot = it & 1;
             const uint32_t ph = (it >> 1) & 1;
-            mbar_wait_sleep(unit_full + slot, ph);
+            mbar_wait_spin(unit_full + slot, ph);
             const int32_t u = unit_id[slot];
             __syncwarp();
+            if (lane == 0) mbar_arrive(unit_empty + slot);
             if (u < 0) break;
             const int64_t b = u / p.n_qtiles;
             const int64_t tile0 = b * p.tiles_per_unit;
             const int64_t tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
             const int bslot = it % bslots;
-            mbar_wait_sleep(b_full + bslot, (uint32_t)(it / bslots) & 1);
+            mbar_wait_spin(b_full + bslot, (uint32_t)(it / bslots) & 1);
+            mbar_wait_spin(bias_full + slot, ph);
             const uint32_t bbase = smem_u32(sB + (size_t)bslot * b_bytes);
+            const uint32_t bbias = smem_u32(sBbias + slot * N * kBiasK);
             for (int64_t tile = tile0; tile < tile1; ++tile) {
-                mbar_wait_sleep(acc_empty + acc, accph ^ 1);
+                mbar_wait_spin(acc_empty + acc, accph ^ 1);
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + (uint32_t)(acc * N);
                 for (int c = 0; c < p.kchunks; ++c) {
-                    mbar_wait_sleep(a_full + stage, aph);
+                    mbar_wait_spin(a_full + stage, aph);
                     tc_fence_after();
                     if (lane == 0) {
                         const uint32_t abase = smem_u32(sA + (size_t)stage * a_stage_bytes);
@@ -430,7 +450,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         aph ^= 1;
                     }
                 }
-                if (lane == 0) tc_commit(acc_full + acc);
+                if (lane == 0) {
+                    // + bias_q on every row: constant A (127) x per-query digits
+                    tc_mma_i8(tmem_d, make_desc<32>(abias), make_desc<32>(bbias), idesc, 1u);
+                    tc_commit(acc_full + acc);
+                }
                 __syncwarp();
                 if (++acc == 2) {
                     acc = 0;
@@ -439,21 +463,156 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (lane == 0) {
                 tc_commit(b_empty + bslot);
-                mbar_arrive(unit_empty + slot);
+                tc_commit(bias_empty + slot);
             }
             __syncwarp();
         }
+    } else if (warp == kBiasWarp) {
+        // =============================== bias builder ===================
+        // Per work unit and query column: the bound B_q (see header), the
+        // digit sum S_q = ceil(-B_q / 127) clamped to [kSMin, kSMax] (a bias
+        // that would need more than kSMax flags its 32-column chunk), the
+        // digits (S_q spread over 32 int8) into the bias B tile, and
+        // bias_q = 127 * S_q for the epilogue's exact re-test.
+        for (int it = 0;; ++it) {
+            const int slot = it & 1;
+            const uint32_t ph = (it >> 1) & 1;
+            mbar_wait_sleep(unit_full + slot, ph);
+            const int32_t u = unit_id[slot];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(unit_empty + slot);
+            if (u < 0) break;
+            const int64_t t = u % p.n_qtiles, b = u / p.n_qtiles;
+            const int64_t q0 = t * N;
+            const int nqt = (int)min((int64_t)N, a.nq - q0);
+            mbar_wait_sleep(bias_empty + slot, ph ^ 1);
+            // norm range of the unit's rows (per-tile ranges, precomputed)
+            float nlo = INFINITY, nhi = -INFINITY;
+            int32_t xlo = INT32_MAX;
+            const bool filtered = (a.mode == 0 || a.mode == 3);
+            if (filtered && M != kIP) {
+                const int64_t gt0 = (a.r_lo >> 7) + b * p.tiles_per_unit;
+                const int64_t gt1 = (a.r_lo >> 7) + min(p.n_tiles, (b + 1) * p.tiles_per_unit);
+                for (int64_t g = gt0 + lane; g < gt1; g += 32) {
+                    if constexpr (M == kL2) {
+                        xlo = min(xlo, __ldg(a.grp_lo + g));
+                    } else {
+                        nlo = fminf(nlo, __int_as_float(__ldg(a.grp_lo + g)));
+                        nhi = fmaxf(nhi, __int_as_float(__ldg(a.grp_hi + g)));
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    xlo = min(xlo, __shfl_xor_sync(0xffffffffu, xlo, o));
+                    nlo = fminf(nlo, __shfl_xor_sync(0xffffffffu, nlo, o));
+                    nhi = fmaxf(nhi, __shfl_xor_sync(0xffffffffu, nhi, o));
+                }
+            }
+            int32_t *bias_out = bias_s + slot * N;
+            int32_t *thr_out = thr_all + slot * N;
+            int32_t *digits_out = reinterpret_cast<int32_t *>(sBbias + slot * N * kBiasK);
+            for (int i = 0; i < N / 32; ++i) {
+                const int q = i * 32 + lane;
+                int S = kSMin;  // padded columns: most negative bias
+                bool exc = false;
+                // thresholds for the exact test; padded columns never pass
+                thr_out[q] = (filtered && q < nqt)
+                                 ? __ldg(a.thr + q0 + q)
+                                 : ((M == kIP) ? INT32_MAX : (M == kL2 ? INT32_MIN : 0x7fc00000));
+                if (!filtered) {
+                    S = 0;  // dense / diagnostic passes: plain dots
+                } else if (q < nqt) {
+                    const int32_t T = __ldg(a.thr + q0 + q);
+                    long long B;  // necessary condition dot >= B
+                    if constexpr (M == kIP) {
+                        B = T;
+                    } else if constexpr (M == kL2) {
+                        B = ((long long)xlo - (long long)T + 1) >> 1;
+                    } else {
+                        const float P = __int_as_float(T);
+                        const float w = P >= 0.f ? nlo : nhi;
+                        const float bf = __fmul_rd(P, w);  // toward -inf: conservative
+                        B = bf >= 4.0e9f ? (long long)4000000000LL
+                                         : (bf <= -4.0e9f ? (long long)-4000000000LL
+                                                          : (long long)ceilf(bf));
+                    }
+                    // smallest S with 127*S >= -B
+                    const long long nb = -B;
+                    long long s = nb >= 0 ? (nb + kBiasA - 1) / kBiasA : -((-nb) / kBiasA);
+                    if (s > kSMax) {
+                        s = kSMax;
+                        exc = true;
+                    }
+                    if (s < kSMin) s = kSMin;
+                    S = (int)s;
+                }
+                bias_out[q] = kBiasA * S;
+                // spread S over 32 int8 digits: base + (j < rem)
+                const int base = (S >= 0) ? S / kBiasK : -((-S + kBiasK - 1) / kBiasK);
+                const int rem = S - base * kBiasK;  // 0 .. 31
+                const uint32_t b8 = (uint32_t)(base & 0xff);
+                const uint32_t b8p = (uint32_t)((base + 1) & 0xff);
+#pragma unroll
+                for (int w = 0; w < kBiasK / 4; ++w) {
+                    uint32_t word = 0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        word |= ((4 * w + j) < rem ? b8p : b8) << (8 * j);
+                    digits_out[q * (kBiasK / 4) + w] = (int32_t)word;
+                }
+                const unsigned eb = __ballot_sync(0xffffffffu, exc);
+                if (lane == 0) exc_s[slot * (N / 32) + i] = eb != 0;
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bias_full + slot);
+        }
+    } else if (warp == 2) {
+        // =============================== survivor flush =================
+        // Drains one work unit's staging slot while the epilogue warps
+        // already fill the other: one atomic per (query, unit) reserves space
+        // in the query's global candidate list, then the staged survivors
+        // are copied.  The epilogue never waits on global atomics.
+        for (int it = 0;; ++it) {
+            const int slot = it & 1;
+            const uint32_t ph = (it >> 1) & 1;
+            mbar_wait_sleep(unit_full + slot, ph);
+            const int32_t u = unit_id[slot];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(unit_empty + slot);
+            if (u < 0) break;
+            const int64_t q0 = (u % p.n_qtiles) * N;
+            mbar_wait_sleep(stage_full + slot, ph);
+            if (a.mode == 0) {
+                int32_t *qc = qcnt_all + slot * N;
+                const Staged *sb = stage_all + slot * kStageCap;
+                const int ns = min(stage_n_all[slot], kStageCap);
+                for (int q = lane; q < N; q += 32) {
+                    const int c = qc[q];
+                    if (c > 0) {
+                        qbase[q] = atomicAdd(a.ccount + q0 + q, c);
+                        qc[q] = 0;
+                    }
+                }
+                __syncwarp();
+                for (int e = lane; e < ns; e += 32) {
+                    const Staged s = sb[e];
+                    const int32_t dst = qbase[s.qloc] + s.sq;
+                    if (dst < a.cap) a.cand[(q0 + s.qloc) * a.cap + dst] = Cand{s.row, s.dot};
+                }
+                __syncwarp();
+                if (lane == 0) stage_n_all[slot] = 0;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(stage_free + slot);
+        }
     } else if (warp >= kEpiWarp0) {
         // =============================== epilogue =======================
-        // 16 warps: warp w reads TMEM lane quarter (w % 4) -- its 32 database
-        // rows -- and column block (w - 4) / 4 of kCB = N/4 queries.
         constexpr int kCB = N / 4;                 // columns per warp
         constexpr int kC = kCB < 32 ? kCB : 32;    // columns per TMEM load
         const int ew = warp - kEpiWarp0;           // 0..15
         const int quarter = warp & 3;
-        const int cblk = ew >> 2;
-        const int col0 = cblk * kCB;               // first column of this warp
-        const int etid = threadIdx.x - kEpiWarp0 * 32;
+        const int col0 = (ew >> 2) * kCB;          // first column of this warp
         int acc = 0;
         uint32_t accph = 0;
         for (int it = 0;; ++it) {
@@ -461,47 +620,60 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t ph = (it >> 1) & 1;
             mbar_wait(unit_full + slot, ph);
             const int32_t u = unit_id[slot];
-            epi_barrier();
-            if (etid == 0) mbar_arrive(unit_empty + slot);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(unit_empty + slot);
             if (u < 0) break;
             const int64_t t = u % p.n_qtiles, b = u / p.n_qtiles;
             const int64_t q0 = t * N;
             const int nqt = (int)min((int64_t)N, a.nq - q0);
-            for (int i = etid; i < N && a.mode == 0; i += kEpiThreads) {
-                int32_t v;
-                if (i < nqt) {
-                    v = __ldg(a.thr + q0 + i);
-                } else {
-                    v = (M == kIP) ? INT32_MAX : (M == kL2 ? INT32_MIN : 0x7fc00000);
-                }
-                thr_s[i] = v;
-            }
-            epi_barrier();
+            // this unit's bias, thresholds and exception flags; a free
+            // staging slot (the flush warp drained its previous use)
+            mbar_wait(bias_full + slot, ph);
+            mbar_wait(stage_free + slot, ph ^ 1);
+            int32_t *stage_n = stage_n_all + slot;
+            int32_t *qcnt = qcnt_all + slot * N;
+            Staged *stage_buf = stage_all + slot * kStageCap;
             const int64_t tile0 = b * p.tiles_per_unit;
             const int64_t tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
-            const uint32_t thr_addr = smem_u32(thr_s);
-            // per-warp column bounds (IP uses the thresholds directly)
-            const uint32_t bnd_addr = (M == kIP) ? thr_addr + 4u * (uint32_t)col0
-                                                 : smem_u32(bnd_s + ew * kCB);
-            // column chunks this warp actually has queries for
+            const uint32_t thr_addr = smem_u32(thr_all + slot * N);
+            const uint32_t bias_addr = smem_u32(bias_s + slot * N);
             const int nch = max(0, min(kCB / kC, (nqt - col0 + kC - 1) / kC));
-            // 32-bit row arithmetic (n <= INT32_MAX is enforced on the host)
+            // exceptional 32-column chunks of this warp
+            uint32_t excm = 0;
+            for (int ci = 0; ci < kCB / kC; ++ci)
+                if (exc_s[slot * (N / 32) + (col0 + ci * kC) / 32]) excm |= 1u << ci;
             const int32_t r_hi = (int32_t)a.r_hi;
             int32_t wrow0 = (int32_t)(a.r_lo + tile0 * kBlockM) + quarter * 32;
             const int ntl = (int)(tile1 - tile0);
-            if (a.mode != 0) {
-                // dense / diagnostic passes: every dot is written out
-                for (int ti = 0; ti < ntl; ++ti, wrow0 += kBlockM) {
-                    const int32_t row = wrow0 + lane;
-                    mbar_wait(acc_full + acc, accph);
-                    tc_fence_after();
-                    const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) +
-                                           (uint32_t)(acc * N) + (uint32_t)col0;
+            // the row's norm for the exact test, prefetched one tile ahead
+            int32_t nx_norm = 0;
+            if (a.mode == 0 && M != kIP && ntl > 0 && wrow0 + lane < r_hi)
+                nx_norm = (M == kL2) ? __ldg(a.db_sqnorm + wrow0 + lane)
+                                     : __float_as_int(__ldg(a.db_norm + wrow0 + lane));
+            for (int ti = 0; ti < ntl; ++ti, wrow0 += kBlockM) {
+                const int32_t row = wrow0 + lane;
+                const bool valid = row < r_hi;
+                const int32_t row_norm = nx_norm;
+                if (a.mode == 0 && M != kIP && ti + 1 < ntl && row + kBlockM < r_hi)
+                    nx_norm = (M == kL2) ? __ldg(a.db_sqnorm + row + kBlockM)
+                                         : __float_as_int(__ldg(a.db_norm + row + kBlockM));
+                mbar_wait(acc_full + acc, accph);
+                tc_fence_after();
+                const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) +
+                                       (uint32_t)(acc * N) + (uint32_t)col0;
+                if (a.mode == 1 || a.mode == 2 || p.experiment != 0) {
+#pragma unroll 1
                     for (int ci = 0; ci < nch; ++ci) {
                         int32_t cur[kC];
+                        if (p.experiment == 2) continue;  // no TMEM read at all
                         tmem_ld_cols<kC>(tbase + (uint32_t)(ci * kC), cur);
                         tmem_wait();
-                        if (row >= r_hi) continue;
+                        if (p.experiment == 1) {          // TMEM read only
+                            if (cur[0] == 0x12345678 && cur[31 % kC] == 0x7654321) *stage_n = 0;
+                            continue;
+                        }
+                        // dense / diagnostic passes (bias 0): every dot out
+                        if (!valid) continue;
 #pragma unroll
                         for (int j = 0; j < kC; ++j) {
                             const int c = col0 + ci * kC + j;
@@ -520,140 +692,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                         acc = 0;
                         accph ^= 1;
                     }
+                    continue;
                 }
-                continue;
-            }
-            // Per-unit column constants in registers (this lane's kCB/32
-            // columns): thresholds; for angular the NaN of padded columns
-            // becomes +inf (bound INT_MAX) and the sign picks min/max norm.
-            constexpr int kPL = (kCB + 31) / 32;
-            int32_t thr_r[kPL];
+                // The whole tile slice of this warp goes to registers first and
+                // the accumulator is released at once: the MMA can refill it
+                // while this warp filters (survivor bursts in one warp then no
+                // longer hold back the tensor core).
+                int32_t vals[kCB / kC][kC];
 #pragma unroll
-            for (int i = 0; i < kPL; ++i) {
-                const int c = i * 32 + lane;
-                thr_r[i] = c < kCB ? lds32(thr_addr + 4u * (uint32_t)(col0 + c)) : 0;
-                if constexpr (M == kAngular)
-                    if (__int_as_float(thr_r[i]) != __int_as_float(thr_r[i]))
-                        thr_r[i] = 0x7f800000;  // +inf
-            }
-            // prefetch of the first tile's per-row / per-group scalars
-            int32_t nx_a = 0, nx_lo = 0, nx_hi = 0;
-            if (ntl > 0) {
-                const int32_t row = wrow0 + lane;
-                if constexpr (M == kL2) {
-                    nx_a = row < r_hi ? __ldg(a.db_sqnorm + row) : 0;
-                    nx_lo = __ldg(a.grp_lo + (wrow0 >> 5));
-                } else if constexpr (M == kAngular) {
-                    nx_a = row < r_hi ? __float_as_int(__ldg(a.db_norm + row)) : 0;
-                    nx_lo = __ldg(a.grp_lo + (wrow0 >> 5));
-                    nx_hi = __ldg(a.grp_hi + (wrow0 >> 5));
-                }
-            }
-            for (int ti = 0; ti < ntl; ++ti, wrow0 += kBlockM) {
-                const int32_t row = wrow0 + lane;
-                const bool valid = row < r_hi;
-                const int32_t rv = nx_a, glo = nx_lo, ghi = nx_hi;
-                if (ti + 1 < ntl) {  // prefetch the next tile's scalars
-                    const int32_t nrow = row + kBlockM;
-                    if constexpr (M == kL2) {
-                        nx_a = nrow < r_hi ? __ldg(a.db_sqnorm + nrow) : 0;
-                        nx_lo = __ldg(a.grp_lo + ((wrow0 + kBlockM) >> 5));
-                    } else if constexpr (M == kAngular) {
-                        nx_a = nrow < r_hi ? __float_as_int(__ldg(a.db_norm + nrow)) : 0;
-                        nx_lo = __ldg(a.grp_lo + ((wrow0 + kBlockM) >> 5));
-                        nx_hi = __ldg(a.grp_hi + ((wrow0 + kBlockM) >> 5));
-                    }
-                }
-                if constexpr (M != kIP) {
-                    // Necessary integer condition per (warp rows, column):
-                    //   L2:      xx_i - 2 dot <= T  =>  dot >= ceil((min xx - T) / 2)
-                    //   angular: dot / xn_i >= P    =>  dot >= ceil(P * (P >= 0 ? min xn
-                    //                                                          : max xn))
-                    // with the product rounded toward -inf (conservative).  The
-                    // norm range of the warp's 32 rows comes precomputed (a
-                    // superset range when rows past r_hi share the group).  Rows
-                    // sorted by norm at index build make it, hence the bound,
-                    // tight; the exact per-row test runs on the rare survivors.
-#pragma unroll
-                    for (int i = 0; i < kPL; ++i) {
-                        int32_t B;
-                        if constexpr (M == kL2) {
-                            const long long num = (long long)glo - (long long)thr_r[i];
-                            B = clamp_i64((num + 1) >> 1);
-                        } else {
-                            const float P = __int_as_float(thr_r[i]);
-                            B = __float2int_ru(__fmul_rd(P, P >= 0.f ? __int_as_float(glo)
-                                                                     : __int_as_float(ghi)));
-                        }
-                        if (i * 32 + lane < kCB) sts32(bnd_addr + 4u * (uint32_t)(i * 32 + lane), B);
-                    }
-                    __syncwarp();
-                }
-                mbar_wait(acc_full + acc, accph);
-                tc_fence_after();
-                const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) +
-                                       (uint32_t)(acc * N) + (uint32_t)col0;
-#pragma unroll 1
-                for (int ci = 0; ci < nch; ++ci) {
-                    int32_t cur[kC];
-                    tmem_ld_cols<kC>(tbase + (uint32_t)(ci * kC), cur);
-                    tmem_wait();
-                    // fast path: one integer compare per (row, query), one
-                    // accumulated predicate per group of 8 columns
-                    bool hit[kC / 8];
-#pragma unroll
-                    for (int h = 0; h < kC / 8; ++h) {
-                        const int4 b0 = lds128(bnd_addr + 4u * (uint32_t)(ci * kC + 8 * h));
-                        const int4 b1 = lds128(bnd_addr + 4u * (uint32_t)(ci * kC + 8 * h + 4));
-                        const int32_t *c8 = cur + 8 * h;
-                        hit[h] = (c8[0] >= b0.x) | (c8[1] >= b0.y) | (c8[2] >= b0.z) |
-                                 (c8[3] >= b0.w) | (c8[4] >= b1.x) | (c8[5] >= b1.y) |
-                                 (c8[6] >= b1.z) | (c8[7] >= b1.w);
-                    }
-                    bool anyhit = false;
-#pragma unroll
-                    for (int h = 0; h < kC / 8; ++h) anyhit |= hit[h];
-                    if (!(anyhit && valid)) continue;
-                    // slow path (lanes with a candidate only): per hit group an
-                    // 8-bit column mask; the value of a set bit is picked with a
-                    // select chain (no dynamic register indexing); exact test.
-                    const int32_t xx = (M == kL2) ? rv : 0;
-                    const float inv_xn = (M == kAngular) ? __frcp_rn(__int_as_float(rv)) : 0.f;
-#pragma unroll
-                    for (int h = 0; h < kC / 8; ++h) {
-                        if (!hit[h]) continue;
-                        const int32_t *c8 = cur + 8 * h;
-                        const int4 b0 = lds128(bnd_addr + 4u * (uint32_t)(ci * kC + 8 * h));
-                        const int4 b1 = lds128(bnd_addr + 4u * (uint32_t)(ci * kC + 8 * h + 4));
-                        uint32_t m8 =
-                            ((uint32_t)(c8[0] >= b0.x) << 0) | ((uint32_t)(c8[1] >= b0.y) << 1) |
-                            ((uint32_t)(c8[2] >= b0.z) << 2) | ((uint32_t)(c8[3] >= b0.w) << 3) |
-                            ((uint32_t)(c8[4] >= b1.x) << 4) | ((uint32_t)(c8[5] >= b1.y) << 5) |
-                            ((uint32_t)(c8[6] >= b1.z) << 6) | ((uint32_t)(c8[7] >= b1.w) << 7);
-                        while (m8) {
-                            const int j = __ffs(m8) - 1;
-                            m8 &= m8 - 1;
-                            int32_t v = c8[0];
-#pragma unroll
-                            for (int jj = 1; jj < 8; ++jj) v = (j == jj) ? c8[jj] : v;
-                            const int qloc = col0 + ci * kC + 8 * h + j;
-                            if constexpr (M != kIP) {
-                                const int32_t T = lds32(thr_addr + 4u * (uint32_t)qloc);
-                                if (!passes<M>(v, T, xx, inv_xn)) continue;
-                            }
-                            const int e = atomicAdd(stage_n, 1);
-                            if (e < kStageCap) {
-                                const int sq = atomicAdd(qcnt + qloc, 1);
-                                stage_buf[e] = Staged{qloc, sq, row, v};
-                            } else {
-                                // staging full: direct append (slow, rare)
-                                const int32_t s = atomicAdd(a.ccount + q0 + qloc, 1);
-                                if (s < a.cap)
-                                    a.cand[(q0 + qloc) * a.cap + s] = Cand{row, v};
-                            }
-                        }
-                    }
-                }
+                for (int ci = 0; ci < kCB / kC; ++ci)
+                    tmem_ld_cols<kC>(tbase + (uint32_t)(ci * kC), vals[ci]);
+                tmem_wait();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(acc_empty + acc);
@@ -661,29 +710,87 @@ __global__ void __launch_bounds__(kThreads, 1)
                     acc = 0;
                     accph ^= 1;
                 }
-            }
-            {
-                // ---- flush the unit's staged survivors ----
-                epi_barrier();
-                for (int i = etid; i < N; i += kEpiThreads) {
-                    int c = qcnt[i];
-                    if (c > 0) {
-                        qbase[i] = atomicAdd(a.ccount + q0 + i, c);
-                        qcnt[i] = 0;
+#pragma unroll
+                for (int ci = 0; ci < kCB / kC; ++ci) {
+                    if (ci >= nch) break;
+                    const int32_t(&cur)[kC] = vals[ci];
+                    if (a.mode == 3) {
+                        // masked dense (survivor-dense early rounds): every
+                        // element gets its slot; rows failing the bound are
+                        // marked row = -1 (no atomics at all)
+                        if (!valid) continue;
+                        const bool exc = (excm >> ci) & 1u;
+#pragma unroll
+                        for (int j = 0; j < kC; ++j) {
+                            const int c = col0 + ci * kC + j;
+                            if (c >= nqt) continue;
+                            const int32_t dot = (int32_t)((uint32_t)cur[j] -
+                                                          (uint32_t)lds32(bias_addr + 4u * (uint32_t)c));
+                            const bool keep = cur[j] >= 0 || exc;
+                            a.cand[(q0 + c) * a.cap + (row - (int32_t)a.r_lo)] =
+                                keep ? Cand{row, dot} : Cand{-1, 0};
+                        }
+                        continue;
+                    }
+                    // fast path: is any biased value >= 0 (bound possibly met)?
+                    // one AND per 8 columns, then the sign of their AND
+                    int32_t gand[kC / 8];
+#pragma unroll
+                    for (int h = 0; h < kC / 8; ++h) {
+                        const int32_t *c8 = cur + 8 * h;
+                        gand[h] = (c8[0] & c8[1] & c8[2]) & (c8[3] & c8[4] & c8[5]) & (c8[6] & c8[7]);
+                    }
+                    int32_t all = gand[0];
+#pragma unroll
+                    for (int h = 1; h < kC / 8; ++h) all &= gand[h];
+                    const bool exc = (excm >> ci) & 1u;
+                    if (!((all >= 0 || exc) && valid)) continue;
+                    // slow path (lanes with a candidate only), only for groups of
+                    // 8 columns with a non-negative value; a set bit's value is
+                    // picked with a select chain (no dynamic register
+                    // indexing); exact test on the dot.
+                    const int32_t xx = (M == kL2) ? row_norm : 0;
+                    const float inv_xn = (M == kAngular) ? __frcp_rn(__int_as_float(row_norm)) : 0.f;
+#pragma unroll
+                    for (int h = 0; h < kC / 8; ++h) {
+                        if (gand[h] < 0 && !exc) continue;
+                        const int32_t *c8 = cur + 8 * h;
+                        uint32_t m8 = exc ? 0xffu : 0u;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) m8 |= (uint32_t)(c8[j] >= 0) << j;
+                        while (m8) {
+                            const int j = __ffs(m8) - 1;
+                            m8 &= m8 - 1;
+                            int32_t v = c8[0];
+#pragma unroll
+                            for (int jj = 1; jj < 8; ++jj) v = (j == jj) ? c8[jj] : v;
+                            const int qloc = col0 + ci * kC + 8 * h + j;
+                            const int32_t dot =
+                                (int32_t)((uint32_t)v - (uint32_t)lds32(bias_addr + 4u * (uint32_t)qloc));
+                            const int32_t T = lds32(thr_addr + 4u * (uint32_t)qloc);
+                            if (!passes<M>(dot, T, xx, inv_xn)) continue;
+                            const int e = atomicAdd(stage_n, 1);
+                            if (e < kStageCap) {
+                                const int sq = atomicAdd(qcnt + qloc, 1);
+                                stage_buf[e] = Staged{qloc, sq, row, dot};
+                            } else {
+                                // staging full: direct append (slow, rare)
+                                const int32_t s = atomicAdd(a.ccount + q0 + qloc, 1);
+                                if (s < a.cap) a.cand[(q0 + qloc) * a.cap + s] = Cand{row, dot};
+                            }
+                        }
                     }
                 }
-                epi_barrier();
-                const int ns = min(*stage_n, kStageCap);
-                for (int e = etid; e < ns; e += kEpiThreads) {
-                    Staged s = stage_buf[e];
-                    int32_t dst = qbase[s.qloc] + s.sq;
-                    if (dst < a.cap) a.cand[(q0 + s.qloc) * a.cap + dst] = Cand{s.row, s.dot};
-                }
-                epi_barrier();
-                if (etid == 0) *stage_n = 0;
+            }
+            // this warp is done with the unit's bias / thresholds and staging
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(bias_empty + slot);
+                mbar_arrive(stage_full + slot);
             }
         }
     }
+
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {
@@ -736,16 +843,27 @@ cudaError_t launch_t(const FilterArgs &a, int *sched, cudaStream_t st) {
     p.n_qtiles = (a.nq + N - 1) / N;
     p.kchunks = (int)(a.kdim / SW);
     const int sms = num_sms();
-    int64_t tpu = (p.n_tiles * p.n_qtiles) / ((int64_t)sms * 4);
-    if (tpu < 1) tpu = 1;
-    if (tpu > 32) tpu = 32;
+    // tiles per unit: a power of two <= 32, so units stay inside one
+    // 32-tile norm-sorted block of an index laid out by qa_order_rows_by_norm
+    int64_t want = (p.n_tiles * p.n_qtiles) / ((int64_t)sms * 4);
+    int64_t tpu = 1;
+    while (tpu * 2 <= want && tpu < 32) tpu *= 2;
     p.tiles_per_unit = tpu;
     p.n_units = ((p.n_tiles + tpu - 1) / tpu) * p.n_qtiles;
     p.sched = sched;
-    p.b_slots = (2 * (size_t)N * a.kdim <= 65536) ? 2 : 1;
+    {
+        static int exp_mode = -1;
+        if (exp_mode < 0) {
+            const char *v = getenv("QA_B200_EXPERIMENT");
+            exp_mode = v ? atoi(v) : 0;
+        }
+        p.experiment = exp_mode;
+    }
+    p.b_slots =(2 * (size_t)N * a.kdim <= 65536) ? 2 : 1;
     const size_t fixed = 1024 /*align slack*/ + (size_t)p.b_slots * N * a.kdim +
-                         kStageCap * sizeof(Staged) + 7 * N * sizeof(int32_t) +
-                         256;
+                         kBlockM * kBiasK + 2 * (size_t)N * kBiasK +
+                         2 * kStageCap * sizeof(Staged) +
+                         (7 * N + 2 * (N / 32)) * sizeof(int32_t) + 256;
     const size_t budget = 227 * 1024;
     const size_t stage_bytes = (size_t)kBlockM * SW;
     // each stage also costs two 8-byte mbarriers
@@ -775,8 +893,8 @@ cudaError_t dispatch_metric(const FilterArgs &a, int *sched, cudaStream_t st) {
 
 template <int SW>
 cudaError_t dispatch_n(const FilterArgs &a, int *sched, cudaStream_t st) {
-    // Largest query tile whose double-buffered B fits (N * kdim <= 64 KiB),
-    // no larger than the query chunk needs.
+    // Largest query tile whose B buffer fits 64 KiB, no larger than the query
+    // chunk needs.
     int nmax = (int)(65536 / a.kdim);
     if (a.nq > 128 && nmax >= 256) return dispatch_metric<SW, 256>(a, sched, st);
     if (a.nq > 64 && nmax >= 128) return dispatch_metric<SW, 128>(a, sched, st);
@@ -791,6 +909,8 @@ cudaError_t launch_filter_tc(const FilterArgs &a, int *sched, cudaStream_t st) {
     if (a.kdim % 32 != 0 || a.kdim > 1024) return cudaErrorNotSupported;
     if (a.ldd % 16 != 0 || a.ldq % 16 != 0) return cudaErrorNotSupported;
     if (a.r_hi > INT32_MAX) return cudaErrorNotSupported;
+    // the biased accumulator must not wrap: |dot| + |bias| < 2^31
+    if (a.kdim > 65536) return cudaErrorNotSupported;
     if (a.kdim % 128 == 0) return dispatch_n<128>(a, sched, st);
     if (a.kdim == 64) return dispatch_n<64>(a, sched, st);
     if (a.kdim == 32) return dispatch_n<32>(a, sched, st);

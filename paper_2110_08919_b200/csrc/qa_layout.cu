@@ -15,18 +15,19 @@ namespace qa {
 
 namespace {
 
-// Tile interleave: stored tile t <- sorted tile (t * step) mod T (step
-// coprime to T), so every prefix of stored rows samples the whole norm range
-// -- the search rounds scan row prefixes and need representative samples --
-// while each 128-row tile still holds rows of nearly equal norm.  A partial
-// last tile stays last.
+// Block interleave: stored block t <- sorted block (t * step + T/2) mod T
+// (step coprime to T; blocks of 32 tiles = 4096 rows), so every prefix of
+// stored rows samples the whole norm range -- the search rounds scan row
+// prefixes and need representative samples -- while each block (and every
+// filter work unit, which never crosses a block) holds rows of nearly equal
+// norm.  A partial last block stays last.
 __global__ void interleave_tiles_kernel(const int32_t *__restrict__ sorted, int64_t n,
                                         int64_t tile, int64_t full_tiles, int64_t step,
                                         int32_t *__restrict__ perm) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int64_t t = i / tile;
-    const int64_t src_t = t < full_tiles ? (t * step) % full_tiles : t;
+    const int64_t src_t = t < full_tiles ? (t * step + full_tiles / 2) % full_tiles : t;
     perm[i] = sorted[src_t * tile + (i - t * tile)];
 }
 
@@ -55,7 +56,7 @@ __global__ void permute_rows_kernel(const int8_t *__restrict__ src, const int32_
     }
 }
 
-// one warp per 32-row group
+// one warp per 128-row tile (4 rows per lane)
 __global__ void group_ranges_kernel(int metric, const int32_t *__restrict__ sqnorm,
                                     const float *__restrict__ norm, int64_t n,
                                     int32_t *__restrict__ lo, int32_t *__restrict__ hi,
@@ -63,14 +64,23 @@ __global__ void group_ranges_kernel(int metric, const int32_t *__restrict__ sqno
     const int lane = threadIdx.x & 31;
     const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (g >= groups) return;
-    const int64_t r = g * 32 + lane;
-    const bool ok = r < n;
     if (metric == 1) {
-        int32_t v = ok ? sqnorm[r] : INT32_MAX;
+        int32_t v = INT32_MAX;
+        for (int i = 0; i < 4; ++i) {
+            const int64_t r = g * 128 + i * 32 + lane;
+            if (r < n) v = min(v, sqnorm[r]);
+        }
         for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
         if (lane == 0) lo[g] = v;
     } else {
-        float vmin = ok ? norm[r] : INFINITY, vmax = ok ? norm[r] : -INFINITY;
+        float vmin = INFINITY, vmax = -INFINITY;
+        for (int i = 0; i < 4; ++i) {
+            const int64_t r = g * 128 + i * 32 + lane;
+            if (r < n) {
+                vmin = fminf(vmin, norm[r]);
+                vmax = fmaxf(vmax, norm[r]);
+            }
+        }
         for (int o = 16; o; o >>= 1) {
             vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
             vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
@@ -111,7 +121,7 @@ cudaError_t launch_order_by_key(const int32_t *key, int64_t n, int32_t *perm, vo
     e = cub::DeviceRadixSort::SortPairs((char *)scratch + off, temp, (const uint32_t *)key,
                                         keys_out, vals_in, sorted, (int)n, 0, 32, st);
     if (e != cudaSuccess) return e;
-    const int64_t tile = 128, full = n / tile;
+    const int64_t tile = 128 * 32, full = n / tile;
     int64_t step = 1;
     if (full > 1) {
         // a step near T/phi, coprime to T: spreads consecutive stored tiles

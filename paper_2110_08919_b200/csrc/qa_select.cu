@@ -161,8 +161,11 @@ __global__ void __launch_bounds__(kWarpsMax * 32) select_kernel(SelectArgs a, in
             Entry e;
             bool keep = false;
             if (i < take) {
-                e = make_entry<M>(cd[pos + i], qq, qn, a.db_sqnorm, a.db_norm, a.row_ids);
-                keep = !full || entry_less(e, kth);
+                const Cand c = cd[pos + i];
+                if (c.row >= 0) {  // row -1: slot of a masked-dense pass, filtered out
+                    e = make_entry<M>(c, qq, qn, a.db_sqnorm, a.db_norm, a.row_ids);
+                    keep = !full || entry_less(e, kth);
+                }
             }
             const unsigned bal = __ballot_sync(0xffffffffu, keep);
             if (keep) S[ns + __popc(bal & ((1u << lane) - 1))] = e;
@@ -343,25 +346,44 @@ __global__ void __launch_bounds__(256) select_reg_kernel(SelectArgs a) {
         else
             rsentinel(t[e]);
     }
-    for (int pos = 0; pos < m; pos += 128) {
-        // k-th retained key (sentinel while fewer than k): candidates not
-        // below it cannot enter
-        const K kth = rget(t, k - 1);
+    // Candidates are scored 32 at a time; those below the current k-th key
+    // are compacted into this warp's smem stage, which is sorted and merged
+    // whenever it holds 128 (and once at the end).
+    __shared__ K stage_all[8][160];
+    K *stage = stage_all[threadIdx.x >> 5];
+    K kth = rget(t, k - 1);  // sentinel while fewer than k retained
+    int fill = 0;
+    for (int pos = 0; pos < m; pos += 32) {
+        const int i = pos + lane;
+        bool keep = false;
+        K key;
+        if (i < m) {
+            const Cand c = cd[i];
+            if (c.row >= 0) {  // row -1: slot of a masked-dense pass, filtered out
+                const Entry en = make_entry<M>(c, qq, qn, a.db_sqnorm, a.db_norm, a.row_ids);
+                to_key<M>(en, key);
+                keep = rlt(key, kth);
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) stage[fill + __popc(bal & ((1u << lane) - 1))] = key;
+        fill += __popc(bal);
+        const bool last = pos + 32 >= m;
+        while (fill >= 128 || (last && fill > 0)) {
+        __syncwarp();
+        const int ns = min(fill, 128);
         K s[4];
-        int ns = 0;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            const int i = pos + e * 32 + lane;
-            bool keep = false;
-            if (i < m) {
-                const Entry en = make_entry<M>(cd[i], qq, qn, a.db_sqnorm, a.db_norm, a.row_ids);
-                to_key<M>(en, s[e]);
-                keep = rlt(s[e], kth);
-            }
-            if (!keep) rsentinel(s[e]);
-            ns += __popc(__ballot_sync(0xffffffffu, keep));
+            if (e * 32 + lane < ns)
+                s[e] = stage[e * 32 + lane];
+            else
+                rsentinel(s[e]);
         }
-        if (ns == 0) continue;
+        __syncwarp();
+        if (fill > 128 && lane < fill - 128) stage[lane] = stage[128 + lane];
+        fill -= ns;
+        __syncwarp();
         rsort128(s);
         // reverse S (i -> 127 - i): lane -> 31 - lane, e -> 3 - e
         K r[4];
@@ -376,6 +398,8 @@ __global__ void __launch_bounds__(256) select_reg_kernel(SelectArgs a) {
 #pragma unroll
         for (int stride = 64; stride > 0; stride >>= 1) rstage(t, 256, stride);
         cur = min(k, cur + ns);
+        kth = rget(t, k - 1);
+        }
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
