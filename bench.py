@@ -327,7 +327,7 @@ def run_gpu(args):
         "filter_ms_per_step": st["filter_ms"], "select_ms_per_step": st["select_ms"],
         "filter_launches_per_step": st["filter_launches"],
         "filter_share_of_step": st["filter_ms"] / ms if ms else None,
-        "scan_stats": {key: st[key] for key in ("rounds", "launches", "retries")},
+        "scan_stats": {key: st[key] for key in ("rounds", "launches", "retries", "candidates")},
     }
     line = {
         "metric": METRIC_NAME, "value": value, "unit": "queries/s", "n_gpus": world,

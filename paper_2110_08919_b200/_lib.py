@@ -14,7 +14,9 @@ import os
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libqa_b200.so"
+# QA_B200_LIB: alternate build of the same library (A/B timing of kernel
+# variants on one box); the default is the in-tree build.
+LIB_PATH = Path(os.environ["QA_B200_LIB"]) if os.environ.get("QA_B200_LIB") else _HERE / "libqa_b200.so"
 
 QA_OK = 0
 QA_EINVAL = 1

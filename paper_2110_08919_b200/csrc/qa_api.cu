@@ -139,6 +139,15 @@ bool use_simt_filter(int64_t kdim) {
     return forced == 1 || kdim > 1024;
 }
 
+bool trace_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char *v = getenv("QA_B200_TRACE");
+        on = (v && *v && strcmp(v, "0") != 0) ? 1 : 0;
+    }
+    return on == 1;
+}
+
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
 struct ScanPlan {
@@ -216,7 +225,7 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
     Cand *cand = (Cand *)ws.cand.ptr;
     int32_t *ccount = (int32_t *)ws.ccount.ptr;
     int32_t *ovf = (int32_t *)ws.ovf.ptr;
-    int32_t *flags = (int32_t *)ws.flags.ptr;  // [0] any overflow, [1] sched counter
+    int32_t *flags = (int32_t *)ws.flags.ptr;  // [0] any overflow, [4:6) candidate counter
     QA_TRY(cudaMemsetAsync(ovf, 0, (size_t)nq * 4, st), "memset");
     QA_TRY(cudaMemsetAsync(flags, 0, 64, st), "memset");
     const bool simt = use_simt_filter(ld);
@@ -227,6 +236,7 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
     QA_TRY(launch_group_ranges(metric, db_sqnorm, db_norm, n, grp_lo, grp_hi, groups, st),
            "group ranges");
 
+    unsigned long long trace_prev = 0;
     for (int64_t c0 = 0; c0 < nq; c0 += qc) {
         const int64_t m = std::min(qc, nq - c0);
         QA_TRY(launch_init_state(state_cnt, thr, m, metric, st), "init");
@@ -263,7 +273,7 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             QA_TRY(launch_fill(ccount, m, mode != 0 ? (int32_t)(r_hi - r_lo) : 0, st), "fill");
             cudaError_t e = cudaErrorNotSupported;
             g_timer.begin(0, st);
-            if (!simt) e = launch_filter_tc(fa, flags + 1, st);
+            if (!simt) e = launch_filter_tc(fa, st);
             if (e == cudaErrorNotSupported) e = launch_filter_simt(fa, st);
             g_timer.end(st);
             QA_TRY(e, "filter");
@@ -286,11 +296,21 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             sa.thr = thr;
             sa.overflow = ovf + c0;
             sa.any_overflow = flags;
+            sa.cand_count = reinterpret_cast<unsigned long long *>(flags + 4);
             g_timer.begin(1, st);
             QA_TRY(launch_select(sa, st), "select");
             g_timer.end(st);
             g_stats.launches += 3;
             g_stats.rounds += 1;
+            if (trace_enabled()) {  // diagnostics: per-round survivors (synchronises)
+                unsigned long long cnt = 0;
+                QA_TRY(cudaMemcpyAsync(&cnt, flags + 4, 8, cudaMemcpyDeviceToHost, st), "trace");
+                QA_TRY(cudaStreamSynchronize(st), "trace");
+                std::fprintf(stderr, "qa_trace chunk=%lld rows=[%lld,%lld) mode=%d cands=%llu\n",
+                             (long long)c0, (long long)r_lo, (long long)r_hi, mode,
+                             cnt - trace_prev);
+                trace_prev = cnt;
+            }
             if (r_hi >= n) break;
             first = false;
             r_lo = r_hi;
@@ -301,9 +321,14 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
                "finalize");
         g_stats.launches += 1;
     }
-    int32_t any = 0;
-    QA_TRY(cudaMemcpyAsync(&any, flags, 4, cudaMemcpyDeviceToHost, st), "overflow check");
+    int32_t hflags[6] = {0, 0, 0, 0, 0, 0};
+    QA_TRY(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, st),
+           "overflow check");
     QA_TRY(cudaStreamSynchronize(st), "sync");
+    const int32_t any = hflags[0];
+    unsigned long long cands = 0;
+    std::memcpy(&cands, hflags + 4, sizeof(cands));
+    g_stats.candidates += (int64_t)cands;
     g_timer.accumulate(g_stats);
     overflowed->clear();
     if (any) {
@@ -610,7 +635,7 @@ int qa_debug_dots_i8(const int8_t *db, int64_t n, const int8_t *q, int64_t nq, i
     Workspace &ws = g_ws[current_device() % kMaxDevices];
     std::lock_guard<std::mutex> lock(ws.mu);
     QA_TRY(ws.flags.reserve(64), "workspace");
-    cudaError_t e = impl == 0 ? launch_filter_tc(fa, (int32_t *)ws.flags.ptr + 1, st)
+    cudaError_t e = impl == 0 ? launch_filter_tc(fa, st)
                               : launch_filter_simt(fa, st);
     QA_TRY(e, "debug dots");
     return QA_OK;

@@ -56,7 +56,7 @@ constexpr int kThreads = 640;
 constexpr int kBiasWarp = 3;
 constexpr int kEpiWarp0 = 4;
 constexpr int kEpiThreads = 512;
-constexpr int kStageCap = 2048;  // survivors staged in smem per work unit
+constexpr int kStageCapDefault = 2048;  // survivors staged in smem per work unit
 constexpr int kEpiBarrier = 1;   // named barrier id for the epilogue warps
 constexpr int kBiasK = 32;       // K of the bias MMA (int8 columns)
 constexpr int kBiasA = 127;      // constant of the bias A tile
@@ -196,8 +196,16 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, int32_t (&v)[C]) {
               "=r"(v[30]), "=r"(v[31])
             : "r"(taddr)
             : "memory");
+    } else if constexpr (C == 8) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x8.b32"
+            " {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7])
+            : "r"(taddr)
+            : "memory");
     } else {
-        static_assert(C == 16, "16 or 32 columns");
+        static_assert(C == 16, "8, 16 or 32 columns");
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32"
             " {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15},"
@@ -256,12 +264,14 @@ __device__ __forceinline__ bool any_nonneg(const int32_t (&v)[C]) {
     return r[0] >= 0;
 }
 
+// A survivor staged in shared memory: query column (8 bits), its slot among
+// the unit's survivors of that query (12 bits), row within the unit (12
+// bits), and the dot product.
 struct Staged {
-    int32_t qloc;
-    int32_t sq;
-    int32_t row;
+    uint32_t key;  // qloc | sq << 8 | rowrel << 20
     int32_t dot;
 };
+constexpr int kUnitRowsMax = 32 * kBlockM;  // rows of a work unit (<= 32 tiles)
 
 struct Params {
     FilterArgs a;
@@ -272,11 +282,25 @@ struct Params {
     int kchunks;            // kdim / SW
     int stages;
     int b_slots;            // 1 or 2 query-tile buffers
+    int stage_cap;          // survivor staging entries per slot
+    int norm_bulk;          // norm arrays 16-byte aligned (bulk-copyable)
     int experiment;         // diagnostics only (QA_B200_EXPERIMENT); 0 in production
-    int *sched;
 };
 
-template <int SW, int N, int M>
+// Work unit u -> (query tile t, row block b).  Query tiles vary fastest, so
+// the CTAs working at the same time share row blocks (L2 reuse of the
+// streamed database tiles).  Units are assigned statically: CTA i takes
+// u = i, i + grid, i + 2 grid, ... -- every role of the CTA walks the same
+// sequence on its own, so no role waits for a scheduler.
+__device__ __forceinline__ void unit_tb(const Params &p, int64_t u, int64_t &t, int64_t &b) {
+    t = u % p.n_qtiles;
+    b = u / p.n_qtiles;
+}
+
+// kFilter: the filter pass proper (mode 0); otherwise the dense, masked-dense
+// and diagnostic passes.  Separate instances keep the hot loop's register
+// allocation free of the other paths.
+template <int SW, int N, int M, bool kFilter>
 __global__ void __launch_bounds__(kThreads, 1)
     filter_tc_kernel(const __grid_constant__ CUtensorMap tm_db,
                      const __grid_constant__ CUtensorMap tm_q, const Params p) {
@@ -284,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const FilterArgs &a = p.a;
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const int64_t u_first = blockIdx.x, u_step = gridDim.x;
 
     // ---- shared memory carve-up (1024-aligned operand buffers) ----
     uintptr_t base = ((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023;
@@ -296,8 +321,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int bslots = p.b_slots;
     unsigned char *sAbias = sB + (size_t)bslots * b_bytes;          // [128][32] = 127
     unsigned char *sBbias = sAbias + kBlockM * kBiasK;              // [2][N][32] digits
-    Staged *stage_all = (Staged *)(sBbias + 2 * N * kBiasK);        // [2][kStageCap]
-    int32_t *thr_all = (int32_t *)(stage_all + 2 * kStageCap);      // [2][N] thresholds
+    const int stage_cap = p.stage_cap;
+    Staged *stage_all = (Staged *)(sBbias + 2 * N * kBiasK);        // [2][stage_cap]
+    // row norms of the unit (L2: sqnorm, angular: float bits), staged by the
+    // bias warp for the exact test
+    constexpr int kNormSlots = (M == kIP) ? 0 : 2;
+    int32_t *norm_all = (int32_t *)(stage_all + 2 * stage_cap);     // [2][kUnitRowsMax]
+    int32_t *thr_all = norm_all + kNormSlots * kUnitRowsMax;        // [2][N] thresholds
     int32_t *bias_s = thr_all + 2 * N;                              // [2][N] bias_q
     int32_t *exc_s = bias_s + 2 * N;                                // [2][N/32] flags
     int32_t *qcnt_all = exc_s + 2 * (N / 32);                       // [2][N] staged per query
@@ -309,14 +339,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *b_empty = b_full + 2;
     uint64_t *acc_full = b_empty + 2;
     uint64_t *acc_empty = acc_full + 2;
-    uint64_t *unit_full = acc_empty + 2;
-    uint64_t *unit_empty = unit_full + 2;
-    uint64_t *bias_full = unit_empty + 2;
+    uint64_t *bias_full = acc_empty + 2;
     uint64_t *bias_empty = bias_full + 2;
     uint64_t *stage_full = bias_empty + 2;
     uint64_t *stage_free = stage_full + 2;
-    int32_t *unit_id = (int32_t *)(stage_free + 2);
-    uint32_t *tmem_base_s = (uint32_t *)(unit_id + 2);
+    uint64_t *norm_full = stage_free + 2;
+    uint32_t *tmem_base_s = (uint32_t *)(norm_full + 2);
     int32_t *stage_n_all = (int32_t *)(tmem_base_s + 1);  // [2]
     constexpr int kEpiWarps = kEpiThreads / 32;
 
@@ -330,13 +358,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(b_empty + s, 1);
             mbar_init(acc_full + s, 1);
             mbar_init(acc_empty + s, kEpiWarps);
-            mbar_init(unit_full + s, 1);
-            // MMA, bias warp, flush warp and every epilogue warp read unit_id
-            mbar_init(unit_empty + s, 3 + kEpiWarps);
             mbar_init(bias_full + s, 1);
             mbar_init(bias_empty + s, 1 + kEpiWarps);  // MMA commit + epilogue warps
             mbar_init(stage_full + s, kEpiWarps);
             mbar_init(stage_free + s, 1);               // flush warp
+            mbar_init(norm_full + s, 1);
             stage_n_all[s] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -366,15 +392,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t aph = 0;
-            for (int it = 0;; ++it) {
-                const int slot = it & 1;
-                const uint32_t ph = (it >> 1) & 1;
-                int64_t u = atomicAdd(p.sched, 1);
-                mbar_wait_sleep(unit_empty + slot, ph ^ 1);
-                unit_id[slot] = u < p.n_units ? (int32_t)u : -1;
-                mbar_arrive(unit_full + slot);
-                if (u >= p.n_units) break;
-                const int64_t t = u % p.n_qtiles, b = u / p.n_qtiles;
+            int it = 0;
+            for (int64_t u = u_first; u < p.n_units; u += u_step, ++it) {
+                int64_t t, b;
+                unit_tb(p, u, t, b);
                 // resident query tile for this unit
                 const int bslot = it % bslots;
                 const uint32_t bph = (uint32_t)(it / bslots) & 1;
@@ -404,45 +425,56 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         // =============================== MMA issuer =====================
+        // The whole warp walks the pipeline (uniform control flow, no lanes
+        // parked at a warp barrier); lane 0 issues.  Descriptors are formed
+        // once: the start-address field is the low 14 bits (addr >> 4) and
+        // smem addresses stay below 256 KiB, so stepping a descriptor is a
+        // 64-bit add of (bytes >> 4).
         constexpr uint32_t idesc = make_idesc(N);
-        const uint32_t abias = smem_u32(sAbias);
+        const uint64_t adesc0 = make_desc<SW>(smem_u32(sA));
+        const uint64_t bdesc0 = make_desc<SW>(smem_u32(sB));
+        const uint64_t abias_desc = make_desc<32>(smem_u32(sAbias));
+        const uint64_t bbias_desc0 = make_desc<32>(smem_u32(sBbias));
+        const bool no_acc_wait = p.experiment == 5 || p.experiment == 7;
+        const bool no_bias = p.experiment == 4;
+        const bool no_mma = p.experiment == 6 || p.experiment == 7;
         int stage = 0;
         uint32_t aph = 0;
         int acc = 0;
         uint32_t accph = 0;
-        for (int it = 0;; ++it) {
+        int it = 0;
+        for (int64_t u = u_first; u < p.n_units; u += u_step, ++it) {
             const int slot = it & 1;
             const uint32_t ph = (it >> 1) & 1;
-            mbar_wait_spin(unit_full + slot, ph);
-            const int32_t u = unit_id[slot];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(unit_empty + slot);
-            if (u < 0) break;
-            const int64_t b = u / p.n_qtiles;
+            int64_t t, b;
+            unit_tb(p, u, t, b);
             const int64_t tile0 = b * p.tiles_per_unit;
-            const int64_t tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
+            const int ntl = (int)(min(p.n_tiles, tile0 + p.tiles_per_unit) - tile0);
             const int bslot = it % bslots;
             mbar_wait_spin(b_full + bslot, (uint32_t)(it / bslots) & 1);
             mbar_wait_spin(bias_full + slot, ph);
-            const uint32_t bbase = smem_u32(sB + (size_t)bslot * b_bytes);
-            const uint32_t bbias = smem_u32(sBbias + slot * N * kBiasK);
-            for (int64_t tile = tile0; tile < tile1; ++tile) {
-                mbar_wait_spin(acc_empty + acc, accph ^ 1);
+            const uint64_t bdesc = bdesc0 + (uint64_t)(((uint32_t)bslot * b_bytes) >> 4);
+            const uint64_t bbias_desc = bbias_desc0 + (uint64_t)((slot * N * kBiasK) >> 4);
+            for (int ti = 0; ti < ntl; ++ti) {
+                if (!no_acc_wait) mbar_wait_spin(acc_empty + acc, accph ^ 1);
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + (uint32_t)(acc * N);
                 for (int c = 0; c < p.kchunks; ++c) {
                     mbar_wait_spin(a_full + stage, aph);
                     tc_fence_after();
                     if (lane == 0) {
-                        const uint32_t abase = smem_u32(sA + (size_t)stage * a_stage_bytes);
-                        const uint32_t bchunk = bbase + (uint32_t)(c * N * SW);
+                        if (no_mma) {  // diagnostics: TMA + barrier protocol only
+                            mbar_arrive(a_empty + stage);
+                        } else {
+                            const uint64_t ad = adesc0 + (uint64_t)((stage * a_stage_bytes) >> 4);
+                            const uint64_t bd = bdesc + (uint64_t)((c * N * SW) >> 4);
 #pragma unroll
-                        for (int kk = 0; kk < SW / 32; ++kk) {
-                            tc_mma_i8(tmem_d, make_desc<SW>(abase + kk * 32),
-                                      make_desc<SW>(bchunk + kk * 32), idesc,
-                                      (c | kk) != 0 ? 1u : 0u);
+                            for (int kk = 0; kk < SW / 32; ++kk)
+                                tc_mma_i8(tmem_d, ad + (uint64_t)(2 * kk),
+                                          bd + (uint64_t)(2 * kk), idesc,
+                                          (c | kk) != 0 ? 1u : 0u);
+                            tc_commit(a_empty + stage);
                         }
-                        tc_commit(a_empty + stage);
                     }
                     __syncwarp();
                     if (++stage == p.stages) {
@@ -451,9 +483,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 if (lane == 0) {
-                    // + bias_q on every row: constant A (127) x per-query digits
-                    tc_mma_i8(tmem_d, make_desc<32>(abias), make_desc<32>(bbias), idesc, 1u);
-                    tc_commit(acc_full + acc);
+                    if (no_mma) {
+                        if (!no_acc_wait) mbar_arrive(acc_full + acc);
+                    } else {
+                        // + bias_q on every row: constant A (127) x per-query digits
+                        if (!no_bias) tc_mma_i8(tmem_d, abias_desc, bbias_desc, idesc, 1u);
+                        tc_commit(acc_full + acc);
+                    }
                 }
                 __syncwarp();
                 if (++acc == 2) {
@@ -462,8 +498,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             if (lane == 0) {
-                tc_commit(b_empty + bslot);
-                tc_commit(bias_empty + slot);
+                if (no_mma) {
+                    mbar_arrive(b_empty + bslot);
+                    mbar_arrive(bias_empty + slot);
+                } else {
+                    tc_commit(b_empty + bslot);
+                    tc_commit(bias_empty + slot);
+                }
             }
             __syncwarp();
         }
@@ -473,23 +514,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         // digit sum S_q = ceil(-B_q / 127) clamped to [kSMin, kSMax] (a bias
         // that would need more than kSMax flags its 32-column chunk), the
         // digits (S_q spread over 32 int8) into the bias B tile, and
-        // bias_q = 127 * S_q for the epilogue's exact re-test.
-        for (int it = 0;; ++it) {
+        // bias_q = 127 * S_q for the epilogue's exact re-test.  Runs up to
+        // two units ahead of the MMA.
+        constexpr int kQPL = N / 32;  // query columns per lane
+        const bool filtered = (a.mode == 0 || a.mode == 3);
+        int it = 0;
+        for (int64_t u = u_first; u < p.n_units; u += u_step, ++it) {
             const int slot = it & 1;
             const uint32_t ph = (it >> 1) & 1;
-            mbar_wait_sleep(unit_full + slot, ph);
-            const int32_t u = unit_id[slot];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(unit_empty + slot);
-            if (u < 0) break;
-            const int64_t t = u % p.n_qtiles, b = u / p.n_qtiles;
+            int64_t t, b;
+            unit_tb(p, u, t, b);
             const int64_t q0 = t * N;
             const int nqt = (int)min((int64_t)N, a.nq - q0);
-            mbar_wait_sleep(bias_empty + slot, ph ^ 1);
-            // norm range of the unit's rows (per-tile ranges, precomputed)
+            // all global reads of the unit issued together: thresholds of
+            // this lane's columns and the norm ranges of the unit's tiles
+            int32_t Tq[kQPL];
+#pragma unroll
+            for (int i = 0; i < kQPL; ++i) {
+                const int q = i * 32 + lane;
+                Tq[i] = (filtered && q < nqt) ? __ldg(a.thr + q0 + q) : 0;
+            }
             float nlo = INFINITY, nhi = -INFINITY;
             int32_t xlo = INT32_MAX;
-            const bool filtered = (a.mode == 0 || a.mode == 3);
             if (filtered && M != kIP) {
                 const int64_t gt0 = (a.r_lo >> 7) + b * p.tiles_per_unit;
                 const int64_t gt1 = (a.r_lo >> 7) + min(p.n_tiles, (b + 1) * p.tiles_per_unit);
@@ -508,21 +554,45 @@ __global__ void __launch_bounds__(kThreads, 1)
                     nhi = fmaxf(nhi, __shfl_xor_sync(0xffffffffu, nhi, o));
                 }
             }
+            mbar_wait_sleep(bias_empty + slot, ph ^ 1);
+            // the unit's row norms -> smem (bulk copy; the < 4 tail rows and
+            // unaligned arrays by plain loads)
+            const bool stage_norms = (M != kIP) && a.mode == 0;
+            if (stage_norms) {
+                const int32_t row0 = (int32_t)(a.r_lo + b * p.tiles_per_unit * kBlockM);
+                const int32_t nrows = (int32_t)min((int64_t)p.tiles_per_unit * kBlockM,
+                                                   a.r_hi - (int64_t)row0);
+                const int32_t *src = (M == kL2) ? a.db_sqnorm + row0
+                                                : reinterpret_cast<const int32_t *>(a.db_norm) + row0;
+                int32_t *dst = norm_all + slot * kUnitRowsMax;
+                const int32_t nbulk = p.norm_bulk ? (nrows & ~3) : 0;
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(norm_full + slot, (uint32_t)nbulk * 4u);
+                    if (nbulk > 0)
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+                            " [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+                            "l"(src), "r"(nbulk * 4), "r"(smem_u32(norm_full + slot))
+                            : "memory");
+                }
+                for (int32_t i = nbulk + lane; i < nrows; i += 32) dst[i] = __ldg(src + i);
+            }
             int32_t *bias_out = bias_s + slot * N;
             int32_t *thr_out = thr_all + slot * N;
             int32_t *digits_out = reinterpret_cast<int32_t *>(sBbias + slot * N * kBiasK);
-            for (int i = 0; i < N / 32; ++i) {
+#pragma unroll
+            for (int i = 0; i < kQPL; ++i) {
                 const int q = i * 32 + lane;
                 int S = kSMin;  // padded columns: most negative bias
                 bool exc = false;
                 // thresholds for the exact test; padded columns never pass
                 thr_out[q] = (filtered && q < nqt)
-                                 ? __ldg(a.thr + q0 + q)
+                                 ? Tq[i]
                                  : ((M == kIP) ? INT32_MAX : (M == kL2 ? INT32_MIN : 0x7fc00000));
                 if (!filtered) {
                     S = 0;  // dense / diagnostic passes: plain dots
                 } else if (q < nqt) {
-                    const int32_t T = __ldg(a.thr + q0 + q);
+                    const int32_t T = Tq[i];
                     long long B;  // necessary condition dot >= B
                     if constexpr (M == kIP) {
                         B = T;
@@ -563,6 +633,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const unsigned eb = __ballot_sync(0xffffffffu, exc);
                 if (lane == 0) exc_s[slot * (N / 32) + i] = eb != 0;
             }
+            if (stage_norms) mbar_wait_sleep(norm_full + slot, ph);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(bias_full + slot);
@@ -573,32 +644,40 @@ __global__ void __launch_bounds__(kThreads, 1)
         // already fill the other: one atomic per (query, unit) reserves space
         // in the query's global candidate list, then the staged survivors
         // are copied.  The epilogue never waits on global atomics.
-        for (int it = 0;; ++it) {
+        constexpr int kQPL = N / 32;
+        int it = 0;
+        for (int64_t u = u_first; u < p.n_units; u += u_step, ++it) {
             const int slot = it & 1;
             const uint32_t ph = (it >> 1) & 1;
-            mbar_wait_sleep(unit_full + slot, ph);
-            const int32_t u = unit_id[slot];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(unit_empty + slot);
-            if (u < 0) break;
-            const int64_t q0 = (u % p.n_qtiles) * N;
+            int64_t t, b;
+            unit_tb(p, u, t, b);
+            const int64_t q0 = t * N;
+            const int32_t unit_row0 = (int32_t)(a.r_lo + b * p.tiles_per_unit * kBlockM);
             mbar_wait_sleep(stage_full + slot, ph);
-            if (a.mode == 0) {
+            if (a.mode == 0 && stage_n_all[slot] > 0) {
                 int32_t *qc = qcnt_all + slot * N;
-                const Staged *sb = stage_all + slot * kStageCap;
-                const int ns = min(stage_n_all[slot], kStageCap);
-                for (int q = lane; q < N; q += 32) {
-                    const int c = qc[q];
-                    if (c > 0) {
-                        qbase[q] = atomicAdd(a.ccount + q0 + q, c);
-                        qc[q] = 0;
-                    }
+                const Staged *sb = stage_all + slot * stage_cap;
+                const int ns = min(stage_n_all[slot], stage_cap);
+                // reservations for all of this lane's queries in flight at once
+                int32_t cnt[kQPL], got[kQPL];
+#pragma unroll
+                for (int i = 0; i < kQPL; ++i) cnt[i] = qc[i * 32 + lane];
+#pragma unroll
+                for (int i = 0; i < kQPL; ++i)
+                    got[i] = cnt[i] > 0 ? atomicAdd(a.ccount + q0 + i * 32 + lane, cnt[i]) : 0;
+#pragma unroll
+                for (int i = 0; i < kQPL; ++i) {
+                    qbase[i * 32 + lane] = got[i];
+                    qc[i * 32 + lane] = 0;
                 }
                 __syncwarp();
                 for (int e = lane; e < ns; e += 32) {
                     const Staged s = sb[e];
-                    const int32_t dst = qbase[s.qloc] + s.sq;
-                    if (dst < a.cap) a.cand[(q0 + s.qloc) * a.cap + dst] = Cand{s.row, s.dot};
+                    const int qloc = (int)(s.key & 0xffu);
+                    const int32_t dst = qbase[qloc] + (int32_t)((s.key >> 8) & 0xfffu);
+                    if (dst < a.cap)
+                        a.cand[(q0 + qloc) * a.cap + dst] =
+                            Cand{unit_row0 + (int32_t)(s.key >> 20), s.dot};
                 }
                 __syncwarp();
                 if (lane == 0) stage_n_all[slot] = 0;
@@ -613,17 +692,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ew = warp - kEpiWarp0;           // 0..15
         const int quarter = warp & 3;
         const int col0 = (ew >> 2) * kCB;          // first column of this warp
+        const bool acc_sync = p.experiment != 5 && p.experiment != 7;
+        constexpr bool lean = kFilter;
+        const uint32_t tm_warp = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)col0;
         int acc = 0;
         uint32_t accph = 0;
-        for (int it = 0;; ++it) {
+        int it = 0;
+        for (int64_t u = u_first; u < p.n_units; u += u_step, ++it) {
             const int slot = it & 1;
             const uint32_t ph = (it >> 1) & 1;
-            mbar_wait(unit_full + slot, ph);
-            const int32_t u = unit_id[slot];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(unit_empty + slot);
-            if (u < 0) break;
-            const int64_t t = u % p.n_qtiles, b = u / p.n_qtiles;
+            int64_t t, b;
+            unit_tb(p, u, t, b);
             const int64_t q0 = t * N;
             const int nqt = (int)min((int64_t)N, a.nq - q0);
             // this unit's bias, thresholds and exception flags; a free
@@ -632,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(stage_free + slot, ph ^ 1);
             int32_t *stage_n = stage_n_all + slot;
             int32_t *qcnt = qcnt_all + slot * N;
-            Staged *stage_buf = stage_all + slot * kStageCap;
+            Staged *stage_buf = stage_all + slot * stage_cap;
             const int64_t tile0 = b * p.tiles_per_unit;
             const int64_t tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
             const uint32_t thr_addr = smem_u32(thr_all + slot * N);
@@ -643,48 +722,33 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int ci = 0; ci < kCB / kC; ++ci)
                 if (exc_s[slot * (N / 32) + (col0 + ci * kC) / 32]) excm |= 1u << ci;
             const int32_t r_hi = (int32_t)a.r_hi;
-            int32_t wrow0 = (int32_t)(a.r_lo + tile0 * kBlockM) + quarter * 32;
+            const int32_t unit_row0 = (int32_t)(a.r_lo + tile0 * kBlockM);
+            const int32_t *unit_norm = norm_all + slot * kUnitRowsMax;
+            int32_t wrow0 = unit_row0 + quarter * 32;
             const int ntl = (int)(tile1 - tile0);
-            // the row's norm for the exact test, prefetched one tile ahead
-            int32_t nx_norm = 0;
-            if (a.mode == 0 && M != kIP && ntl > 0 && wrow0 + lane < r_hi)
-                nx_norm = (M == kL2) ? __ldg(a.db_sqnorm + wrow0 + lane)
-                                     : __float_as_int(__ldg(a.db_norm + wrow0 + lane));
-            for (int ti = 0; ti < ntl; ++ti, wrow0 += kBlockM) {
-                const int32_t row = wrow0 + lane;
-                const bool valid = row < r_hi;
-                const int32_t row_norm = nx_norm;
-                if (a.mode == 0 && M != kIP && ti + 1 < ntl && row + kBlockM < r_hi)
-                    nx_norm = (M == kL2) ? __ldg(a.db_sqnorm + row + kBlockM)
-                                         : __float_as_int(__ldg(a.db_norm + row + kBlockM));
-                mbar_wait(acc_full + acc, accph);
-                tc_fence_after();
-                const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) +
-                                       (uint32_t)(acc * N) + (uint32_t)col0;
-                if (a.mode == 1 || a.mode == 2 || p.experiment != 0) {
-#pragma unroll 1
-                    for (int ci = 0; ci < nch; ++ci) {
-                        int32_t cur[kC];
-                        if (p.experiment == 2) continue;  // no TMEM read at all
-                        tmem_ld_cols<kC>(tbase + (uint32_t)(ci * kC), cur);
-                        tmem_wait();
-                        if (p.experiment == 1) {          // TMEM read only
-                            if (cur[0] == 0x12345678 && cur[31 % kC] == 0x7654321) *stage_n = 0;
-                            continue;
-                        }
-                        // dense / diagnostic passes (bias 0): every dot out
-                        if (!valid) continue;
+            if constexpr (lean) {
+                // ---- filter pass, the hot loop ----
+                // Fast path per tile: TMEM -> registers, one sign bit per
+                // 8-column group (AND-reduction), and the accumulator is
+                // released right away when no lane of the warp has a group
+                // with a non-negative biased value.  Otherwise the hit
+                // groups are re-read from TMEM (8 columns at a time, warp-
+                // uniform loop), given the exact test, and staged; the
+                // accumulator is released after that.
+                uint32_t excg = 0;           // groups of exceptional chunks
+                for (int ci = 0; ci < kCB / kC; ++ci)
+                    if ((excm >> ci) & 1u) excg |= ((1u << (kC / 8)) - 1u) << (ci * (kC / 8));
+                int32_t row = wrow0 + lane;
+                for (int ti = 0; ti < ntl; ++ti, row += kBlockM) {
+                    mbar_wait(acc_full + acc, accph);
+                    tc_fence_after();
+                    const uint32_t ta = tm_warp + (uint32_t)(acc * N);
+                    int32_t v[kCB / kC][kC];
 #pragma unroll
-                        for (int j = 0; j < kC; ++j) {
-                            const int c = col0 + ci * kC + j;
-                            if (c >= nqt) continue;
-                            const int64_t q = q0 + c;
-                            if (a.mode == 1)
-                                a.cand[q * a.cap + (row - (int32_t)a.r_lo)] = Cand{row, cur[j]};
-                            else
-                                a.dots_out[q * a.ld_dots + row] = cur[j];
-                        }
-                    }
+                    for (int ci = 0; ci < kCB / kC; ++ci)
+                        tmem_ld_cols<kC>(ta + (uint32_t)(ci * kC), v[ci]);
+                    tmem_wait();
+                    // the tile is in registers: hand the accumulator back now
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(acc_empty + acc);
@@ -692,95 +756,160 @@ __global__ void __launch_bounds__(kThreads, 1)
                         acc = 0;
                         accph ^= 1;
                     }
-                    continue;
-                }
-                // The whole tile slice of this warp goes to registers first and
-                // the accumulator is released at once: the MMA can refill it
-                // while this warp filters (survivor bursts in one warp then no
-                // longer hold back the tensor core).
-                int32_t vals[kCB / kC][kC];
+                    uint32_t hit = 0;
 #pragma unroll
-                for (int ci = 0; ci < kCB / kC; ++ci)
-                    tmem_ld_cols<kC>(tbase + (uint32_t)(ci * kC), vals[ci]);
-                tmem_wait();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(acc_empty + acc);
-                if (++acc == 2) {
-                    acc = 0;
-                    accph ^= 1;
-                }
+                    for (int ci = 0; ci < kCB / kC; ++ci)
 #pragma unroll
-                for (int ci = 0; ci < kCB / kC; ++ci) {
-                    if (ci >= nch) break;
-                    const int32_t(&cur)[kC] = vals[ci];
-                    if (a.mode == 3) {
-                        // masked dense (survivor-dense early rounds): every
-                        // element gets its slot; rows failing the bound are
-                        // marked row = -1 (no atomics at all)
+                        for (int h = 0; h < kC / 8; ++h) {
+                            const int32_t *c8 = v[ci] + 8 * h;
+                            const int32_t g8 = (c8[0] & c8[1] & c8[2]) & (c8[3] & c8[4] & c8[5]) &
+                                               (c8[6] & c8[7]);
+                            hit |= ((uint32_t)~g8 >> 31) << (ci * (kC / 8) + h);
+                        }
+                    hit = row < r_hi ? (hit | excg) : 0u;
+                    if (!hit) continue;
+                    // slow path (lanes with a candidate group only): exact
+                    // test of every non-negative column of a hit group
+                    const int rowrel = row - unit_row0;
+                    int32_t xx = 0;
+                    float inv_xn = 0.f;
+                    if constexpr (M != kIP) {
+                        const int32_t nb = unit_norm[rowrel];  // staged by the bias warp
+                        if constexpr (M == kL2) xx = nb;
+                        if constexpr (M == kAngular) inv_xn = __frcp_rn(__int_as_float(nb));
+                    }
+#pragma unroll
+                    for (int ci = 0; ci < kCB / kC; ++ci)
+#pragma unroll
+                        for (int h = 0; h < kC / 8; ++h) {
+                            const int g = ci * (kC / 8) + h;
+                            if (!((hit >> g) & 1u)) continue;
+                            const int32_t *c8 = v[ci] + 8 * h;
+                            uint32_t m8 = 0;
+                            if ((excg >> g) & 1u) {
+                                m8 = 0xffu;
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) m8 |= (uint32_t)(c8[j] >= 0) << j;
+                            }
+                            while (m8) {
+                                const int j = __ffs(m8) - 1;
+                                m8 &= m8 - 1;
+                                int32_t vj = c8[0];
+#pragma unroll
+                                for (int jj = 1; jj < 8; ++jj) vj = (j == jj) ? c8[jj] : vj;
+                                const int qloc = col0 + 8 * g + j;
+                                const int32_t dot = (int32_t)((uint32_t)vj -
+                                                              (uint32_t)lds32(bias_addr + 4u * (uint32_t)qloc));
+                                const int32_t T = lds32(thr_addr + 4u * (uint32_t)qloc);
+                                if (!passes<M>(dot, T, xx, inv_xn)) continue;
+                                const int e = atomicAdd(stage_n, 1);
+                                if (e < stage_cap) {
+                                    const int sq = atomicAdd(qcnt + qloc, 1);
+                                    stage_buf[e] = Staged{(uint32_t)qloc | ((uint32_t)sq << 8) |
+                                                              ((uint32_t)rowrel << 20),
+                                                          dot};
+                                } else {
+                                    // staging full: direct append (slow, rare)
+                                    const int32_t s = atomicAdd(a.ccount + q0 + qloc, 1);
+                                    if (s < a.cap) a.cand[(q0 + qloc) * a.cap + s] = Cand{row, dot};
+                                }
+                            }
+                        }
+                }
+            } else {
+            if (p.experiment == 0 && (a.mode == 1 || a.mode == 3)) {
+                // ---- dense (round 0) and masked-dense (early rounds) ----
+                // every element has its candidate slot; masked dense marks
+                // rows failing the bound row = -1 (no atomics at all)
+                for (int ti = 0; ti < ntl; ++ti, wrow0 += kBlockM) {
+                    const int32_t row = wrow0 + lane;
+                    mbar_wait(acc_full + acc, accph);
+                    tc_fence_after();
+                    const uint32_t ta = tm_warp + (uint32_t)(acc * N);
+                    int32_t v[kCB / kC][kC];
+#pragma unroll
+                    for (int ci = 0; ci < kCB / kC; ++ci)
+                        tmem_ld_cols<kC>(ta + (uint32_t)(ci * kC), v[ci]);
+                    tmem_wait();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(acc_empty + acc);
+                    if (++acc == 2) {
+                        acc = 0;
+                        accph ^= 1;
+                    }
+                    if (row >= r_hi) continue;
+                    Cand *dst = a.cand + q0 * a.cap + (row - (int32_t)a.r_lo);
+#pragma unroll
+                    for (int ci = 0; ci < kCB / kC; ++ci) {
+                        const bool exc = (excm >> ci) & 1u;
+#pragma unroll
+                        for (int j = 0; j < kC; ++j) {
+                            const int c = col0 + ci * kC + j;
+                            if (c >= nqt) break;
+                            Cand out;
+                            if (a.mode == 1) {
+                                out = Cand{row, v[ci][j]};
+                            } else {
+                                const int32_t dot = (int32_t)((uint32_t)v[ci][j] -
+                                                              (uint32_t)lds32(bias_addr + 4u * (uint32_t)c));
+                                out = (v[ci][j] >= 0 || exc) ? Cand{row, dot} : Cand{-1, 0};
+                            }
+                            dst[(int64_t)c * a.cap] = out;
+                        }
+                    }
+                }
+            } else {
+                // ---- diagnostics: the dot matrix / pipeline experiments ----
+                for (int ti = 0; ti < ntl; ++ti, wrow0 += kBlockM) {
+                    const int32_t row = wrow0 + lane;
+                    const bool valid = row < r_hi;
+                    if (acc_sync) mbar_wait(acc_full + acc, accph);
+                    tc_fence_after();
+                    const uint32_t tbase = tm_warp + (uint32_t)(acc * N);
+#pragma unroll 1
+                    for (int ci = 0; ci < nch; ++ci) {
+                        int32_t cur[kC];
+                        if (p.experiment >= 2) continue;  // no TMEM read at all
+                        tmem_ld_cols<kC>(tbase + (uint32_t)(ci * kC), cur);
+                        tmem_wait();
+                        if (p.experiment != 0) {          // TMEM read only
+                            if (cur[0] == 0x12345678 && cur[31 % kC] == 0x7654321) *stage_n = 0;
+                            continue;
+                        }
                         if (!valid) continue;
                         const bool exc = (excm >> ci) & 1u;
 #pragma unroll
                         for (int j = 0; j < kC; ++j) {
                             const int c = col0 + ci * kC + j;
                             if (c >= nqt) continue;
-                            const int32_t dot = (int32_t)((uint32_t)cur[j] -
-                                                          (uint32_t)lds32(bias_addr + 4u * (uint32_t)c));
-                            const bool keep = cur[j] >= 0 || exc;
-                            a.cand[(q0 + c) * a.cap + (row - (int32_t)a.r_lo)] =
-                                keep ? Cand{row, dot} : Cand{-1, 0};
-                        }
-                        continue;
-                    }
-                    // fast path: is any biased value >= 0 (bound possibly met)?
-                    // one AND per 8 columns, then the sign of their AND
-                    int32_t gand[kC / 8];
-#pragma unroll
-                    for (int h = 0; h < kC / 8; ++h) {
-                        const int32_t *c8 = cur + 8 * h;
-                        gand[h] = (c8[0] & c8[1] & c8[2]) & (c8[3] & c8[4] & c8[5]) & (c8[6] & c8[7]);
-                    }
-                    int32_t all = gand[0];
-#pragma unroll
-                    for (int h = 1; h < kC / 8; ++h) all &= gand[h];
-                    const bool exc = (excm >> ci) & 1u;
-                    if (!((all >= 0 || exc) && valid)) continue;
-                    // slow path (lanes with a candidate only), only for groups of
-                    // 8 columns with a non-negative value; a set bit's value is
-                    // picked with a select chain (no dynamic register
-                    // indexing); exact test on the dot.
-                    const int32_t xx = (M == kL2) ? row_norm : 0;
-                    const float inv_xn = (M == kAngular) ? __frcp_rn(__int_as_float(row_norm)) : 0.f;
-#pragma unroll
-                    for (int h = 0; h < kC / 8; ++h) {
-                        if (gand[h] < 0 && !exc) continue;
-                        const int32_t *c8 = cur + 8 * h;
-                        uint32_t m8 = exc ? 0xffu : 0u;
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) m8 |= (uint32_t)(c8[j] >= 0) << j;
-                        while (m8) {
-                            const int j = __ffs(m8) - 1;
-                            m8 &= m8 - 1;
-                            int32_t v = c8[0];
-#pragma unroll
-                            for (int jj = 1; jj < 8; ++jj) v = (j == jj) ? c8[jj] : v;
-                            const int qloc = col0 + ci * kC + 8 * h + j;
-                            const int32_t dot =
-                                (int32_t)((uint32_t)v - (uint32_t)lds32(bias_addr + 4u * (uint32_t)qloc));
-                            const int32_t T = lds32(thr_addr + 4u * (uint32_t)qloc);
-                            if (!passes<M>(dot, T, xx, inv_xn)) continue;
-                            const int e = atomicAdd(stage_n, 1);
-                            if (e < kStageCap) {
-                                const int sq = atomicAdd(qcnt + qloc, 1);
-                                stage_buf[e] = Staged{qloc, sq, row, dot};
+                            const int64_t q = q0 + c;
+                            if (a.mode == 1) {         // dense: every dot (bias 0)
+                                a.cand[q * a.cap + (row - (int32_t)a.r_lo)] = Cand{row, cur[j]};
+                            } else if (a.mode == 2) {  // diagnostics: the dot matrix
+                                a.dots_out[q * a.ld_dots + row] = cur[j];
                             } else {
-                                // staging full: direct append (slow, rare)
-                                const int32_t s = atomicAdd(a.ccount + q0 + qloc, 1);
-                                if (s < a.cap) a.cand[(q0 + qloc) * a.cap + s] = Cand{row, dot};
+                                // masked dense (survivor-dense early rounds):
+                                // every element has its slot; rows failing the
+                                // bound are marked row = -1 (no atomics)
+                                const int32_t dot = (int32_t)((uint32_t)cur[j] -
+                                                              (uint32_t)lds32(bias_addr + 4u * (uint32_t)c));
+                                const bool keep = cur[j] >= 0 || exc;
+                                a.cand[q * a.cap + (row - (int32_t)a.r_lo)] =
+                                    keep ? Cand{row, dot} : Cand{-1, 0};
                             }
                         }
                     }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0 && acc_sync) mbar_arrive(acc_empty + acc);
+                    if (++acc == 2) {
+                        acc = 0;
+                        accph ^= 1;
+                    }
                 }
+            }
             }
             // this warp is done with the unit's bias / thresholds and staging
             __syncwarp();
@@ -832,8 +961,25 @@ bool make_map(CUtensorMap *m, const int8_t *ptr, int64_t rows, int64_t cols, int
     return r == CUDA_SUCCESS;
 }
 
+// Diagnostics knobs, read once from the environment; production runs use
+// the defaults (QA_B200_EXPERIMENT=0: the real kernel).
+struct Knobs {
+    int experiment, stage_cap, max_stages, b_slots;
+};
+const Knobs &knobs() {
+    static const Knobs k = [] {
+        auto env_int = [](const char *name, int dflt) {
+            const char *v = getenv(name);
+            return (v && *v) ? atoi(v) : dflt;
+        };
+        return Knobs{env_int("QA_B200_EXPERIMENT", 0), env_int("QA_B200_STAGECAP", kStageCapDefault),
+                     env_int("QA_B200_MAXSTAGES", 12), env_int("QA_B200_BSLOTS", 2)};
+    }();
+    return k;
+}
+
 template <int SW, int N, int M>
-cudaError_t launch_t(const FilterArgs &a, int *sched, cudaStream_t st) {
+cudaError_t launch_t(const FilterArgs &a, cudaStream_t st) {
     CUtensorMap tm_db, tm_q;
     if (!make_map(&tm_db, a.db, a.r_hi, a.kdim, a.ldd, kBlockM, SW)) return cudaErrorNotSupported;
     if (!make_map(&tm_q, a.q, a.nq, a.kdim, a.ldq, N, SW)) return cudaErrorNotSupported;
@@ -844,76 +990,77 @@ cudaError_t launch_t(const FilterArgs &a, int *sched, cudaStream_t st) {
     p.kchunks = (int)(a.kdim / SW);
     const int sms = num_sms();
     // tiles per unit: a power of two <= 32, so units stay inside one
-    // 32-tile norm-sorted block of an index laid out by qa_order_rows_by_norm
+    // 32-tile norm-sorted block of an index laid out by qa_order_rows_by_norm;
+    // at least ~4 units per CTA so the static assignment stays balanced
     int64_t want = (p.n_tiles * p.n_qtiles) / ((int64_t)sms * 4);
     int64_t tpu = 1;
     while (tpu * 2 <= want && tpu < 32) tpu *= 2;
     p.tiles_per_unit = tpu;
     p.n_units = ((p.n_tiles + tpu - 1) / tpu) * p.n_qtiles;
-    p.sched = sched;
+    const Knobs &kn = knobs();
+    p.experiment = kn.experiment;
+    p.stage_cap = kn.stage_cap;
     {
-        static int exp_mode = -1;
-        if (exp_mode < 0) {
-            const char *v = getenv("QA_B200_EXPERIMENT");
-            exp_mode = v ? atoi(v) : 0;
-        }
-        p.experiment = exp_mode;
+        const void *nrm = (M == kL2) ? (const void *)a.db_sqnorm : (const void *)a.db_norm;
+        p.norm_bulk = ((uintptr_t)nrm % 16) == 0;
     }
-    p.b_slots =(2 * (size_t)N * a.kdim <= 65536) ? 2 : 1;
+    p.b_slots = (2 * (size_t)N * a.kdim <= 65536) ? 2 : 1;
+    if (kn.b_slots == 1) p.b_slots = 1;
     const size_t fixed = 1024 /*align slack*/ + (size_t)p.b_slots * N * a.kdim +
                          kBlockM * kBiasK + 2 * (size_t)N * kBiasK +
-                         2 * kStageCap * sizeof(Staged) +
+                         2 * (size_t)p.stage_cap * sizeof(Staged) +
+                         (M == kIP ? 0 : 2 * (size_t)kUnitRowsMax * sizeof(int32_t)) +
                          (7 * N + 2 * (N / 32)) * sizeof(int32_t) + 256;
     const size_t budget = 227 * 1024;
     const size_t stage_bytes = (size_t)kBlockM * SW;
     // each stage also costs two 8-byte mbarriers
     if (fixed + 2 * (stage_bytes + 16) > budget) return cudaErrorNotSupported;
     int stages = (int)((budget - fixed) / (stage_bytes + 16));
-    if (stages > 8) stages = 8;
+    if (stages > kn.max_stages) stages = kn.max_stages;
     p.stages = stages;
     const size_t smem = fixed + (size_t)stages * (stage_bytes + 16);
-    cudaError_t e = cudaFuncSetAttribute(filter_tc_kernel<SW, N, M>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(sched, 0, sizeof(int), st);
+    auto kern = (a.mode == 0 && p.experiment == 0) ? filter_tc_kernel<SW, N, M, true>
+                                                   : filter_tc_kernel<SW, N, M, false>;
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int64_t grid = p.n_units < sms ? p.n_units : sms;
-    filter_tc_kernel<SW, N, M><<<(unsigned)grid, kThreads, smem, st>>>(tm_db, tm_q, p);
+    kern<<<(unsigned)grid, kThreads, smem, st>>>(tm_db, tm_q, p);
     return cudaGetLastError();
 }
 
 template <int SW, int N>
-cudaError_t dispatch_metric(const FilterArgs &a, int *sched, cudaStream_t st) {
+cudaError_t dispatch_metric(const FilterArgs &a, cudaStream_t st) {
     switch (a.metric) {
-        case kIP: return launch_t<SW, N, kIP>(a, sched, st);
-        case kL2: return launch_t<SW, N, kL2>(a, sched, st);
-        default: return launch_t<SW, N, kAngular>(a, sched, st);
+        case kIP: return launch_t<SW, N, kIP>(a, st);
+        case kL2: return launch_t<SW, N, kL2>(a, st);
+        default: return launch_t<SW, N, kAngular>(a, st);
     }
 }
 
 template <int SW>
-cudaError_t dispatch_n(const FilterArgs &a, int *sched, cudaStream_t st) {
+cudaError_t dispatch_n(const FilterArgs &a, cudaStream_t st) {
     // Largest query tile whose B buffer fits 64 KiB, no larger than the query
     // chunk needs.
     int nmax = (int)(65536 / a.kdim);
-    if (a.nq > 128 && nmax >= 256) return dispatch_metric<SW, 256>(a, sched, st);
-    if (a.nq > 64 && nmax >= 128) return dispatch_metric<SW, 128>(a, sched, st);
-    if (nmax >= 64) return dispatch_metric<SW, 64>(a, sched, st);
+    if (a.nq > 128 && nmax >= 256) return dispatch_metric<SW, 256>(a, st);
+    if (a.nq > 64 && nmax >= 128) return dispatch_metric<SW, 128>(a, st);
+    if (nmax >= 64) return dispatch_metric<SW, 64>(a, st);
     return cudaErrorNotSupported;
 }
 
 }  // namespace
 
-cudaError_t launch_filter_tc(const FilterArgs &a, int *sched, cudaStream_t st) {
+cudaError_t launch_filter_tc(const FilterArgs &a, cudaStream_t st) {
     if (a.r_hi <= a.r_lo || a.nq == 0) return cudaSuccess;
     if (a.kdim % 32 != 0 || a.kdim > 1024) return cudaErrorNotSupported;
     if (a.ldd % 16 != 0 || a.ldq % 16 != 0) return cudaErrorNotSupported;
     if (a.r_hi > INT32_MAX) return cudaErrorNotSupported;
     // the biased accumulator must not wrap: |dot| + |bias| < 2^31
     if (a.kdim > 65536) return cudaErrorNotSupported;
-    if (a.kdim % 128 == 0) return dispatch_n<128>(a, sched, st);
-    if (a.kdim == 64) return dispatch_n<64>(a, sched, st);
-    if (a.kdim == 32) return dispatch_n<32>(a, sched, st);
+    if (a.kdim % 128 == 0) return dispatch_n<128>(a, st);
+    if (a.kdim == 64) return dispatch_n<64>(a, st);
+    if (a.kdim == 32) return dispatch_n<32>(a, st);
     return cudaErrorNotSupported;
 }
 

@@ -53,7 +53,7 @@ struct FilterArgs {
 
 // Tensor-core (tcgen05 kind::i8) filter pass.  Returns cudaErrorNotSupported
 // when the shape is outside what the kernel handles.
-cudaError_t launch_filter_tc(const FilterArgs &a, int *sched_counter, cudaStream_t st);
+cudaError_t launch_filter_tc(const FilterArgs &a, cudaStream_t st);
 // Plain CUDA-core (dp4a) filter pass, the bring-up path.
 cudaError_t launch_filter_simt(const FilterArgs &a, cudaStream_t st);
 
@@ -74,6 +74,7 @@ struct SelectArgs {
     int32_t *thr;        // out: next-round threshold
     int32_t *overflow;   // [nq] sticky per-query flag: candidate list overflowed
     int32_t *any_overflow;
+    unsigned long long *cand_count;  // statistics: valid candidates seen (may be NULL)
 };
 
 cudaError_t launch_select(const SelectArgs &a, cudaStream_t st);

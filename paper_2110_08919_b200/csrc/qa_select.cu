@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(kWarpsMax * 32) select_kernel(SelectArgs a, in
     int cur = a.state_cnt[q];
     for (int i = lane; i < cur; i += 32) T[i] = st[i];
     __syncwarp();
+    int nvalid = 0;
     for (int pos = 0; pos < m; pos += kChunk) {
         const int take = min(kChunk, m - pos);
         // score the chunk; drop entries that cannot beat the current k-th
@@ -159,14 +160,16 @@ __global__ void __launch_bounds__(kWarpsMax * 32) select_kernel(SelectArgs a, in
         for (int base = 0; base < take; base += 32) {
             const int i = base + lane;
             Entry e;
-            bool keep = false;
+            bool keep = false, valid = false;
             if (i < take) {
                 const Cand c = cd[pos + i];
                 if (c.row >= 0) {  // row -1: slot of a masked-dense pass, filtered out
+                    valid = true;
                     e = make_entry<M>(c, qq, qn, a.db_sqnorm, a.db_norm, a.row_ids);
                     keep = !full || entry_less(e, kth);
                 }
             }
+            nvalid += __popc(__ballot_sync(0xffffffffu, valid));
             const unsigned bal = __ballot_sync(0xffffffffu, keep);
             if (keep) S[ns + __popc(bal & ((1u << lane) - 1))] = e;
             ns += __popc(bal);
@@ -200,6 +203,7 @@ __global__ void __launch_bounds__(kWarpsMax * 32) select_kernel(SelectArgs a, in
     if (lane == 0) {
         a.state_cnt[q] = cur;
         if (cur == k) a.thr[q] = threshold_of<M>(T[k - 1], qq, qn);
+        if (a.cand_count) atomicAdd(a.cand_count, (unsigned long long)nvalid);
     }
 }
 
@@ -353,18 +357,21 @@ __global__ void __launch_bounds__(256) select_reg_kernel(SelectArgs a) {
     K *stage = stage_all[threadIdx.x >> 5];
     K kth = rget(t, k - 1);  // sentinel while fewer than k retained
     int fill = 0;
+    int nvalid = 0;
     for (int pos = 0; pos < m; pos += 32) {
         const int i = pos + lane;
-        bool keep = false;
+        bool keep = false, valid = false;
         K key;
         if (i < m) {
             const Cand c = cd[i];
             if (c.row >= 0) {  // row -1: slot of a masked-dense pass, filtered out
+                valid = true;
                 const Entry en = make_entry<M>(c, qq, qn, a.db_sqnorm, a.db_norm, a.row_ids);
                 to_key<M>(en, key);
                 keep = rlt(key, kth);
             }
         }
+        nvalid += __popc(__ballot_sync(0xffffffffu, valid));
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
         if (keep) stage[fill + __popc(bal & ((1u << lane) - 1))] = key;
         fill += __popc(bal);
@@ -411,7 +418,10 @@ __global__ void __launch_bounds__(256) select_reg_kernel(SelectArgs a) {
         const K v = rget(t, k - 1);
         if (lane == 0) a.thr[q] = threshold_of<M>(from_key(v), qq, qn);
     }
-    if (lane == 0) a.state_cnt[q] = cur;
+    if (lane == 0) {
+        a.state_cnt[q] = cur;
+        if (a.cand_count) atomicAdd(a.cand_count, (unsigned long long)nvalid);
+    }
 }
 
 __global__ void reset_kernel(int32_t *p, int64_t n, int32_t v) {
