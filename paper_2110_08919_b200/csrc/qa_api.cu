@@ -16,6 +16,7 @@
 // lists are bounded (cap per query); a query that overflows its list in any
 // round is recomputed with a larger cap.
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -118,7 +119,7 @@ struct Buf {
 
 struct Workspace {
     std::mutex mu;
-    Buf state, state_cnt, thr, cand, ccount, ovf, flags, scratch, grp;
+    Buf state, state_cnt, thr, cand, ccount, ovf, flags, scratch, grp, est;
 };
 
 constexpr int kMaxDevices = 64;
@@ -152,9 +153,25 @@ int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
 struct ScanPlan {
     int64_t r0, ratio, cap, qchunk;
+    // threshold estimate: once the prefix reaches est_rows, the rest of the
+    // rows are scanned in ONE pass with the est_j-th best prefix score as the
+    // bound (0 = off)
+    int64_t est_rows, est_j;
 };
 
-ScanPlan plan_scan(int64_t n, int64_t nq, int64_t keff, int64_t cap_min) {
+// Smallest j with P(Poisson(lambda) >= j) <= tail.
+int64_t poisson_quantile(double lambda, double tail) {
+    double pmf = std::exp(-lambda), cdf = pmf;
+    int64_t j = 0;
+    while (1.0 - cdf > tail && j < 100000) {
+        ++j;
+        pmf *= lambda / (double)j;
+        cdf += pmf;
+    }
+    return j + 1;
+}
+
+ScanPlan plan_scan(int64_t n, int64_t nq, int64_t keff, int64_t cap_min, bool allow_estimate) {
     ScanPlan p;
     // a power of two >= 256: with ratio 2 every round boundary >= 4096 is a
     // multiple of the index's 4096-row norm blocks (qa_layout.cu)
@@ -167,6 +184,33 @@ ScanPlan plan_scan(int64_t n, int64_t nq, int64_t keff, int64_t cap_min) {
     p.ratio = nq >= 256 ? 2 : 16;
     if (const char *v = getenv("QA_B200_RATIO")) p.ratio = std::max(2, atoi(v));
     p.cap = std::max<int64_t>({2048, p.r0, 2 * keff * p.ratio, cap_min});
+    // Threshold estimate.  In a prefix of P rows (the index interleaves its
+    // norm blocks, so a prefix is a spread sample) about k*P/n rows beat the
+    // final k-th score; taking the j-th prefix score with j a high quantile
+    // of that count makes ">= k rows pass" near-certain, and the check after
+    // the pass proves it per query (the rare misses are recomputed without
+    // the estimate).  The final pass then admits ~j*n/P candidates per query
+    // instead of ~k per doubling round.
+    p.est_rows = 0;
+    p.est_j = 0;
+    if (allow_estimate && p.ratio == 2) {
+        int64_t P = 32768;
+        if (const char *v = getenv("QA_B200_EST_ROWS")) P = atoll(v);
+        while (P < 64 * keff) P *= 2;
+        if (P > 0 && 4 * P <= n) {
+            const double lambda = (double)keff * (double)P / (double)n;
+            double tail = 1e-4;
+            if (const char *v = getenv("QA_B200_EST_TAIL")) tail = atof(v);
+            int64_t j = std::max<int64_t>(8, poisson_quantile(lambda, tail));
+            // diagnostics/tests: force j (small j makes the estimate fail often)
+            if (const char *v = getenv("QA_B200_EST_J")) j = std::max<int64_t>(1, atoll(v));
+            if (j < keff) {
+                p.est_rows = P;
+                p.est_j = j;
+                p.cap = std::max<int64_t>(p.cap, 4 * j * (n / P));
+            }
+        }
+    }
     const int64_t per_q = p.cap * (int64_t)sizeof(Cand) + keff * (int64_t)sizeof(Entry) + 64;
     const int64_t budget = (int64_t)1 << 30;
     p.qchunk = std::max<int64_t>(1, std::min<int64_t>(nq, budget / per_q));
@@ -208,9 +252,9 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
               const float *db_norm, const int32_t *row_ids, const int8_t *q, int64_t nq,
               const int32_t *q_sqnorm,
               const float *q_norm, int64_t keff, int metric, int64_t id_offset,
-              double *out_scores, int32_t *out_ids, int64_t cap_min, cudaStream_t st,
-              std::vector<int32_t> *overflowed) {
-    ScanPlan pl = plan_scan(n, nq, keff, cap_min);
+              double *out_scores, int32_t *out_ids, int64_t cap_min, bool allow_estimate,
+              cudaStream_t st, std::vector<int32_t> *overflowed) {
+    ScanPlan pl = plan_scan(n, nq, keff, cap_min, allow_estimate);
     const int64_t qc = pl.qchunk;
     QA_TRY(ws.state.reserve((size_t)qc * keff * sizeof(Entry)), "workspace");
     QA_TRY(ws.state_cnt.reserve((size_t)qc * 4), "workspace");
@@ -219,6 +263,8 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
     QA_TRY(ws.ccount.reserve((size_t)qc * 4), "workspace");
     QA_TRY(ws.ovf.reserve((size_t)nq * 4), "workspace");
     QA_TRY(ws.flags.reserve(64), "workspace");
+    QA_TRY(ws.est.reserve((size_t)qc * 8), "workspace");
+    unsigned long long *est = (unsigned long long *)ws.est.ptr;
     Entry *state = (Entry *)ws.state.ptr;
     int32_t *state_cnt = (int32_t *)ws.state_cnt.ptr;
     int32_t *thr = (int32_t *)ws.thr.ptr;
@@ -242,7 +288,7 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
         QA_TRY(launch_init_state(state_cnt, thr, m, metric, st), "init");
         g_stats.launches += 1;
         int64_t r_lo = 0, r_hi = pl.r0;
-        bool first = true;
+        bool first = true, estimated = false;
         for (;;) {
             FilterArgs fa;
             fa.db = db;
@@ -270,6 +316,10 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             fa.mode = mode;
             fa.dots_out = nullptr;
             fa.ld_dots = 0;
+            // ~k new candidates per doubling of the rows seen; the estimated
+            // final pass admits ~est_j per prefix-sized slice
+            fa.exp_cands = estimated ? (double)pl.est_j * (double)(r_hi - r_lo) / (double)r_lo
+                                     : (double)keff * (double)(r_hi - r_lo) / (double)std::max<int64_t>(r_lo, 1);
             QA_TRY(launch_fill(ccount, m, mode != 0 ? (int32_t)(r_hi - r_lo) : 0, st), "fill");
             cudaError_t e = cudaErrorNotSupported;
             g_timer.begin(0, st);
@@ -314,7 +364,24 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             if (r_hi >= n) break;
             first = false;
             r_lo = r_hi;
-            r_hi = std::min(n, round_up(r_hi * pl.ratio, 128));
+            if (pl.est_rows > 0 && r_hi >= pl.est_rows) {
+                // one pass over the rest with the estimated bound
+                QA_TRY(launch_estimate(state, state_cnt, thr, est, m, keff, pl.est_j, metric,
+                                       q_sqnorm ? q_sqnorm + c0 : nullptr,
+                                       q_norm ? q_norm + c0 : nullptr, st),
+                       "estimate");
+                g_stats.launches += 1;
+                estimated = true;
+                r_hi = n;
+            } else {
+                r_hi = std::min(n, round_up(r_hi * pl.ratio, 128));
+            }
+        }
+        if (estimated) {
+            // queries whose k-th score fell short of the estimate are redone
+            QA_TRY(launch_check_estimate(state, state_cnt, est, m, keff, ovf + c0, flags, st),
+                   "estimate check");
+            g_stats.launches += 1;
         }
         QA_TRY(launch_finalize(state, m, keff, keff, metric, id_offset, out_scores + c0 * keff,
                                out_ids + c0 * keff, st),
@@ -372,9 +439,9 @@ int scan_entry(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_
     std::vector<int32_t> ovf;
     g_timer.reset();
     int rc = scan_impl(ws, db, n, d, ld, db_sqnorm, db_norm, row_ids, q, nq, q_sqnorm, q_norm, keff, metric,
-                       id_offset, out_scores, out_ids, 0, st, &ovf);
+                       id_offset, out_scores, out_ids, 0, true, st, &ovf);
     if (rc != QA_OK) return rc;
-    int64_t cap = plan_scan(n, nq, keff, 0).cap;
+    int64_t cap = plan_scan(n, nq, keff, 0, true).cap;
     while (!ovf.empty()) {
         // Recompute the overflowed queries with 4x the candidate capacity;
         // once cap >= n no list can overflow.
@@ -403,7 +470,8 @@ int scan_entry(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_
                                                                                  qn);
         std::vector<int32_t> ovf2;
         rc = scan_impl(ws, db, n, d, ld, db_sqnorm, db_norm, row_ids, qsub, m, q_sqnorm ? qsq : nullptr,
-                       q_norm ? qn : nullptr, keff, metric, id_offset, s, ids, cap, st, &ovf2);
+                       q_norm ? qn : nullptr, keff, metric, id_offset, s, ids, cap, false, st,
+                       &ovf2);
         if (rc == QA_OK) {
             scatter_results_kernel<<<(unsigned)((m * keff + 255) / 256), 256, 0, st>>>(
                 s, ids, idx, m, keff, out_scores, out_ids);

@@ -49,6 +49,9 @@ struct FilterArgs {
     int mode;
     int32_t *dots_out;
     int64_t ld_dots;
+    // expected candidates per query in this pass (mode 0; sizes the work
+    // units so their survivors fit the on-chip staging)
+    double exp_cands;
 };
 
 // Tensor-core (tcgen05 kind::i8) filter pass.  Returns cudaErrorNotSupported
@@ -81,6 +84,14 @@ cudaError_t launch_select(const SelectArgs &a, cudaStream_t st);
 cudaError_t launch_init_state(int32_t *state_cnt, int32_t *thr, int64_t nq, int metric,
                               cudaStream_t st);
 cudaError_t launch_fill(int32_t *p, int64_t n, int32_t v, cudaStream_t st);
+// thr[q] := threshold of the j-th kept entry (est[q] = its order key)
+cudaError_t launch_estimate(const Entry *state, const int32_t *state_cnt, int32_t *thr,
+                            unsigned long long *est, int64_t nq, int64_t k, int64_t j, int metric,
+                            const int32_t *q_sqnorm, const float *q_norm, cudaStream_t st);
+// redo[q] := 1 where the k-th kept entry is worse than est[q]
+cudaError_t launch_check_estimate(const Entry *state, const int32_t *state_cnt,
+                                  const unsigned long long *est, int64_t nq, int64_t k,
+                                  int32_t *redo, int32_t *any_redo, cudaStream_t st);
 cudaError_t launch_finalize(const Entry *state, int64_t nq, int64_t k, int64_t keff, int metric,
                             int64_t id_offset, double *out_scores, int32_t *out_ids,
                             cudaStream_t st);

@@ -559,6 +559,78 @@ cudaError_t launch_fill(int32_t *p, int64_t n, int32_t v, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// Threshold estimate for the final pass: the j-th best score of the prefix
+// scanned so far (j < k), a bound that about j * n / prefix rows of the whole
+// set reach.  est[q] keeps its order key for the check after the pass;
+// ~0 = no estimate (fewer than j entries: the k-th threshold stays).
+template <int M>
+__global__ void estimate_kernel(const Entry *__restrict__ state,
+                                const int32_t *__restrict__ state_cnt, int32_t *__restrict__ thr,
+                                unsigned long long *__restrict__ est, int64_t nq, int64_t k,
+                                int64_t j, const int32_t *__restrict__ q_sqnorm,
+                                const float *__restrict__ q_norm) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    if (state_cnt[q] < j) {
+        est[q] = ~0ull;
+        return;
+    }
+    const Entry e = state[q * k + j - 1];
+    const int32_t qq = (M == kL2) ? q_sqnorm[q] : 0;
+    const float qn = (M == kAngular) ? q_norm[q] : 1.0f;
+    thr[q] = threshold_of<M>(e, qq, qn);
+    est[q] = e.skey;
+}
+
+// After the final pass: the result is exact iff the k-th kept score is at
+// least the estimate's score (every row that failed the estimate's bound is
+// strictly worse).  Queries where it is not are flagged for recomputation.
+__global__ void check_estimate_kernel(const Entry *__restrict__ state,
+                                      const int32_t *__restrict__ state_cnt,
+                                      const unsigned long long *__restrict__ est, int64_t nq,
+                                      int64_t k, int32_t *__restrict__ redo,
+                                      int32_t *__restrict__ any_redo) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    const unsigned long long e = est[q];
+    if (e == ~0ull) return;
+    const bool ok = state_cnt[q] >= k && state[q * k + k - 1].skey <= e;
+    if (!ok) {
+        redo[q] = 1;
+        atomicExch(any_redo, 1);
+    }
+}
+
+cudaError_t launch_estimate(const Entry *state, const int32_t *state_cnt, int32_t *thr,
+                            unsigned long long *est, int64_t nq, int64_t k, int64_t j, int metric,
+                            const int32_t *q_sqnorm, const float *q_norm, cudaStream_t st) {
+    if (nq == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)((nq + 255) / 256);
+    switch (metric) {
+        case kIP:
+            estimate_kernel<kIP><<<grid, 256, 0, st>>>(state, state_cnt, thr, est, nq, k, j,
+                                                       q_sqnorm, q_norm);
+            break;
+        case kL2:
+            estimate_kernel<kL2><<<grid, 256, 0, st>>>(state, state_cnt, thr, est, nq, k, j,
+                                                       q_sqnorm, q_norm);
+            break;
+        default:
+            estimate_kernel<kAngular><<<grid, 256, 0, st>>>(state, state_cnt, thr, est, nq, k, j,
+                                                            q_sqnorm, q_norm);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_estimate(const Entry *state, const int32_t *state_cnt,
+                                  const unsigned long long *est, int64_t nq, int64_t k,
+                                  int32_t *redo, int32_t *any_redo, cudaStream_t st) {
+    if (nq == 0) return cudaSuccess;
+    check_estimate_kernel<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(state, state_cnt, est, nq,
+                                                                       k, redo, any_redo);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_init_state(int32_t *state_cnt, int32_t *thr, int64_t nq, int metric,
                               cudaStream_t st) {
     if (nq == 0) return cudaSuccess;

@@ -314,3 +314,29 @@ def test_norm_sorted_index_equals_unsorted(oracle, metric):
     osc, oids = _scan_oracle(oracle, X, Q, 100, metric)
     np.testing.assert_array_equal(a[1].cpu().numpy(), oids)
     np.testing.assert_array_equal(a[0].cpu().numpy(), osc)
+
+
+@pytest.mark.parametrize("metric", [0, 1, 2])
+@pytest.mark.parametrize("force_j", [None, "1"])
+def test_threshold_estimate_path_exact(oracle, monkeypatch, metric, force_j):
+    # The estimated-bound final pass (qa_api.cu plan_scan): a small prefix
+    # triggers it at this size; j=1 (the best prefix score as the bound)
+    # makes the estimate fail for many queries, which must then be
+    # recomputed without it -- results exact either way.
+    from paper_2110_08919_b200 import _lib
+
+    monkeypatch.setenv("QA_B200_EST_ROWS", "2048")
+    if force_j:
+        monkeypatch.setenv("QA_B200_EST_J", force_j)
+    rng = np.random.default_rng(400 + metric)
+    X = _rand_codes(rng, 40_000, 64, -30, 31, nonzero=True)
+    Q = _rand_codes(rng, 300, 64, -30, 31, nonzero=True)
+    db = dev.DeviceCodes.from_host(X).sorted_by_norm()
+    qs = dev.DeviceCodes.from_host(Q)
+    sc, ids = dev.scan_topk(db, qs, 20, metric)
+    st = _lib.last_scan_stats()
+    osc, oids = _scan_oracle(oracle, X, Q, 20, metric)
+    np.testing.assert_array_equal(ids.cpu().numpy(), oids)
+    np.testing.assert_array_equal(sc.cpu().numpy(), osc)
+    if force_j:
+        assert st["retries"] >= 1  # the recompute path ran

@@ -39,7 +39,11 @@ def short(name):
 
 def main():
     ks = load(sys.argv[1])
-    last = max(i for i, (n, _) in enumerate(ks) if "init_state" in n)
+    back = int(sys.argv[2]) if len(sys.argv) > 2 else 1  # n-th last search call
+    inits = [i for i, (n, _) in enumerate(ks) if "init_state" in n]
+    last = inits[-back]
+    if back > 1:
+        ks = ks[:inits[-back + 1]]
     # include the group-range / encode launches just before init_state
     seq = ks[last:]
     fil = [round(v, 1) for n, v in seq if "filter" in n]

@@ -13,22 +13,36 @@
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
+__device__ __forceinline__ uint64_t make_desc32(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3fff) | ((uint64_t)1 << 16) | ((uint64_t)16 << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)6 << 61);
+}
 __device__ __forceinline__ uint64_t make_desc128(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3fff) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) |
            ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
-template <int KIND, int N>  // KIND 0 = i8, 1 = f16(bf16)
-__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int reps, long long *cycles) {
+template <int KIND, int N, int VAR = 0>  // KIND 0 = i8, 1 = f16(bf16)
+__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int reps, long long *cycles,
+                                                          const int8_t *stream_src, int stream_tiles) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     uintptr_t base = ((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023;
     unsigned char *sA = (unsigned char *)base;        // 128 x 128 B
     unsigned char *sB = sA + 128 * 128;               // N x 128 B
+    unsigned char *sS = sB + N * 128;                 // 4 x 16 KiB streaming ring
     __shared__ uint64_t bar;
+    __shared__ uint64_t cbar[2];
+    __shared__ uint64_t sfull[4];
+    __shared__ volatile int stop;
     __shared__ uint32_t tmem_base_s;
     for (int i = threadIdx.x; i < (128 + N) * 128 / 4; i += blockDim.x)
         reinterpret_cast<int32_t *>(sA)[i] = 0x01010101;
     if (threadIdx.x == 0) {
+        stop = 0;
+        for (int i = 0; i < 4; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sfull[i])));
+        for (int i = 0; i < 2; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&cbar[i])));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -69,6 +83,24 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int reps, long long *c
                         "l"(ad), "l"(bd), "r"(idesc), "r"(kk)
                         : "memory");
             }
+            if (VAR >= 1)
+                asm volatile(
+                    "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                        smem_u32(&cbar[0]))
+                    : "memory");
+            if (VAR >= 2) {
+                const uint64_t ad = (VAR == 2) ? make_desc32(a0) : make_desc128(a0);
+                const uint64_t bd = (VAR == 2) ? make_desc32(b0) : make_desc128(b0);
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                    "l"(ad), "l"(bd), "r"(idesc), "r"(1)
+                    : "memory");
+                asm volatile(
+                    "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                        smem_u32(&cbar[1]))
+                    : "memory");
+            }
         }
         asm volatile(
             "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -81,6 +113,28 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int reps, long long *c
             : "memory");
         t1 = clock64();
         cycles[blockIdx.x] = t1 - t0;
+        stop = 1;
+    } else if (threadIdx.x == 64 && stream_tiles > 0) {
+        // L2 -> smem stream of 16 KiB bulk copies, 4 in flight, concurrent
+        // with the MMAs (the filter kernel's database-tile traffic)
+        uint32_t ph[4] = {0, 0, 0, 0};
+        long long i = 0;
+        for (int s = 0; s < 4; ++s, ++i) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 16384;" ::"r"(smem_u32(&sfull[s])) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16384, [%2];"
+                         ::"r"(smem_u32(sS + s * 16384)), "l"(stream_src + ((blockIdx.x * 131 + i) % stream_tiles) * 16384), "r"(smem_u32(&sfull[s])) : "memory");
+        }
+        while (!stop) {
+            for (int s = 0; s < 4 && !stop; ++s, ++i) {
+                asm volatile("{\n\t.reg .pred p;\n\tW2_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W2_%=;\n\t}" ::"r"(smem_u32(&sfull[s])), "r"(ph[s]) : "memory");
+                ph[s] ^= 1;
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 16384;" ::"r"(smem_u32(&sfull[s])) : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16384, [%2];"
+                             ::"r"(smem_u32(sS + s * 16384)), "l"(stream_src + ((blockIdx.x * 131 + i) % stream_tiles) * 16384), "r"(smem_u32(&sfull[s])) : "memory");
+            }
+        }
+        for (int s = 0; s < 4; ++s)
+            asm volatile("{\n\t.reg .pred p;\n\tW3_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W3_%=;\n\t}" ::"r"(smem_u32(&sfull[s])), "r"(ph[s]) : "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -90,20 +144,20 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int reps, long long *c
     }
 }
 
-template <int KIND, int N>
-void run(const char *name, int sms) {
+template <int KIND, int N, int VAR = 0>
+void run(const char *name, int sms, const int8_t *src = nullptr, int tiles = 0) {
     const int reps = 4096;
     long long *d;
     cudaMalloc(&d, sms * sizeof(long long));
-    size_t smem = 1024 + (128 + N) * 128;
-    cudaFuncSetAttribute(mma_rate_kernel<KIND, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    size_t smem = 1024 + (128 + N) * 128 + 4 * 16384;
+    cudaFuncSetAttribute(mma_rate_kernel<KIND, N, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    mma_rate_kernel<KIND, N><<<sms, 128, smem>>>(16, d);  // warm
+    mma_rate_kernel<KIND, N, VAR><<<sms, 128, smem>>>(16, d, src, tiles);  // warm
     cudaEventRecord(e0);
-    mma_rate_kernel<KIND, N><<<sms, 128, smem>>>(reps, d);
+    mma_rate_kernel<KIND, N, VAR><<<sms, 128, smem>>>(reps, d, src, tiles);
     cudaEventRecord(e1);
     cudaError_t err = cudaDeviceSynchronize();
     float ms = 0;
@@ -113,18 +167,29 @@ void run(const char *name, int sms) {
     double avg = 0;
     for (int i = 0; i < sms; ++i) avg += (double)h[i];
     avg /= sms;
-    const double mmas = 4.0 * reps;
+    const double mmas = (VAR >= 2 ? 5.0 : 4.0) * reps;
     const double kmul = KIND == 0 ? 32 : 16;
     const double ops = 2.0 * 128 * N * kmul * mmas * sms;
-    printf("%-10s N=%3d  %7.1f cycles/MMA  %8.1f T(FL)OP/s over %.3f ms  (%s)\n", name, N,
+    printf("%-6s%s N=%3d  %7.1f cycles/MMA  %8.1f T(FL)OP/s over %.3f ms  (%s)\n", name,
+           tiles ? "+stream" : (VAR == 1 ? "+commit" : (VAR == 2 ? "+bias32" : (VAR == 3 ? "+bias128" : "       "))), N,
            avg / mmas, ops / (ms * 1e-3) / 1e12, ms, cudaGetErrorString(err));
+    (void)0;
     cudaFree(d);
 }
 
 int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int8_t *src;
+    const int tiles = 4096;  // 64 MiB, L2 resident
+    cudaMalloc(&src, (size_t)tiles * 16384);
+    cudaMemset(src, 1, (size_t)tiles * 16384);
     run<0, 256>("i8", sms);
+    run<0, 256, 1>("i8", sms);
+    run<0, 256, 2>("i8", sms);
+    run<0, 256, 3>("i8", sms);
+    run<0, 256>("i8", sms, src, tiles);
+    run<0, 128>("i8", sms, src, tiles);
     run<0, 128>("i8", sms);
     run<0, 64>("i8", sms);
     run<1, 256>("bf16", sms);
