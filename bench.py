@@ -315,6 +315,16 @@ def run_gpu(args):
     # algorithmic ops = 2 * nq * rows * d (unpadded d) per launch, divided by
     # the CUDA-event time of those launches on their stream.
     peak_tops = 2.0 * float(peaks["bf16_tflops"])
+    # DRAM traffic of the dominant launch (the final, estimated-bound pass)
+    # from the committed ncu --set full capture of this workload; compare to
+    # its algorithmic bytes (the database rows it scans, once)
+    traffic, traffic_note = None, "no committed ncu capture"
+    tfile = ROOT / "profiles" / "r01_filter_traffic.json"
+    if tfile.exists() and args.config == 1 and args.n is None and args.nq is None:
+        tj = json.loads(tfile.read_text())
+        traffic = tj["dram_bytes_read"] + tj["dram_bytes_write"]
+        traffic_note = (f"bytes per launch of the final filter pass ({tj['source']}); "
+                        f"algorithmic bytes {tj['algorithmic_db_bytes']}")
     achieved = (st["filter_ops"] / (st["filter_ms"] / 1e3) / 1e12) if st["filter_ms"] > 0 else None
     roofline = {
         "bound": "tensor", "kernel": "filter_tc_kernel (tcgen05 kind::i8 + fused threshold top-k epilogue)",
@@ -323,7 +333,8 @@ def run_gpu(args):
         "peak_source": f"2 x dense bf16 {peaks_src} (int8 dense = 2x bf16 on B200; "
                        f"spec 4500 TOP/s)",
         "frac_of_spec_4500": (achieved / 4500.0) if achieved else None,
-        "traffic": None,
+        "traffic": traffic,
+        "traffic_note": traffic_note,
         "filter_ms_per_step": st["filter_ms"], "select_ms_per_step": st["select_ms"],
         "filter_launches_per_step": st["filter_launches"],
         "filter_share_of_step": st["filter_ms"] / ms if ms else None,
