@@ -174,8 +174,10 @@ int64_t poisson_quantile(double lambda, double tail) {
 ScanPlan plan_scan(int64_t n, int64_t nq, int64_t keff, int64_t cap_min, bool allow_estimate) {
     ScanPlan p;
     // a power of two >= 256: with ratio 2 every round boundary >= 4096 is a
-    // multiple of the index's 4096-row norm blocks (qa_layout.cu)
-    int64_t r0 = 256;
+    // multiple of the index's 4096-row norm blocks (qa_layout.cu).  1024
+    // measured best for cfg1 (a dense round is cheaper than two doubling
+    // rounds of a few hundred rows each).
+    int64_t r0 = 1024;
     if (const char *v = getenv("QA_B200_R0")) r0 = std::max<int64_t>(128, atoll(v));
     while (r0 < keff) r0 *= 2;
     p.r0 = std::min(n, r0);
@@ -311,7 +313,11 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             // round 0: dense (every row); survivor-dense early rounds whose
             // rows fit the candidate list: masked dense (no atomics); then the
             // filter with staged survivors
-            const bool masked = !first && (r_hi - r_lo) <= std::min<int64_t>(pl.cap, 2048);
+            static const int64_t masked_max = [] {
+                const char *v = getenv("QA_B200_MASKED_MAX");  // diagnostics knob
+                return v ? (int64_t)atoll(v) : (int64_t)1024;
+            }();
+            const bool masked = !first && (r_hi - r_lo) <= std::min<int64_t>(pl.cap, masked_max);
             const int mode = first ? 1 : (masked ? 3 : 0);
             fa.mode = mode;
             fa.dots_out = nullptr;
