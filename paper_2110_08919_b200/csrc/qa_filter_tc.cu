@@ -42,6 +42,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "qa_common.cuh"
@@ -124,11 +125,34 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) 
     }
 }
 
+template <uint32_t kMaxNs>
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t parity) {
+    uint32_t ns = 32;
+    while (!mbar_try(bar, parity)) {
+        __nanosleep(ns);
+        ns = ns < kMaxNs ? ns * 2 : kMaxNs;
+    }
+}
+
 // Pure polling wait for the latency-critical MMA issuer.
 __device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
     while (!mbar_try(bar, parity)) {
     }
 }
+
+// Wait accounting (diagnostics build, -DQA_WAIT_STATS): cycles each role
+// spends in each wait, summed per CTA and printed by CTAs 0..1.
+#ifdef QA_WAIT_STATS
+#define WSTAT(i, stmt)                      \
+    do {                                    \
+        const long long _t0 = clock64();    \
+        stmt;                               \
+        wst[i] += clock64() - _t0;          \
+    } while (0)
+#else
+#define WSTAT(i, stmt) stmt
+#endif
+constexpr int kWst = 16;
 
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar,
                                             int32_t c0, int32_t c1) {
@@ -171,6 +195,70 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint6
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
         "}" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// One K chunk of a tile, issued by one elected lane of a converged warp:
+// KSTEPS MMAs of K=32 bytes (descriptor start addresses step by 32 B = 2 in
+// the >>4 encoding), then a commit to `bar`.  Inline PTX with elect.sync
+// keeps the issue free of per-lane branching.
+template <int KSTEPS>
+__device__ __forceinline__ void mma_chunk_elect(uint32_t tmem_d, uint64_t ad, uint64_t bd,
+                                                uint32_t idesc, uint32_t first, uint32_t bar) {
+    static_assert(KSTEPS == 1 || KSTEPS == 2 || KSTEPS == 4, "1, 2 or 4 K steps");
+    if constexpr (KSTEPS == 4) {
+        asm volatile(
+            "{\n\t.reg .pred e, p;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.eq.u32 p, %4, 0;\n\t"
+            "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+            "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a1, b1, %3, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a2, b2, %3, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a3, b3, %3, 1;\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t"
+            "}" ::"r"(tmem_d),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(first), "r"(bar)
+            : "memory");
+    } else if constexpr (KSTEPS == 2) {
+        asm volatile(
+            "{\n\t.reg .pred e, p;\n\t.reg .b64 a1, b1;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.eq.u32 p, %4, 0;\n\t"
+            "add.s64 a1, %1, 2;\n\tadd.s64 b1, %2, 2;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a1, b1, %3, 1;\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t"
+            "}" ::"r"(tmem_d),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(first), "r"(bar)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred e, p;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.eq.u32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t"
+            "}" ::"r"(tmem_d),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(first), "r"(bar)
+            : "memory");
+    }
+}
+
+// The bias MMA of a tile (accumulate) and the commit that hands the tile to
+// the epilogue, by one elected lane of a converged warp.
+__device__ __forceinline__ void mma_bias_commit_elect(uint32_t tmem_d, uint64_t ad, uint64_t bd,
+                                                      uint32_t idesc, uint32_t do_mma,
+                                                      uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred e, m;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.and.u32 m, %4, 0, e;\n\t"
+        "@m tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 1;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t"
+        "}" ::"r"(tmem_d),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(do_mma), "r"(bar)
         : "memory");
 }
 
@@ -309,6 +397,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t u_first = blockIdx.x, u_step = gridDim.x;
+#ifdef QA_WAIT_STATS
+    long long wst[kWst] = {};
+    __shared__ unsigned long long wst_s[kWst];
+    if (threadIdx.x < kWst) wst_s[threadIdx.x] = 0;
+    const long long t_start = clock64();
+#endif
 
     // ---- shared memory carve-up (1024-aligned operand buffers) ----
     uintptr_t base = ((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023;
@@ -399,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // resident query tile for this unit
                 const int bslot = it % bslots;
                 const uint32_t bph = (uint32_t)(it / bslots) & 1;
-                mbar_wait_sleep(b_empty + bslot, bph ^ 1);
+                WSTAT(0, mbar_wait_sleep(b_empty + bslot, bph ^ 1));
                 mbar_arrive_expect_tx(b_full + bslot, b_bytes);
                 unsigned char *dstB = sB + (size_t)bslot * b_bytes;
                 for (int c = 0; c < p.kchunks; ++c)
@@ -409,9 +503,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int64_t tile0 = b * p.tiles_per_unit;
                 const int64_t tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
                 for (int64_t tile = tile0; tile < tile1; ++tile) {
-                    const int32_t row0 = (int32_t)(a.r_lo + tile * kBlockM);
+                    // (experiment 10: always the same, L2-hot tile)
+                    const int32_t row0 = (int32_t)(a.r_lo + (p.experiment == 10 ? 0 : tile) * kBlockM);
                     for (int c = 0; c < p.kchunks; ++c) {
-                        mbar_wait_sleep(a_empty + stage, aph ^ 1);
+                        WSTAT(1, mbar_wait_sleep(a_empty + stage, aph ^ 1));
                         mbar_arrive_expect_tx(a_full + stage, a_stage_bytes);
                         tma_load_2d(sA + (size_t)stage * a_stage_bytes, &tm_db, a_full + stage,
                                     c * SW, row0);
@@ -436,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t abias_desc = make_desc<32>(smem_u32(sAbias));
         const uint64_t bbias_desc0 = make_desc<32>(smem_u32(sBbias));
         const bool no_acc_wait = p.experiment == 5 || p.experiment == 7;
-        const bool no_bias = p.experiment == 4;
+        const bool no_bias = p.experiment == 4 || p.experiment == 9;
         const bool no_mma = p.experiment == 6 || p.experiment == 7;
         int stage = 0;
         uint32_t aph = 0;
@@ -451,47 +546,41 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t tile0 = b * p.tiles_per_unit;
             const int ntl = (int)(min(p.n_tiles, tile0 + p.tiles_per_unit) - tile0);
             const int bslot = it % bslots;
-            mbar_wait_spin(b_full + bslot, (uint32_t)(it / bslots) & 1);
-            mbar_wait_spin(bias_full + slot, ph);
+            WSTAT(2, mbar_wait_spin(b_full + bslot, (uint32_t)(it / bslots) & 1));
+            WSTAT(3, mbar_wait_spin(bias_full + slot, ph));
             const uint64_t bdesc = bdesc0 + (uint64_t)(((uint32_t)bslot * b_bytes) >> 4);
             const uint64_t bbias_desc = bbias_desc0 + (uint64_t)((slot * N * kBiasK) >> 4);
             for (int ti = 0; ti < ntl; ++ti) {
-                if (!no_acc_wait) mbar_wait_spin(acc_empty + acc, accph ^ 1);
+                if (!no_acc_wait) WSTAT(4, mbar_wait_spin(acc_empty + acc, accph ^ 1));
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + (uint32_t)(acc * N);
                 for (int c = 0; c < p.kchunks; ++c) {
-                    mbar_wait_spin(a_full + stage, aph);
+                    WSTAT(5, mbar_wait_spin(a_full + stage, aph));
                     tc_fence_after();
-                    if (lane == 0) {
-                        if (no_mma) {  // diagnostics: TMA + barrier protocol only
-                            mbar_arrive(a_empty + stage);
-                        } else {
-                            const uint64_t ad = adesc0 + (uint64_t)((stage * a_stage_bytes) >> 4);
-                            const uint64_t bd = bdesc + (uint64_t)((c * N * SW) >> 4);
-#pragma unroll
-                            for (int kk = 0; kk < SW / 32; ++kk)
-                                tc_mma_i8(tmem_d, ad + (uint64_t)(2 * kk),
-                                          bd + (uint64_t)(2 * kk), idesc,
-                                          (c | kk) != 0 ? 1u : 0u);
-                            tc_commit(a_empty + stage);
-                        }
+                    if (no_mma) {  // diagnostics: TMA + barrier protocol only
+                        if (lane == 0) mbar_arrive(a_empty + stage);
+                        __syncwarp();
+                    } else {
+                        // "mma-with-elect": the whole warp reaches the issue,
+                        // one lane issues (no divergent branch around it)
+                        const uint64_t ad = adesc0 + (uint64_t)((stage * a_stage_bytes) >> 4);
+                        const uint64_t bd = bdesc + (uint64_t)((c * N * SW) >> 4);
+                        mma_chunk_elect<SW / 32>(tmem_d, ad, bd, idesc, c == 0 ? 1u : 0u,
+                                                 smem_u32(a_empty + stage));
                     }
-                    __syncwarp();
                     if (++stage == p.stages) {
                         stage = 0;
                         aph ^= 1;
                     }
                 }
-                if (lane == 0) {
-                    if (no_mma) {
-                        if (!no_acc_wait) mbar_arrive(acc_full + acc);
-                    } else {
-                        // + bias_q on every row: constant A (127) x per-query digits
-                        if (!no_bias) tc_mma_i8(tmem_d, abias_desc, bbias_desc, idesc, 1u);
-                        tc_commit(acc_full + acc);
-                    }
+                if (no_mma) {
+                    if (lane == 0 && !no_acc_wait) mbar_arrive(acc_full + acc);
+                    __syncwarp();
+                } else {
+                    // + bias_q on every row: constant A (127) x per-query digits
+                    mma_bias_commit_elect(tmem_d, abias_desc, bbias_desc, idesc, no_bias ? 0u : 1u,
+                                          smem_u32(acc_full + acc));
                 }
-                __syncwarp();
                 if (++acc == 2) {
                     acc = 0;
                     accph ^= 1;
@@ -554,7 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     nhi = fmaxf(nhi, __shfl_xor_sync(0xffffffffu, nhi, o));
                 }
             }
-            mbar_wait_sleep(bias_empty + slot, ph ^ 1);
+            WSTAT(6, mbar_wait_sleep(bias_empty + slot, ph ^ 1));
             // the unit's row norms -> smem (bulk copy; the < 4 tail rows and
             // unaligned arrays by plain loads)
             const bool stage_norms = (M != kIP) && a.mode == 0;
@@ -633,7 +722,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const unsigned eb = __ballot_sync(0xffffffffu, exc);
                 if (lane == 0) exc_s[slot * (N / 32) + i] = eb != 0;
             }
-            if (stage_norms) mbar_wait_sleep(norm_full + slot, ph);
+            if (stage_norms) WSTAT(7, mbar_wait_sleep(norm_full + slot, ph));
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(bias_full + slot);
@@ -653,7 +742,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             unit_tb(p, u, t, b);
             const int64_t q0 = t * N;
             const int32_t unit_row0 = (int32_t)(a.r_lo + b * p.tiles_per_unit * kBlockM);
-            mbar_wait_sleep(stage_full + slot, ph);
+            WSTAT(8, mbar_wait_sleep(stage_full + slot, ph));
             if (a.mode == 0 && stage_n_all[slot] > 0) {
                 int32_t *qc = qcnt_all + slot * N;
                 const Staged *sb = stage_all + slot * stage_cap;
@@ -707,8 +796,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int nqt = (int)min((int64_t)N, a.nq - q0);
             // this unit's bias, thresholds and exception flags; a free
             // staging slot (the flush warp drained its previous use)
-            mbar_wait(bias_full + slot, ph);
-            mbar_wait(stage_free + slot, ph ^ 1);
+            WSTAT(9, mbar_wait(bias_full + slot, ph));
+            WSTAT(10, mbar_wait(stage_free + slot, ph ^ 1));
             int32_t *stage_n = stage_n_all + slot;
             int32_t *qcnt = qcnt_all + slot * N;
             Staged *stage_buf = stage_all + slot * stage_cap;
@@ -740,7 +829,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if ((excm >> ci) & 1u) excg |= ((1u << (kC / 8)) - 1u) << (ci * (kC / 8));
                 int32_t row = wrow0 + lane;
                 for (int ti = 0; ti < ntl; ++ti, row += kBlockM) {
-                    mbar_wait(acc_full + acc, accph);
+                    WSTAT(11, mbar_wait(acc_full + acc, accph));
                     tc_fence_after();
                     const uint32_t ta = tm_warp + (uint32_t)(acc * N);
                     int32_t v[kCB / kC][kC];
@@ -768,6 +857,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     hit = row < r_hi ? (hit | excg) : 0u;
                     if (!hit) continue;
+                    if (p.experiment == 8) continue;  // diagnostics: drop survivors
                     // slow path (lanes with a candidate group only): exact
                     // test of every non-negative column of a hit group
                     const int rowrel = row - unit_row0;
@@ -865,7 +955,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int ti = 0; ti < ntl; ++ti, wrow0 += kBlockM) {
                     const int32_t row = wrow0 + lane;
                     const bool valid = row < r_hi;
-                    if (acc_sync) mbar_wait(acc_full + acc, accph);
+                    if (acc_sync) {
+                        if (p.experiment == 11)
+                            WSTAT(12, mbar_wait_backoff<256>(acc_full + acc, accph));
+                        else
+                            WSTAT(12, mbar_wait(acc_full + acc, accph));
+                    }
                     tc_fence_after();
                     const uint32_t tbase = tm_warp + (uint32_t)(acc * N);
 #pragma unroll 1
@@ -920,6 +1015,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
 
+#ifdef QA_WAIT_STATS
+    if (lane == 0)
+        for (int i = 0; i < kWst; ++i)
+            if (wst[i]) atomicAdd(&wst_s[i], (unsigned long long)wst[i]);
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < 2)
+        printf("wst cta=%d total=%lld prod[b_empty=%llu a_empty=%llu] mma[b_full=%llu bias_full=%llu "
+               "acc_empty=%llu a_full=%llu] bias[bias_empty=%llu norm=%llu] flush[stage_full=%llu] "
+               "epi/16[bias_full=%llu stage_free=%llu acc_full=%llu acc_full_x=%llu]\n",
+               (int)blockIdx.x, clock64() - t_start, wst_s[0], wst_s[1], wst_s[2], wst_s[3],
+               wst_s[4], wst_s[5], wst_s[6], wst_s[7], wst_s[8], wst_s[9] / 16, wst_s[10] / 16,
+               wst_s[11] / 16, wst_s[12] / 16);
+#endif
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {
@@ -1019,7 +1127,7 @@ cudaError_t launch_t(const FilterArgs &a, cudaStream_t st) {
     if (stages > kn.max_stages) stages = kn.max_stages;
     p.stages = stages;
     const size_t smem = fixed + (size_t)stages * (stage_bytes + 16);
-    auto kern = (a.mode == 0 && p.experiment == 0) ? filter_tc_kernel<SW, N, M, true>
+    auto kern = (a.mode == 0 && (p.experiment == 0 || p.experiment == 8)) ? filter_tc_kernel<SW, N, M, true>
                                                    : filter_tc_kernel<SW, N, M, false>;
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
