@@ -306,6 +306,18 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, int32_t (&v)[C]) {
     }
 }
 
+// Shared-memory atomics / stores by 32-bit shared address.  (Through a
+// generic pointer the compiler emits generic ATOM / ST, an order of
+// magnitude slower on the survivor path.)
+__device__ __forceinline__ int32_t atom_add_smem(uint32_t addr, int32_t v) {
+    int32_t old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void sts64(uint32_t addr, uint32_t a, uint32_t b) {
+    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
+}
+
 __device__ __forceinline__ int32_t lds32(uint32_t addr) {
     int32_t r;
     asm volatile("ld.shared.b32 %0, [%1];" : "=r"(r) : "r"(addr));
@@ -405,10 +417,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
 
     // ---- shared memory carve-up (1024-aligned operand buffers) ----
-    uintptr_t base = ((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023;
+    // (pointer arithmetic on the __shared__ array, not integer casts: the
+    // compiler then knows every derived pointer is shared memory and emits
+    // LDS / STS / ATOMS instead of generic accesses)
+    unsigned char *sA = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t a_stage_bytes = kBlockM * SW;
     const uint32_t b_bytes = (uint32_t)N * (uint32_t)a.kdim;
-    unsigned char *sA = (unsigned char *)base;
     unsigned char *sB = sA + (size_t)p.stages * a_stage_bytes;
     // the query tile is double-buffered across work units when two copies fit
     // in 64 KiB, else single-buffered (one MMA bubble per unit switch)
@@ -799,8 +813,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             WSTAT(9, mbar_wait(bias_full + slot, ph));
             WSTAT(10, mbar_wait(stage_free + slot, ph ^ 1));
             int32_t *stage_n = stage_n_all + slot;
-            int32_t *qcnt = qcnt_all + slot * N;
-            Staged *stage_buf = stage_all + slot * stage_cap;
+            const uint32_t stage_n_addr = smem_u32(stage_n);
+            const uint32_t qcnt_addr = smem_u32(qcnt_all + slot * N);
+            const uint32_t stage_addr = smem_u32(stage_all + slot * stage_cap);
             const int64_t tile0 = b * p.tiles_per_unit;
             const int64_t tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
             const uint32_t thr_addr = smem_u32(thr_all + slot * N);
@@ -893,12 +908,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                               (uint32_t)lds32(bias_addr + 4u * (uint32_t)qloc));
                                 const int32_t T = lds32(thr_addr + 4u * (uint32_t)qloc);
                                 if (!passes<M>(dot, T, xx, inv_xn)) continue;
-                                const int e = atomicAdd(stage_n, 1);
+                                const int e = atom_add_smem(stage_n_addr, 1);
                                 if (e < stage_cap) {
-                                    const int sq = atomicAdd(qcnt + qloc, 1);
-                                    stage_buf[e] = Staged{(uint32_t)qloc | ((uint32_t)sq << 8) |
-                                                              ((uint32_t)rowrel << 20),
-                                                          dot};
+                                    const int sq = atom_add_smem(qcnt_addr + 4u * (uint32_t)qloc, 1);
+                                    sts64(stage_addr + 8u * (uint32_t)e,
+                                          (uint32_t)qloc | ((uint32_t)sq << 8) | ((uint32_t)rowrel << 20),
+                                          (uint32_t)dot);
                                 } else {
                                     // staging full: direct append (slow, rare)
                                     const int32_t s = atomicAdd(a.ccount + q0 + qloc, 1);
