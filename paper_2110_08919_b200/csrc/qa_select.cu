@@ -25,6 +25,11 @@ namespace {
 
 constexpr int kChunk = 256;  // candidates sorted per merge step
 constexpr int kWarpsMax = 8;
+// select_reg_kernel occupancy: 6 blocks of 8 warps per SM (<= 40 registers;
+// a few bytes spill) measured faster than 5 at 48 registers.
+#ifndef QA_SEL_MINB
+#define QA_SEL_MINB 6
+#endif
 
 __device__ __forceinline__ int next_pow2(int v) {
     int p = 1;
@@ -324,7 +329,7 @@ __device__ __forceinline__ void rsort128(K (&x)[4]) {
 }
 
 template <int M, typename K>
-__global__ void __launch_bounds__(256) select_reg_kernel(SelectArgs a) {
+__global__ void __launch_bounds__(256, QA_SEL_MINB) select_reg_kernel(SelectArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (q >= a.nq) return;
