@@ -25,10 +25,10 @@ namespace {
 
 constexpr int kChunk = 256;  // candidates sorted per merge step
 constexpr int kWarpsMax = 8;
-// select_reg_kernel occupancy: 6 blocks of 8 warps per SM (<= 40 registers;
-// a few bytes spill) measured faster than 5 at 48 registers.
+// select_reg_kernel occupancy: 5 blocks of 8 warps per SM (<= 48 registers)
+// measured best with the branch-free compare-exchange (6 spills more).
 #ifndef QA_SEL_MINB
-#define QA_SEL_MINB 6
+#define QA_SEL_MINB 5
 #endif
 
 __device__ __forceinline__ int next_pow2(int v) {
@@ -233,7 +233,15 @@ struct RKey96 {
 
 __device__ __forceinline__ bool rlt(const RKey64 &a, const RKey64 &b) { return a.k < b.k; }
 __device__ __forceinline__ bool rlt(const RKey96 &a, const RKey96 &b) {
-    return a.k < b.k || (a.k == b.k && a.id < b.id);
+    // no short-circuit: predicates combine without branches
+    return (a.k < b.k) | ((a.k == b.k) & (a.id < b.id));
+}
+// c ? a : b, field by field (compiles to SEL, no divergent branch)
+__device__ __forceinline__ RKey64 rsel(bool c, const RKey64 &a, const RKey64 &b) {
+    return RKey64{c ? a.k : b.k};
+}
+__device__ __forceinline__ RKey96 rsel(bool c, const RKey96 &a, const RKey96 &b) {
+    return RKey96{c ? a.k : b.k, c ? a.id : b.id};
 }
 __device__ __forceinline__ RKey64 rshfl(const RKey64 &a, int m) {
     return RKey64{__shfl_xor_sync(0xffffffffu, a.k, m)};
@@ -284,8 +292,7 @@ template <typename K>
 __device__ __forceinline__ K rget(const K (&x)[4], int i) {
     K v = x[0];
 #pragma unroll
-    for (int e = 1; e < 4; ++e)
-        if ((i >> 5) == e) v = x[e];
+    for (int e = 1; e < 4; ++e) v = rsel((i >> 5) == e, x[e], v);
     return rbcast(v, i & 31);
 }
 
@@ -300,11 +307,11 @@ __device__ __forceinline__ void rstage(K (&x)[4], int size, int stride) {
             const int p = e ^ es;
             if (p > e) {
                 const bool up = (((e * 32 + lane) & size) == 0);
-                if (up ? rlt(x[p], x[e]) : rlt(x[e], x[p])) {
-                    K t = x[e];
-                    x[e] = x[p];
-                    x[p] = t;
-                }
+                const bool sw = up ? rlt(x[p], x[e]) : rlt(x[e], x[p]);
+                const K lo = rsel(sw, x[p], x[e]);
+                const K hi = rsel(sw, x[e], x[p]);
+                x[e] = lo;
+                x[p] = hi;
             }
         }
     } else {
@@ -315,7 +322,7 @@ __device__ __forceinline__ void rstage(K (&x)[4], int size, int stride) {
             const K o = rshfl(x[e], stride);
             // the lower index of an ascending pair keeps the min
             const bool take = (lower == up) ? rlt(o, x[e]) : rlt(x[e], o);
-            if (take) x[e] = o;
+            x[e] = rsel(take, o, x[e]);
         }
     }
 }
@@ -403,8 +410,7 @@ __global__ void __launch_bounds__(256, QA_SEL_MINB) select_reg_kernel(SelectArgs
         for (int e = 0; e < 4; ++e) r[e] = rshfl(s[3 - e], 31);
         // stride-128 step of the bitonic merge: T keeps the 128 smallest
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-            if (rlt(r[e], t[e])) t[e] = r[e];
+        for (int e = 0; e < 4; ++e) t[e] = rsel(rlt(r[e], t[e]), r[e], t[e]);
         // t is bitonic now: finish the merge with strides 64..1 (size 128,
         // ascending everywhere)
 #pragma unroll
