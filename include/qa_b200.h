@@ -104,6 +104,22 @@ int qa_scan_topk_i8_host(const int8_t *data, int64_t n, int64_t d,
                          const float *query_norms, double *out_scores,
                          int32_t *out_ids);
 
+/* ---- float32 exhaustive search (_core.pyx:270-298 _scan_f32) ----
+ * Replaces scan_topk() with float32 data/queries (_core.pyx:333-365, the
+ * dtype == float32 branch 361-362) and norms() on float32 rows
+ * (_core.pyx:150-153).  Scores are the reference's float64 values bit for
+ * bit: each pair is summed sequentially over j (product exact in float64,
+ * explicit round-to-nearest adds); rows ascending by (score, id), ids + id_offset.
+ * db_norm/q_norm (float32, the caller's) are read for metric 2 only.  Inputs
+ * must be finite (the reference's heap order with NaN scores is
+ * insertion-order dependent).  keff = min(k, n) <= 2048.  Asynchronous. */
+int qa_scan_topk_f32(const float *db, int64_t n, int64_t d, int64_t ldd,
+                     const float *db_norm, const float *q, int64_t nq, int64_t ldq,
+                     const float *q_norm, int64_t k, int metric, int64_t id_offset,
+                     double *out_scores, int32_t *out_ids, void *stream);
+/* out[i] = (float)sqrt(sequential float64 sum of x[i, j]^2). */
+int qa_norms_f32(const float *x, int64_t n, int64_t d, int64_t ldx, float *out, void *stream);
+
 /* ---- index layout ----
  * perm = rows ordered by ascending squared norm (stable), and the gather
  * that applies it to codes + norms (norm/norm_out may be NULL).  An index

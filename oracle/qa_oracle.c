@@ -12,6 +12,8 @@
  *   qo_norms_i8      _core.pyx:137-157     (norms, int8 branch via _sumsq_i 66-74)
  *   qo_minmax_f32    per-dim min/max (quantizer.py:196-197 block.min/max)
  *   qo_scan_topk_i8  _core.pyx:301-365     (_scan_i8 + scan_topk; pair kernel 49-96)
+ *   qo_norms_f32     _core.pyx:150-153     (norms, float32 branch via _dot_f 32-37)
+ *   qo_scan_topk_f32 _core.pyx:270-298     (_scan_f32; pair kernel 32-46, 75-84)
  *
  * Pinned against the reference's own compiled _core (oracle/_ref) and against
  * the golden vectors in tests/golden/ -- see tests/test_oracle.py.
@@ -162,6 +164,75 @@ int64_t qo_scan_topk_i8(const int8_t *X, int64_t n, int64_t d, const int8_t *Q,
                 }
             }
             /* pop worst-first into descending slots -> ascending rows */
+            for (int j = size - 1; j >= 0; --j) {
+                out_d[q * keff + j] = hd[0];
+                out_i[q * keff + j] = hi[0];
+                --size;
+                hd[0] = hd[size];
+                hi[0] = hi[size];
+                heap_sift_down(hd, hi, size, 0);
+            }
+        }
+        free(hd);
+        free(hi);
+    }
+    return keff;
+}
+
+/* ---- float32 path: _core.pyx:32-46 (_dot_f/_l2_f), 75-84 (_pair_f),
+ * 150-153 (norms, float32 branch), 270-298 (_scan_f32).  Sequential float64
+ * accumulation in j order; built with -ffp-contract=off so t*t and the adds
+ * round separately exactly as the reference's C does (no FMA on x86-64
+ * baseline). ------------------------------------------------------------ */
+static inline double pair_f32(const float *a, const float *b, int64_t d, int metric,
+                              double na, double nb) {
+    double acc = 0.0;
+    if (metric == 1) {
+        for (int64_t j = 0; j < d; ++j) {
+            double t = (double)a[j] - (double)b[j];
+            acc += t * t;
+        }
+        return acc;
+    }
+    for (int64_t j = 0; j < d; ++j) acc += (double)a[j] * (double)b[j];
+    if (metric == 0) return -acc;
+    return 1.0 - acc / (na * nb);
+}
+
+void qo_norms_f32(const float *x, int64_t n, int64_t d, float *out) {
+    for (int64_t i = 0; i < n; ++i) {
+        double acc = 0.0;
+        for (int64_t j = 0; j < d; ++j) acc += (double)x[i * d + j] * (double)x[i * d + j];
+        out[i] = (float)sqrt(acc);
+    }
+}
+
+int64_t qo_scan_topk_f32(const float *X, int64_t n, int64_t d, const float *Q, int64_t nq,
+                         int64_t k, int metric, const float *xn, const float *qn,
+                         double *out_d, int32_t *out_i) {
+    int64_t keff = k < n ? k : n;
+    if (n == 0 || nq == 0 || keff == 0) return keff;
+#pragma omp parallel
+    {
+        double *hd = (double *)malloc(sizeof(double) * (size_t)(keff + 1));
+        int *hi = (int *)malloc(sizeof(int) * (size_t)(keff + 1));
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t q = 0; q < nq; ++q) {
+            const float *qp = Q + q * d;
+            double qnorm = metric == 2 ? (double)qn[q] : 0.0;
+            int size = 0;
+            for (int64_t r = 0; r < n; ++r) {
+                double dv = pair_f32(qp, X + r * d, d, metric, qnorm,
+                                     metric == 2 ? (double)xn[r] : 0.0);
+                if (size < keff) {
+                    heap_push(hd, hi, size, dv, (int)r);
+                    ++size;
+                } else if (lex_gt(hd[0], hi[0], dv, (int)r)) {
+                    hd[0] = dv;
+                    hi[0] = (int)r;
+                    heap_sift_down(hd, hi, size, 0);
+                }
+            }
             for (int j = size - 1; j >= 0; --j) {
                 out_d[q * keff + j] = hd[0];
                 out_i[q * keff + j] = hi[0];

@@ -43,6 +43,10 @@ def lib():
         L.qo_minmax_f32.restype = None
         L.qo_scan_topk_i8.argtypes = [vp, i64, i64, vp, i64, i64, ctypes.c_int, vp, vp, vp, vp]
         L.qo_scan_topk_i8.restype = i64
+        L.qo_norms_f32.argtypes = [vp, i64, i64, vp]
+        L.qo_norms_f32.restype = None
+        L.qo_scan_topk_f32.argtypes = [vp, i64, i64, vp, i64, i64, ctypes.c_int, vp, vp, vp, vp]
+        L.qo_scan_topk_f32.restype = i64
         _LIB = L
     return _LIB
 
@@ -93,6 +97,30 @@ def scan_topk_i8(X, Q, k, metric, xn=None, qn=None):
         qn = np.ascontiguousarray(qn, dtype=np.float32)
     lib().qo_scan_topk_i8(_ptr(X), n, d, _ptr(Q), nq, int(k), int(metric), _ptr(xn), _ptr(qn),
                           _ptr(od), _ptr(oi))
+    return od, oi
+
+
+def norms_f32(x: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.empty(x.shape[0], dtype=np.float32)
+    lib().qo_norms_f32(_ptr(x), x.shape[0], x.shape[1], _ptr(out))
+    return out
+
+
+def scan_topk_f32(X, Q, k, metric, xn=None, qn=None):
+    """_scan_f32 restated (float64 sequential sums, (score, id) heap)."""
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    Q = np.ascontiguousarray(Q, dtype=np.float32)
+    n, d = X.shape
+    nq = Q.shape[0]
+    keff = min(int(k), n)
+    od = np.empty((nq, keff), dtype=np.float64)
+    oi = np.empty((nq, keff), dtype=np.int32)
+    if metric == 2:
+        xn = np.ascontiguousarray(xn, dtype=np.float32)
+        qn = np.ascontiguousarray(qn, dtype=np.float32)
+    lib().qo_scan_topk_f32(_ptr(X), n, d, _ptr(Q), nq, int(k), int(metric), _ptr(xn), _ptr(qn),
+                           _ptr(od), _ptr(oi))
     return od, oi
 
 

@@ -14,8 +14,9 @@ Surface (host numpy in, host numpy out, reference semantics):
 * ``quantize(values, k, sb, se, bits)`` -> int8 [n, d] -- the encode hook the
   reference lacks (its quantizer.py:291-300 calls numpy directly).
 
-float32 exhaustive search (``_scan_f32``) is the next item of SURVEY.md §8f
-and is not provided by this build: float32 inputs raise NotImplementedError.
+float32 inputs take the float64-exact path (``qa_scan_topk_f32`` /
+``qa_norms_f32``, bit-exact with ``_scan_f32`` and the float32 ``norms``
+branch, _core.pyx:150-153, 270-298): the ground truth for recall.
 """
 
 from __future__ import annotations
@@ -27,6 +28,12 @@ from . import device as _dev
 from ._lib import lib  # noqa: F401  (fails loudly when the library is missing)
 
 BACKEND = "cuda"
+
+
+def _to_dev(arr: np.ndarray, dev) -> torch.Tensor:
+    """Upload a (possibly read-only) host array without writing to it."""
+    arr = np.ascontiguousarray(arr)
+    return torch.from_numpy(arr if arr.flags.writeable else arr.copy()).to(dev)
 
 
 def _check_pair(data, queries):
@@ -50,9 +57,17 @@ def scan_topk(data, queries, k, metric, data_norms=None, query_norms=None):
     if int(metric) == 2 and (data_norms is None or query_norms is None
                              or data_norms.shape[0] != n or query_norms.shape[0] != nq):
         raise ValueError("angular metric needs data and query norms")
-    if data.dtype != np.int8:
-        raise NotImplementedError("float32 exhaustive search is not provided by the cuda backend")
     dev = _dev.default_device()
+    if data.dtype == np.float32:
+        dn = qn = None
+        if int(metric) == 2:
+            dn = torch.from_numpy(np.ascontiguousarray(data_norms, dtype=np.float32)).to(dev)
+            qn = torch.from_numpy(np.ascontiguousarray(query_norms, dtype=np.float32)).to(dev)
+        scores, ids = _dev.scan_topk_f32(_to_dev(data, dev), _to_dev(queries, dev), int(k),
+                                         int(metric), dn, qn)
+        return scores.cpu().numpy(), ids.cpu().numpy()
+    if data.dtype != np.int8:
+        raise ValueError("dtype must be float32 or int8")
     db = _dev.DeviceCodes.from_host(data, dev)
     qs = _dev.DeviceCodes.from_host(queries, dev)
     dn = qn = None
@@ -70,8 +85,10 @@ def norms(mat):
     n, d = mat.shape
     if n == 0 or d == 0:
         return np.zeros(n, dtype=np.float32)
+    if mat.dtype == np.float32:
+        return _dev.norms_f32(_to_dev(mat, _dev.default_device())).cpu().numpy()
     if mat.dtype != np.int8:
-        raise NotImplementedError("float32 norms are not provided by the cuda backend")
+        raise ValueError("dtype must be float32 or int8")
     dc = _dev.DeviceCodes.from_host(mat)
     return dc.norm.cpu().numpy()
 

@@ -66,6 +66,12 @@ SIGNATURES = {
         c_int,
         [c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_int, c_vp, c_vp, c_vp, c_vp],
     ),
+    "qa_scan_topk_f32": (
+        c_int,
+        [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_int, c_i64,
+         c_vp, c_vp, c_vp],
+    ),
+    "qa_norms_f32": (c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
     "qa_merge_topk": (c_int, [c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "qa_debug_dots_i8": (c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_int, c_vp, c_vp]),
     "qa_last_scan_stats": (c_int, [ctypes.POINTER(ScanStats)]),

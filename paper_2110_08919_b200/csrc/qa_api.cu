@@ -120,6 +120,7 @@ struct Buf {
 struct Workspace {
     std::mutex mu;
     Buf state, state_cnt, thr, cand, ccount, ovf, flags, scratch, grp, est;
+    Buf f32_scores, f32_ss, f32_si, f32_sn;  // float32 exact search (qa_exact_f32.cu)
 };
 
 constexpr int kMaxDevices = 64;
@@ -650,6 +651,57 @@ int qa_scan_topk_i8_host(const int8_t *data, int64_t n, int64_t d, const int8_t 
     cudaFree(dids);
     cudaStreamDestroy(st);
     return rc;
+}
+
+int qa_norms_f32(const float *x, int64_t n, int64_t d, int64_t ldx, float *out, void *stream) {
+    if (n < 0 || d < 0 || ldx < d) return set_err(QA_EINVAL, "bad shape");
+    QA_TRY(launch_norms_f32(x, n, d, ldx, out, (cudaStream_t)stream), "norms");
+    return QA_OK;
+}
+
+// float32 exhaustive search: rows in rounds of kF32Rows; every round scores
+// (query chunk x round rows) in float64 exactly as _scan_f32 does, then the
+// select kernel merges the round into each query's (score, id) state.
+int qa_scan_topk_f32(const float *db, int64_t n, int64_t d, int64_t ldd, const float *db_norm,
+                     const float *q, int64_t nq, int64_t ldq, const float *q_norm, int64_t k,
+                     int metric, int64_t id_offset, double *out_scores, int32_t *out_ids,
+                     void *stream) {
+    if (metric < 0 || metric > 2) return set_err(QA_EINVAL, "unknown metric %d", metric);
+    if (k < 0) return set_err(QA_EINVAL, "k must be >= 0");
+    if (n < 0 || nq < 0 || d < 0 || ldd < d || ldq < d) return set_err(QA_EINVAL, "bad shape");
+    const int64_t keff = std::min(k, n);
+    if (n == 0 || nq == 0 || keff == 0) return QA_OK;
+    if (metric == kAngular && (!db_norm || !q_norm))
+        return set_err(QA_EINVAL, "angular metric needs data and query norms");
+    if (keff > kMaxK) return set_err(QA_EUNSUPPORTED, "k above this build's limit");
+    if (n > INT32_MAX || d > INT32_MAX) return set_err(QA_EUNSUPPORTED, "shape above this build's limit");
+    cudaStream_t st = (cudaStream_t)stream;
+    Workspace &ws = g_ws[current_device() % kMaxDevices];
+    std::lock_guard<std::mutex> lock(ws.mu);
+    constexpr int64_t kF32Rows = 16384, kF32Queries = 1024;
+    const int64_t R = std::min(n, kF32Rows);
+    const int64_t qc = std::min(nq, kF32Queries);
+    QA_TRY(ws.f32_scores.reserve((size_t)qc * R * 8), "workspace");
+    QA_TRY(ws.f32_ss.reserve((size_t)qc * keff * 8), "workspace");
+    QA_TRY(ws.f32_si.reserve((size_t)qc * keff * 4), "workspace");
+    QA_TRY(ws.f32_sn.reserve((size_t)qc * 4), "workspace");
+    double *sc = (double *)ws.f32_scores.ptr, *ss = (double *)ws.f32_ss.ptr;
+    int32_t *si = (int32_t *)ws.f32_si.ptr, *sn = (int32_t *)ws.f32_sn.ptr;
+    for (int64_t c0 = 0; c0 < nq; c0 += qc) {
+        const int64_t m = std::min(qc, nq - c0);
+        QA_TRY(cudaMemsetAsync(sn, 0, (size_t)m * 4, st), "memset");
+        for (int64_t r0 = 0; r0 < n; r0 += R) {
+            const int64_t rows = std::min(R, n - r0);
+            QA_TRY(launch_f32_scores(db, ldd, q + c0 * ldq, ldq, d, m, r0, rows, metric, db_norm,
+                                     q_norm ? q_norm + c0 : nullptr, sc, R, st),
+                   "f32 scores");
+            QA_TRY(launch_f32_select(sc, R, rows, r0, ss, si, sn, m, keff, st), "f32 select");
+        }
+        QA_TRY(launch_f32_finalize(ss, si, m, keff, id_offset, out_scores + c0 * keff,
+                                   out_ids + c0 * keff, st),
+               "f32 finalize");
+    }
+    return QA_OK;
 }
 
 int qa_order_rows_by_norm(const int32_t *sqnorm, int64_t n, int32_t *perm, void *stream) {

@@ -109,6 +109,20 @@ cudaError_t launch_merge(const double *in_scores, const int32_t *in_ids, int64_t
                          int64_t kin, int64_t k, double *out_scores, int32_t *out_ids,
                          cudaStream_t st);
 
+// float32 exhaustive search (qa_exact_f32.cu), bit-exact with _scan_f32.
+cudaError_t launch_f32_scores(const float *db, int64_t ldd, const float *q, int64_t ldq, int64_t d,
+                              int64_t nq, int64_t r_lo, int64_t rows, int metric,
+                              const float *db_norm, const float *q_norm, double *out, int64_t ldo,
+                              cudaStream_t st);
+cudaError_t launch_f32_select(const double *scores, int64_t lds, int64_t rows, int64_t id0,
+                              double *st_s, int32_t *st_i, int32_t *st_n, int64_t nq, int64_t k,
+                              cudaStream_t st);
+cudaError_t launch_f32_finalize(const double *st_s, const int32_t *st_i, int64_t nq, int64_t k,
+                                int64_t id_offset, double *out_s, int32_t *out_i, cudaStream_t st);
+cudaError_t launch_norms_f32(const float *x, int64_t n, int64_t d, int64_t ldx, float *out,
+                             cudaStream_t st);
+size_t f32_select_smem(int64_t k);
+
 // Largest list the select kernel sorts in shared memory at once.
 constexpr int64_t kSortMax = 8192;
 // Largest k served (k + one candidate chunk must fit kSortMax).

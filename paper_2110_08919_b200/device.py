@@ -175,6 +175,39 @@ def scan_topk(db: DeviceCodes, q: DeviceCodes, k: int, metric: int, db_norm=None
     return scores, ids
 
 
+def _f32_matrix(x: torch.Tensor, what: str) -> torch.Tensor:
+    if x.dtype != torch.float32 or x.dim() != 2 or not x.is_cuda:
+        raise ValueError(f"{what} must be a float32 [n, d] CUDA tensor")
+    return x if x.stride(1) == 1 else x.contiguous()
+
+
+def norms_f32(x: torch.Tensor) -> torch.Tensor:
+    """float32(sqrt(sequential float64 sum of x^2)) per row (_core.pyx:150-153)."""
+    x = _f32_matrix(x, "x")
+    out = torch.empty((x.shape[0],), dtype=torch.float32, device=x.device)
+    check(lib.qa_norms_f32(_p(x), x.shape[0], x.shape[1], x.stride(0), _p(out), _stream()))
+    return out
+
+
+def scan_topk_f32(db: torch.Tensor, q: torch.Tensor, k: int, metric: int, db_norm=None,
+                  q_norm=None, id_offset: int = 0):
+    """float32 exhaustive top-k, bit-exact with the reference's _scan_f32
+    (_core.pyx:270-298): float64 scores, rows ascending by (score, id)."""
+    db = _f32_matrix(db, "data")
+    q = _f32_matrix(q, "queries")
+    if db.shape[1] != q.shape[1]:
+        raise ValueError("dimension mismatch between data and queries")
+    if k < 0:
+        raise ValueError("k must be >= 0")
+    keff = min(k, db.shape[0])
+    scores = torch.empty((q.shape[0], keff), dtype=torch.float64, device=db.device)
+    ids = torch.empty((q.shape[0], keff), dtype=torch.int32, device=db.device)
+    check(lib.qa_scan_topk_f32(_p(db), db.shape[0], db.shape[1], db.stride(0), _p(db_norm),
+                               _p(q), q.shape[0], q.stride(0), _p(q_norm), int(k), int(metric),
+                               int(id_offset), _p(scores), _p(ids), _stream()))
+    return scores, ids
+
+
 def merge_topk(scores: torch.Tensor, ids: torch.Tensor, k: int):
     """Merge G per-shard sorted lists [G, nq, kin] (global ids) into the
     (score, id)-first k per query."""

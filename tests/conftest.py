@@ -39,6 +39,11 @@ def golden_scan():
 
 
 @pytest.fixture(scope="session")
+def golden_scan_f32():
+    return _split(np.load(GOLDEN / "scan_f32_cases.npz"))
+
+
+@pytest.fixture(scope="session")
 def golden_cfg():
     return _split(np.load(GOLDEN / "cfg_minis.npz"))
 

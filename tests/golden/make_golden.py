@@ -107,6 +107,50 @@ def scan_cases(core):
     return count
 
 
+def scan_f32_cases(core):
+    """float32 exhaustive search (_scan_f32) known answers: mixed scales,
+    integer-valued rows (exact score ties), duplicated rows, signed zeros,
+    d not a multiple of the GPU's 16-dim stage."""
+    arrays = {}
+    rng = np.random.default_rng(11)
+    count = 0
+    for i in range(30):
+        metric = i % 3
+        n = int(rng.integers(1, 500))
+        d = int(rng.integers(1, 150)) if i % 5 else int(rng.integers(1, 8))
+        nq = int(rng.integers(1, 5))
+        kind = i % 4
+        if kind == 0:
+            X = rng.normal(size=(n, d)) * rng.uniform(0.01, 100.0, size=d)
+            Q = rng.normal(size=(nq, d)) * rng.uniform(0.01, 100.0, size=d)
+        elif kind == 1:   # integer-valued: many exactly tied scores
+            X = rng.integers(-3, 4, size=(n, d)).astype(np.float64)
+            Q = rng.integers(-3, 4, size=(nq, d)).astype(np.float64)
+        elif kind == 2:   # sift-like non-negative
+            X = np.clip(np.round(np.abs(rng.normal(0, 40, size=(n, d)))), 0, 255)
+            Q = np.clip(np.round(np.abs(rng.normal(0, 40, size=(nq, d)))), 0, 255)
+        else:             # duplicated rows and signed zeros
+            base = rng.normal(size=(max(1, n // 3), d))
+            X = base[rng.integers(0, base.shape[0], size=n)]
+            X[rng.random((n, d)) < 0.2] = -0.0
+            Q = rng.normal(size=(nq, d))
+        X = X.astype(np.float32)
+        Q = Q.astype(np.float32)
+        if metric == 2:
+            X[~X.any(axis=1), 0] = 1.0
+            Q[~Q.any(axis=1), 0] = 1.0
+        k = int(rng.choice([1, 10, 100, n, n + 1]))
+        xn, qn = core.norms(X), core.norms(Q)
+        sc, ids = core.scan_topk(X, Q, k, metric, xn, qn)
+        pre = f"f{i}"
+        arrays.update({f"{pre}__X": X, f"{pre}__Q": Q, f"{pre}__k": np.int64(k),
+                       f"{pre}__metric": np.int64(metric), f"{pre}__xn": xn,
+                       f"{pre}__qn": qn, f"{pre}__scores": sc, f"{pre}__ids": ids})
+        count += 1
+    np.savez_compressed(OUT / "scan_f32_cases.npz", **arrays)
+    return count
+
+
 def cfg_minis(qa, core):
     """BASELINE cfg0 (L2, min/max) and cfg1 (angular, symmetric) at reduced
     size through the reference pipeline: constructed stats -> fit(ABS_MAX)
@@ -149,10 +193,17 @@ def cfg_minis(qa, core):
 
 def main():
     qa, core = load_reference()
+    if len(sys.argv) > 1:   # regenerate only the named fixtures, e.g. scan_f32
+        for name in sys.argv[1:]:
+            fn = {"encode": lambda: encode_cases(qa), "scan": lambda: scan_cases(core),
+                  "scan_f32": lambda: scan_f32_cases(core), "cfg": lambda: cfg_minis(qa, core)}[name]
+            print(name, fn())
+        return
+    nf = scan_f32_cases(core)
     ne = encode_cases(qa)
     ns = scan_cases(core)
     cfg_minis(qa, core)
-    print(f"wrote {ne} encode cases, {ns} scan cases, cfg minis to {OUT}")
+    print(f"wrote {ne} encode cases, {ns} scan cases, {nf} float32 scan cases, cfg minis to {OUT}")
 
 
 if __name__ == "__main__":

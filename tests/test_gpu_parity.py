@@ -264,6 +264,58 @@ def test_cfg0_full_parity(oracle):
     np.testing.assert_array_equal(sc.cpu().numpy(), osc)
 
 
+# ------------------------------------------- float32 exact search (8f-1) --
+
+def test_scan_f32_golden(golden_scan_f32):
+    for name, c in golden_scan_f32.items():
+        np.testing.assert_array_equal(_backend.norms(c["X"]), c["xn"], err_msg=name)
+        sc, ids = _backend.scan_topk(c["X"], c["Q"], int(c["k"]), int(c["metric"]), c["xn"],
+                                     c["qn"])
+        np.testing.assert_array_equal(ids, c["ids"], err_msg=name)
+        np.testing.assert_array_equal(sc, c["scores"], err_msg=name)
+
+
+@pytest.mark.parametrize("metric", [0, 1, 2])
+def test_scan_f32_vs_oracle_multi_round(oracle, metric):
+    # n spans several 16384-row rounds and nq several 1024-query chunks'
+    # worth of CTA tiles; k = 1, 100, 2048 (the limit)
+    rng = np.random.default_rng(31 + metric)
+    X = (rng.normal(size=(40_000, 77)) * rng.uniform(0.1, 5, size=77)).astype(np.float32)
+    X[5000:5100] = X[:100]            # duplicated rows: exact score ties
+    Q = (rng.normal(size=(70, 77)) * rng.uniform(0.1, 5, size=77)).astype(np.float32)
+    xn, qn = oracle.norms_f32(X), oracle.norms_f32(Q)
+    for k in (1, 100, 2048):
+        sc, ids = _backend.scan_topk(X, Q, k, metric, xn, qn)
+        osc, oids = oracle.scan_topk_f32(X, Q, k, metric, xn, qn)
+        np.testing.assert_array_equal(ids, oids)
+        np.testing.assert_array_equal(sc, osc)
+
+
+def test_scan_f32_many_queries_and_id_offset(oracle):
+    rng = np.random.default_rng(8)
+    X = np.round(rng.normal(size=(3000, 20)) * 3).astype(np.float32)   # heavy ties
+    Q = np.round(rng.normal(size=(2500, 20)) * 3).astype(np.float32)   # > 1 query chunk
+    sc, ids = dev.scan_topk_f32(torch.from_numpy(X).cuda(), torch.from_numpy(Q).cuda(), 10, 1,
+                                id_offset=1000)
+    osc, oids = oracle.scan_topk_f32(X, Q, 10, 1)
+    np.testing.assert_array_equal(ids.cpu().numpy(), oids + 1000)
+    np.testing.assert_array_equal(sc.cpu().numpy(), osc)
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 3])
+def test_ground_truth_and_recall_cfg_minis(golden_cfg, cfg):
+    # GPU float32 ground truth == the reference's (gt32 fixture), and the
+    # int8 search's recall against it equals the reference's exactly
+    g = golden_cfg[f"cfg{cfg}"]
+    X, Q = synth.generate(cfg, n=6000, nq=24)
+    metric = qa.Metric(synth.CONFIGS[cfg]["metric"])
+    gt = qa.batch_ground_truth(qa.DenseDataset(X), qa.DenseDataset(Q), 100, metric)
+    np.testing.assert_array_equal(gt.ids, g["gt32"])
+    r = qa.recall_at_k(gt, g["ids"], 100)
+    r_ref = qa.recall_at_k(qa.GroundTruth(g["gt32"]), g["ids"], 100)
+    assert r.mean == r_ref.mean
+
+
 # ------------------------------------------------------------ sharding --
 
 @pytest.mark.parametrize("G", [2, 3, 8])

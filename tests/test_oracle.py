@@ -104,3 +104,47 @@ def test_oracle_equals_reference_kernel_on_fresh_instances(oracle):
         b = core.scan_topk(X, Q, k, metric, xn, qn)
         np.testing.assert_array_equal(a[1], b[1])
         np.testing.assert_array_equal(a[0], b[0])
+
+
+# ----------------------------------------------- float32 path (_scan_f32) --
+
+def test_scan_f32_matches_reference_golden(oracle, golden_scan_f32):
+    for name, c in golden_scan_f32.items():
+        np.testing.assert_array_equal(oracle.norms_f32(c["X"]), c["xn"], err_msg=name)
+        sc, ids = oracle.scan_topk_f32(c["X"], c["Q"], int(c["k"]), int(c["metric"]), c["xn"],
+                                       c["qn"])
+        np.testing.assert_array_equal(ids, c["ids"], err_msg=name)
+        np.testing.assert_array_equal(sc, c["scores"], err_msg=name)
+
+
+def test_scan_f32_cfg_minis_ground_truth(oracle, golden_cfg):
+    # the reference's float32 ground truth of the reduced BASELINE pipelines
+    for cfg in (0, 1, 3):
+        X, Q = synth.generate(cfg, n=6000, nq=24)
+        metric = synth.CONFIGS[cfg]["metric"]
+        _, ids = oracle.scan_topk_f32(X, Q, 100, metric, oracle.norms_f32(X), oracle.norms_f32(Q))
+        np.testing.assert_array_equal(ids, golden_cfg[f"cfg{cfg}"]["gt32"])
+
+
+def test_scan_f32_equals_reference_kernel_on_fresh_instances(oracle):
+    core = oracle.ref_core()
+    if core is None:
+        pytest.skip("reference _core not built here (make -C oracle ref)")
+    rng = np.random.default_rng(77)
+    for i in range(24):
+        n, d, nq = int(rng.integers(1, 700)), int(rng.integers(1, 90)), int(rng.integers(1, 4))
+        metric = i % 3
+        X = (rng.normal(size=(n, d)) * 10 ** rng.uniform(-3, 3, size=d)).astype(np.float32)
+        Q = (rng.normal(size=(nq, d)) * 10 ** rng.uniform(-3, 3, size=d)).astype(np.float32)
+        if i % 4 == 0:
+            X = np.round(X).astype(np.float32)
+            Q = np.round(Q).astype(np.float32)
+        X[~X.any(axis=1), 0] = 1
+        Q[~Q.any(axis=1), 0] = 1
+        k = int(rng.choice([1, 7, 100, n + 3]))
+        xn, qn = core.norms(X), core.norms(Q)
+        np.testing.assert_array_equal(oracle.norms_f32(X), xn)
+        a = oracle.scan_topk_f32(X, Q, k, metric, xn, qn)
+        b = core.scan_topk(X, Q, k, metric, xn, qn)
+        np.testing.assert_array_equal(a[1], b[1])
+        np.testing.assert_array_equal(a[0], b[0])
