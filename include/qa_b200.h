@@ -19,6 +19,9 @@
  *                      (_core.pyx:340-347, 357-358)
  *   QA_EUNSUPPORTED -> NotImplementedError (shape outside this build's limits)
  *   QA_ECUDA/ENOMEM -> RuntimeError
+ *   QA_EIO          -> OSError; QA_ETRUNCATED / QA_ENONPOSITIVE / QA_EDIM ->
+ *                      TruncatedRecord / NonPositiveDim / DimensionMismatch
+ *                      with the reference's messages (dataset.py:160-209)
  *
  * Metric codes are the reference's (distances.py:22-27):
  *   0 = INNER_PRODUCT (score = -dot), 1 = L2_SQUARED, 2 = ANGULAR (1 - cos).
@@ -37,7 +40,11 @@ enum {
     QA_EINVAL = 1,
     QA_ECUDA = 2,
     QA_ENOMEM = 3,
-    QA_EUNSUPPORTED = 4
+    QA_EUNSUPPORTED = 4,
+    QA_EIO = 5,          /* OSError (open/read/write failed) */
+    QA_ETRUNCATED = 6,   /* TruncatedRecord (errors.py) */
+    QA_ENONPOSITIVE = 7, /* NonPositiveDim */
+    QA_EDIM = 8          /* DimensionMismatch */
 };
 
 /* Library identification. */
@@ -119,6 +126,24 @@ int qa_scan_topk_f32(const float *db, int64_t n, int64_t d, int64_t ldd,
                      double *out_scores, int32_t *out_ids, void *stream);
 /* out[i] = (float)sqrt(sequential float64 sum of x[i, j]^2). */
 int qa_norms_f32(const float *x, int64_t n, int64_t d, int64_t ldx, float *out, void *stream);
+
+/* ---- on-disk vector files (dataset.py:160-275) ----
+ * fvecs/ivecs (itemsize 4), i8vecs/bvecs (itemsize 1): records of an int32
+ * little-endian d followed by d items.  qa_vecs_probe validates the framing
+ * of the whole file exactly as the reference's _load_records/_walk_records
+ * (dataset.py:160-209) and returns n, d (0, 0 for an empty file).
+ * qa_vecs_read copies the payloads of records [row_lo, row_hi) -- e.g. one
+ * rank's row shard -- to dst with row stride ld_bytes: into HBM (dst_on_device,
+ * pinned double-buffered staging, header-stripping 2-D DMA on `stream`;
+ * returns after the copies complete) or into host memory.  recenter_u8 maps
+ * bvecs bytes v -> int8 v - 128 (load_bvecs, dataset.py:231-237).
+ * qa_vecs_write writes n host rows (stride ld_bytes) with d-headers
+ * (save_fvecs/save_ivecs/save_i8vecs, dataset.py:249-275). */
+int qa_vecs_probe(const char *path, int itemsize, int64_t *n, int64_t *d);
+int qa_vecs_read(const char *path, int itemsize, int64_t d, int64_t row_lo, int64_t row_hi,
+                 void *dst, int64_t ld_bytes, int dst_on_device, int recenter_u8, void *stream);
+int qa_vecs_write(const char *path, int itemsize, const void *src, int64_t n, int64_t d,
+                  int64_t ld_bytes);
 
 /* ---- index layout ----
  * perm = rows ordered by ascending squared norm (stable), and the gather

@@ -23,6 +23,10 @@ QA_EINVAL = 1
 QA_ECUDA = 2
 QA_ENOMEM = 3
 QA_EUNSUPPORTED = 4
+QA_EIO = 5
+QA_ETRUNCATED = 6
+QA_ENONPOSITIVE = 7
+QA_EDIM = 8
 
 c_i64 = ctypes.c_int64
 c_int = ctypes.c_int
@@ -72,6 +76,11 @@ SIGNATURES = {
          c_vp, c_vp, c_vp],
     ),
     "qa_norms_f32": (c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
+    "qa_vecs_probe": (c_int, [ctypes.c_char_p, c_int, ctypes.POINTER(c_i64),
+                              ctypes.POINTER(c_i64)]),
+    "qa_vecs_read": (c_int, [ctypes.c_char_p, c_int, c_i64, c_i64, c_i64, c_vp, c_i64, c_int,
+                             c_int, c_vp]),
+    "qa_vecs_write": (c_int, [ctypes.c_char_p, c_int, c_vp, c_i64, c_i64, c_i64]),
     "qa_merge_topk": (c_int, [c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "qa_debug_dots_i8": (c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_int, c_vp, c_vp]),
     "qa_last_scan_stats": (c_int, [ctypes.POINTER(ScanStats)]),
@@ -109,6 +118,14 @@ def check(rc: int) -> None:
         raise ValueError(msg)
     if rc == QA_EUNSUPPORTED:
         raise NotImplementedError(msg)
+    if rc in (QA_ETRUNCATED, QA_ENONPOSITIVE, QA_EDIM):
+        from . import errors
+        raise {QA_ETRUNCATED: errors.TruncatedRecord, QA_ENONPOSITIVE: errors.NonPositiveDim,
+               QA_EDIM: errors.DimensionMismatch}[rc](msg)
+    if rc == QA_EIO:
+        if "No such file" in msg:
+            raise FileNotFoundError(msg)
+        raise OSError(msg)
     raise QAError(msg)
 
 

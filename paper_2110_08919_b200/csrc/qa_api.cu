@@ -88,6 +88,15 @@ int set_err(int code, const char *fmt, ...) {
     return code;
 }
 
+}  // namespace
+
+int set_error_message(int code, const char *msg) {
+    g_err = msg;
+    return code;
+}
+
+namespace {
+
 int cuda_err(cudaError_t e, const char *what) {
     if (e == cudaErrorNotSupported)
         return set_err(QA_EUNSUPPORTED, "%s: shape not supported by this build", what);

@@ -151,6 +151,61 @@ def scan_f32_cases(core):
     return count
 
 
+def vecs_cases():
+    """Framing known answers for the vector-file loaders (dataset.py:160-275):
+    byte strings -> the reference loader's array or its error class/message
+    (the path in messages is written as {path})."""
+    import os
+    import struct
+    import tempfile
+
+    from quantann import dataset as rd
+
+    def rec(d, payload):
+        return struct.pack("<i", d) + payload
+
+    f4 = lambda vals: np.asarray(vals, "<f4").tobytes()
+    cases = {
+        "f_ok": ("fvecs", rec(3, f4([1, 2, 3])) + rec(3, f4([-0.0, np.inf, 1e-40]))),
+        "f_empty": ("fvecs", b""),
+        "f_short_header": ("fvecs", b"\x03\x00"),
+        "f_zero_d": ("fvecs", rec(0, b"")),
+        "f_neg_d": ("fvecs", rec(-2, f4([1, 2]))),
+        "f_mixed": ("fvecs", rec(2, f4([1, 2])) + rec(3, f4([1, 2, 3]))),
+        "f_mixed_whole": ("fvecs", rec(2, f4([1, 2])) + rec(2, f4([1, 2])) + rec(1, f4([5]))
+                          + struct.pack("<i", 2)),
+        "f_trunc_payload": ("fvecs", rec(2, f4([1, 2])) + rec(2, f4([1]))),
+        "f_trunc_header": ("fvecs", rec(2, f4([1, 2])) + b"\x02\x00"),
+        "f_later_neg": ("fvecs", rec(1, f4([1])) + rec(1, f4([2])) + rec(-1, f4([3]))),
+        "f_later_zero_walk": ("fvecs", rec(1, f4([1])) + rec(0, b"") + b"\x00"),
+        "i_ok": ("ivecs", rec(2, np.asarray([5, 7], "<i4").tobytes())
+                 + rec(2, np.asarray([0, 3], "<i4").tobytes())),
+        "i_dup": ("ivecs", rec(2, np.asarray([5, 5], "<i4").tobytes())),
+        "b8_ok": ("i8vecs", rec(4, bytes([0, 127, 128, 255])) + rec(4, bytes([1, 2, 3, 4]))),
+        "b8_trunc": ("i8vecs", rec(4, bytes([0, 1, 2, 3])) + rec(4, bytes([1, 2]))),
+        "bv_ok": ("bvecs", rec(3, bytes([0, 128, 255])) + rec(3, bytes([127, 129, 1]))),
+        "bv_mixed": ("bvecs", rec(3, bytes([0, 128, 255])) + rec(2, bytes([1, 2])) + b"\x00"),
+    }
+    loaders = {"fvecs": rd.load_fvecs, "ivecs": rd.load_ivecs, "i8vecs": rd.load_i8vecs,
+               "bvecs": rd.load_bvecs}
+    arrays = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, (kind, blob) in cases.items():
+            path = os.path.join(tmp, f"{name}.{kind}")
+            with open(path, "wb") as fh:
+                fh.write(blob)
+            arrays[f"{name}__kind"] = np.array(kind)
+            arrays[f"{name}__blob"] = np.frombuffer(blob, np.uint8)
+            try:
+                out = loaders[kind](path)
+                arrays[f"{name}__out"] = out.ids if kind == "ivecs" else out.data
+            except Exception as exc:  # noqa: BLE001 - record the reference's outcome
+                arrays[f"{name}__error"] = np.array(type(exc).__name__)
+                arrays[f"{name}__message"] = np.array(str(exc).replace(path, "{path}"))
+    np.savez_compressed(OUT / "vecs_cases.npz", **arrays)
+    return len(cases)
+
+
 def cfg_minis(qa, core):
     """BASELINE cfg0 (L2, min/max) and cfg1 (angular, symmetric) at reduced
     size through the reference pipeline: constructed stats -> fit(ABS_MAX)
@@ -196,10 +251,11 @@ def main():
     if len(sys.argv) > 1:   # regenerate only the named fixtures, e.g. scan_f32
         for name in sys.argv[1:]:
             fn = {"encode": lambda: encode_cases(qa), "scan": lambda: scan_cases(core),
-                  "scan_f32": lambda: scan_f32_cases(core), "cfg": lambda: cfg_minis(qa, core)}[name]
+                  "scan_f32": lambda: scan_f32_cases(core), "vecs": vecs_cases, "cfg": lambda: cfg_minis(qa, core)}[name]
             print(name, fn())
         return
     nf = scan_f32_cases(core)
+    vecs_cases()
     ne = encode_cases(qa)
     ns = scan_cases(core)
     cfg_minis(qa, core)
