@@ -73,6 +73,7 @@ constexpr int kBiasK = 32;       // K of the bias MMA (int8 columns)
 constexpr int kBiasA = 127;      // constant of the bias A tile
 constexpr int kSMin = -128 * kBiasK;  // digit-sum range
 constexpr int kSMax = 127 * kBiasK;
+constexpr int kMaxBiasReps = 8;  // bias MMAs per tile at most (|bias| <= 4.1M)
 // try_wait suspend-time hint for the epilogue warps' waits (ns)
 constexpr int kWaitHintNs = 20000;
 
@@ -272,6 +273,18 @@ __device__ __forceinline__ void mma_bias_commit_elect(uint32_t tmem_d, uint64_t 
         : "memory");
 }
 
+// an extra bias MMA (same constant A tile and digits; no commit)
+__device__ __forceinline__ void mma_bias_elect(uint32_t tmem_d, uint64_t ad, uint64_t bd,
+                                               uint32_t idesc) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 1;\n\t"
+        "}" ::"r"(tmem_d),
+        "l"(ad), "l"(bd), "r"(idesc)
+        : "memory");
+}
+
 __device__ __forceinline__ void tmem_wait() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -464,6 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *norm_full = stage_free + 2;
     uint32_t *tmem_base_s = (uint32_t *)(norm_full + 2);
     int32_t *stage_n_all = (int32_t *)(tmem_base_s + 1);  // [2]
+    int32_t *reps_s = stage_n_all + 2;  // [2] bias MMAs per tile of the unit
     constexpr int kEpiWarps = kEpiThreads / 32;
 
     if (threadIdx.x == 0) {
@@ -574,6 +588,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             WSTAT(3, mbar_wait_spin(bias_full + slot, ph));
             const uint64_t bdesc = bdesc0 + (uint64_t)(((uint32_t)bslot * b_bytes) >> 4);
             const uint64_t bbias_desc = bbias_desc0 + (uint64_t)((slot * N * kBiasK) >> 4);
+            const int reps = reps_s[slot];  // written before bias_full
             for (int ti = 0; ti < ntl; ++ti) {
                 if (!no_acc_wait) WSTAT(4, mbar_wait_spin(acc_empty + acc, accph ^ 1));
                 tc_fence_after();
@@ -601,7 +616,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (lane == 0 && !no_acc_wait) mbar_arrive(acc_full + acc);
                     __syncwarp();
                 } else {
-                    // + bias_q on every row: constant A (127) x per-query digits
+                    // + bias_q on every row: constant A (127) x per-query digits,
+                    // issued `reps` times (bounds beyond one MMA's range)
+                    if (!no_bias)
+                        for (int r = 1; r < reps; ++r)
+                            mma_bias_elect(tmem_d, abias_desc, bbias_desc, idesc);
                     mma_bias_commit_elect(tmem_d, abias_desc, bbias_desc, idesc, no_bias ? 0u : 1u,
                                           smem_u32(acc_full + acc));
                 }
@@ -693,18 +712,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             int32_t *bias_out = bias_s + slot * N;
             int32_t *thr_out = thr_all + slot * N;
             int32_t *digits_out = reinterpret_cast<int32_t *>(sBbias + slot * N * kBiasK);
+            // the bounds first: the unit's bias MMA count `reps` is the
+            // smallest that represents every representable bound (one MMA
+            // adds up to 127 * 127 * 32 = 516k; codes far from zero, e.g.
+            // SIFT-like data under min/max calibration, give dots of ~1e6)
+            long long Bq[kQPL];
+            int need = 1;
 #pragma unroll
             for (int i = 0; i < kQPL; ++i) {
                 const int q = i * 32 + lane;
-                int S = kSMin;  // padded columns: most negative bias
-                bool exc = false;
-                // thresholds for the exact test; padded columns never pass
-                thr_out[q] = (filtered && q < nqt)
-                                 ? Tq[i]
-                                 : ((M == kIP) ? INT32_MAX : (M == kL2 ? INT32_MIN : 0x7fc00000));
-                if (!filtered) {
-                    S = 0;  // dense / diagnostic passes: plain dots
-                } else if (q < nqt) {
+                Bq[i] = 0;
+                if (filtered && q < nqt) {
                     const int32_t T = Tq[i];
                     long long B;  // necessary condition dot >= B
                     if constexpr (M == kIP) {
@@ -719,9 +737,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                                          : (bf <= -4.0e9f ? (long long)-4000000000LL
                                                           : (long long)ceilf(bf));
                     }
-                    // smallest S with 127*S >= -B
-                    const long long nb = -B;
-                    long long s = nb >= 0 ? (nb + kBiasA - 1) / kBiasA : -((-nb) / kBiasA);
+                    Bq[i] = B;
+                    const long long mag = B >= 0 ? B : -B;
+                    const long long per = (long long)kBiasA * kSMax;  // 516k
+                    if (mag <= per * kMaxBiasReps) need = max(need, (int)((mag + per - 1) / per));
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) need = max(need, __shfl_xor_sync(0xffffffffu, need, o));
+            const int reps = filtered ? max(1, need) : 1;
+            const long long unit_a = (long long)kBiasA * reps;
+#pragma unroll
+            for (int i = 0; i < kQPL; ++i) {
+                const int q = i * 32 + lane;
+                int S = kSMin;  // padded columns: most negative bias
+                bool exc = false;
+                // thresholds for the exact test; padded columns never pass
+                thr_out[q] = (filtered && q < nqt)
+                                 ? Tq[i]
+                                 : ((M == kIP) ? INT32_MAX : (M == kL2 ? INT32_MIN : 0x7fc00000));
+                if (!filtered) {
+                    S = 0;  // dense / diagnostic passes: plain dots
+                } else if (q < nqt) {
+                    // smallest S with reps*127*S >= -B
+                    const long long nb = -Bq[i];
+                    long long s = nb >= 0 ? (nb + unit_a - 1) / unit_a : -((-nb) / unit_a);
                     if (s > kSMax) {
                         s = kSMax;
                         exc = true;
@@ -729,7 +769,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (s < kSMin) s = kSMin;
                     S = (int)s;
                 }
-                bias_out[q] = kBiasA * S;
+                bias_out[q] = (int32_t)(unit_a * S);
                 // spread S over 32 int8 digits: base + (j < rem)
                 const int base = (S >= 0) ? S / kBiasK : -((-S + kBiasK - 1) / kBiasK);
                 const int rem = S - base * kBiasK;  // 0 .. 31
@@ -758,6 +798,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         dst[i] = __float_as_int(__frcp_rn(__int_as_float(dst[i])));
                 }
             }
+            if (lane == 0) reps_s[slot] = reps;
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(bias_full + slot);

@@ -1,12 +1,12 @@
 // qa_layout.cu -- index layout: rows ordered by code norm.
 //
-// The filter epilogue derives one integer bound per (warp of 32 rows,
-// query) from the smallest / largest norm among those rows (qa_filter_tc.cu).
-// Storing the index rows in ascending-norm order makes every warp's norm
-// range narrow, so the bound is nearly the exact per-row test.  The order is
-// a stable radix sort on the int32 squared norm (CUB, part of the CUDA
-// toolkit); reported ids stay the caller's row positions through the
-// row_ids map passed to the scan.
+// The filter derives one integer bound per (work unit of <= 32 tiles,
+// query) from the smallest / largest norm among the unit's rows
+// (qa_filter_tc.cu).  Storing the index rows in norm-banded blocks makes
+// every unit's norm range narrow, so the bound is nearly the exact per-row
+// test.  The order starts from a stable radix sort on the int32 squared norm
+// (CUB, part of the CUDA toolkit); reported ids stay the caller's row
+// positions through the row_ids map passed to the scan.
 #include <cub/device/device_radix_sort.cuh>
 
 #include "qa_internal.h"
@@ -15,20 +15,72 @@ namespace qa {
 
 namespace {
 
-// Block interleave: stored block t <- sorted block (t * step + T/2) mod T
-// (step coprime to T; blocks of 32 tiles = 4096 rows), so every prefix of
-// stored rows samples the whole norm range -- the search rounds scan row
-// prefixes and need representative samples -- while each block (and every
-// filter work unit, which never crosses a block) holds rows of nearly equal
-// norm.  A partial last block stays last.
-__global__ void interleave_tiles_kernel(const int32_t *__restrict__ sorted, int64_t n,
-                                        int64_t tile, int64_t full_tiles, int64_t step,
-                                        int32_t *__restrict__ perm) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// Stored order (perm[i] = sorted row placed at stored row i):
+//
+//   [sample region]  kSampleTiles 128-row tiles taken at evenly spaced
+//                    positions of the norm-sorted order (tile k at sorted
+//                    tile floor(k * Tn / S)), themselves stored interleaved;
+//   [main region]    the remaining sorted rows cut into 4096-row blocks
+//                    (32 tiles, one narrow norm band each), block-interleaved:
+//                    stored block t <- block (t * step + T/2) mod T;
+//   [tail]           a partial last block, last.
+//
+// The search scans row prefixes and its threshold estimate treats the first
+// 32768 rows as a sample of the whole index: the sample region makes that
+// prefix STRATIFIED over every norm band (L2 neighbours concentrate in the
+// bands near the query's norm, so a prefix of a few whole bands misjudges
+// their density).  Main-region blocks start at multiples of 4096 rows, so
+// every filter work unit (<= 32 tiles, aligned) stays inside one band.
+// Indexes too small for the estimate (< 4 sample regions) skip the sample
+// region.
+constexpr int64_t kSampleTiles = 256;  // 32768 rows = the plan's estimate prefix
+
+__device__ __forceinline__ int64_t sampled_le(int64_t x, int64_t S, int64_t Tn) {
+    // number of k in [0, S) with floor(k * Tn / S) <= x
+    if (x < 0) return 0;
+    const int64_t c = ((x + 1) * S + Tn - 1) / Tn;
+    return c < S ? c : S;
+}
+
+__global__ void layout_kernel(const int32_t *__restrict__ sorted, int64_t n, int64_t Tn, int64_t S,
+                              int64_t sstep, int64_t T, int64_t step, int32_t *__restrict__ perm) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int64_t t = i / tile;
-    const int64_t src_t = t < full_tiles ? (t * step + full_tiles / 2) % full_tiles : t;
-    perm[i] = sorted[src_t * tile + (i - t * tile)];
+    if (i < S * 128) {
+        const int64_t slot = i >> 7;
+        const int64_t k = (slot * sstep + S / 2) % S;
+        perm[i] = sorted[(k * Tn / S) * 128 + (i & 127)];
+        return;
+    }
+    const int64_t j = i - S * 128;  // index in the rest (sorted order minus samples)
+    const int64_t bt = j / 4096;
+    const int64_t r = bt < T ? ((bt * step + T / 2) % T) * 4096 + (j % 4096) : j;
+    // rest tile rt -> sorted tile s: the rt-th tile not sampled
+    const int64_t rt = r >> 7;
+    int64_t m = sampled_le(rt, S, Tn);
+    for (;;) {
+        const int64_t m2 = sampled_le(rt + m, S, Tn);
+        if (m2 == m) break;
+        m = m2;
+    }
+    perm[i] = sorted[(rt + m) * 128 + (r & 127)];
+}
+
+int64_t coprime_step(int64_t full) {
+    // a step near T/phi, coprime to T: spreads consecutive stored blocks
+    // across the sorted order
+    if (full <= 1) return 1;
+    int64_t step = (int64_t)((double)full * 0.6180339887) | 1;
+    auto gcd = [](int64_t x, int64_t y) {
+        while (y) {
+            int64_t t = x % y;
+            x = y;
+            y = t;
+        }
+        return x;
+    };
+    while (gcd(step, full) != 1) step += 2;
+    return step;
 }
 
 __global__ void iota_kernel(int32_t *p, int64_t n) {
@@ -121,24 +173,11 @@ cudaError_t launch_order_by_key(const int32_t *key, int64_t n, int32_t *perm, vo
     e = cub::DeviceRadixSort::SortPairs((char *)scratch + off, temp, (const uint32_t *)key,
                                         keys_out, vals_in, sorted, (int)n, 0, 32, st);
     if (e != cudaSuccess) return e;
-    const int64_t tile = 128 * 32, full = n / tile;
-    int64_t step = 1;
-    if (full > 1) {
-        // a step near T/phi, coprime to T: spreads consecutive stored tiles
-        // across the sorted order
-        step = (int64_t)((double)full * 0.6180339887) | 1;
-        auto gcd = [](int64_t x, int64_t y) {
-            while (y) {
-                int64_t t = x % y;
-                x = y;
-                y = t;
-            }
-            return x;
-        };
-        while (gcd(step, full) != 1) step += 2;
-    }
-    interleave_tiles_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sorted, n, tile, full,
-                                                                         step, perm);
+    const int64_t Tn = n / 128;
+    const int64_t S = Tn >= 4 * kSampleTiles ? kSampleTiles : 0;
+    const int64_t T = (n - S * 128) / 4096;
+    layout_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sorted, n, Tn, S, coprime_step(S),
+                                                               T, coprime_step(T), perm);
     return cudaGetLastError();
 }
 
