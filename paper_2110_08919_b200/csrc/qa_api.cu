@@ -193,7 +193,9 @@ ScanPlan plan_scan(int64_t n, int64_t nq, int64_t keff, int64_t cap_min, bool al
     p.r0 = std::min(n, r0);
     // Row growth per round: every round adds ~k*(ratio-1) survivors per query;
     // small ratios cost more rounds (launches), large ones more survivors.
-    p.ratio = nq >= 256 ? 2 : 16;
+    // Small batches: few, wide rounds (each round costs a select launch;
+    // the filter is HBM-bound there, not survivor-bound).
+    p.ratio = nq >= 256 ? 2 : 32;
     if (const char *v = getenv("QA_B200_RATIO")) p.ratio = std::max(2, atoi(v));
     p.cap = std::max<int64_t>({2048, p.r0, 2 * keff * p.ratio, cap_min});
     // Threshold estimate.  In a prefix of P rows (the index interleaves its
@@ -205,7 +207,7 @@ ScanPlan plan_scan(int64_t n, int64_t nq, int64_t keff, int64_t cap_min, bool al
     // instead of ~k per doubling round.
     p.est_rows = 0;
     p.est_j = 0;
-    if (allow_estimate && p.ratio == 2) {
+    if (allow_estimate) {
         int64_t P = 32768;
         if (const char *v = getenv("QA_B200_EST_ROWS")) P = atoll(v);
         while (P < 64 * keff) P *= 2;
@@ -391,6 +393,9 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
                 r_hi = n;
             } else {
                 r_hi = std::min(n, round_up(r_hi * pl.ratio, 128));
+                // rounds stop at the estimate prefix (the index's stratified
+                // sample region, qa_layout.cu)
+                if (pl.est_rows > 0 && r_lo < pl.est_rows) r_hi = std::min(r_hi, pl.est_rows);
             }
         }
         if (estimated) {

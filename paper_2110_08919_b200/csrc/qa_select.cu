@@ -15,6 +15,7 @@
 // merged into T by merge path (each element's output rank = its own index +
 // a binary-search count in the other list).
 #include <cfloat>
+#include <cstdlib>
 
 #include "qa_common.cuh"
 #include "qa_internal.h"
@@ -335,90 +336,143 @@ __device__ __forceinline__ void rsort128(K (&x)[4]) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) rstage(x, size, stride);
 }
 
+// S (sorted ascending, 128) merged into T (sorted ascending, 128): T keeps
+// the 128 smallest of both, sorted.
+template <typename K>
+__device__ __forceinline__ void rmerge128(K (&t)[4], const K (&s)[4]) {
+    // reverse S (i -> 127 - i): lane -> 31 - lane, e -> 3 - e
+    K r[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) r[e] = rshfl(s[3 - e], 31);
+    // stride-128 step of the bitonic merge: T keeps the 128 smallest
+#pragma unroll
+    for (int e = 0; e < 4; ++e) t[e] = rsel(rlt(r[e], t[e]), r[e], t[e]);
+    // t is bitonic now: finish the merge with strides 64..1 (size 128,
+    // ascending everywhere)
+#pragma unroll
+    for (int stride = 64; stride > 0; stride >>= 1) rstage(t, 256, stride);
+}
+
+// wpq warps per query (1, 2, 4 or 8; a block = 8 warps): with few queries
+// the candidates of one query are split over wpq warps (each keeps its own
+// top-k -- only the query's first warp starts from the retained list), and
+// the group's lists are merged through shared memory at the end.  One warp
+// per query is latency-bound on its candidate stream when few warps are
+// resident.
 template <int M, typename K>
-__global__ void __launch_bounds__(256, QA_SEL_MINB) select_reg_kernel(SelectArgs a) {
+__global__ void __launch_bounds__(256, QA_SEL_MINB) select_reg_kernel(SelectArgs a, int wpq) {
     const int lane = threadIdx.x & 31;
-    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (q >= a.nq) return;
-    const int32_t total = a.ccount[q];
-    if (total == 0) return;
+    const int warp = threadIdx.x >> 5;
+    const int wq = warp % wpq;  // this warp's part of its query
+    const int64_t q = (int64_t)blockIdx.x * (8 / wpq) + warp / wpq;
+    __shared__ K stage_all[8][160];
+    K *stage = stage_all[warp];
+    const bool active = q < a.nq && a.ccount[q] > 0;
     const int k = (int)a.k;
-    const int m = (int)min((int64_t)total, a.cap);
-    if (total > a.cap && lane == 0) {
-        a.overflow[q] = 1;
-        atomicExch(a.any_overflow, 1);
-    }
-    const int32_t qq = (M == kL2) ? a.q_sqnorm[q] : 0;
-    const float qn = (M == kAngular) ? a.q_norm[q] : 1.0f;
-    Entry *st = a.state + q * a.k;
-    const Cand *cd = a.cand + q * a.cap;
-    int cur = a.state_cnt[q];
     K t[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        const int i = e * 32 + lane;
-        if (i < cur)
-            to_key<M>(st[i], t[e]);
-        else
-            rsentinel(t[e]);
-    }
-    // Candidates are scored 32 at a time; those below the current k-th key
-    // are compacted into this warp's smem stage, which is sorted and merged
-    // whenever it holds 128 (and once at the end).
-    __shared__ K stage_all[8][160];
-    K *stage = stage_all[threadIdx.x >> 5];
-    K kth = rget(t, k - 1);  // sentinel while fewer than k retained
-    int fill = 0;
-    int nvalid = 0;
-    for (int pos = 0; pos < m; pos += 32) {
-        const int i = pos + lane;
-        bool keep = false, valid = false;
-        K key;
-        if (i < m) {
-            const Cand c = cd[i];
+    for (int e = 0; e < 4; ++e) rsentinel(t[e]);
+    int cur = 0;
+    int32_t qq = 0;
+    float qn = 1.0f;
+    Entry *st = nullptr;
+    if (active) {
+        const int32_t total = a.ccount[q];
+        const int m = (int)min((int64_t)total, a.cap);
+        if (total > a.cap && lane == 0 && wq == 0) {
+            a.overflow[q] = 1;
+            atomicExch(a.any_overflow, 1);
+        }
+        qq = (M == kL2) ? a.q_sqnorm[q] : 0;
+        qn = (M == kAngular) ? a.q_norm[q] : 1.0f;
+        st = a.state + q * a.k;
+        const Cand *cd = a.cand + q * a.cap;
+        const int scur = a.state_cnt[q];
+        cur = wq == 0 ? scur : 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int i = e * 32 + lane;
+            if (i < cur)
+                to_key<M>(st[i], t[e]);
+            else
+                rsentinel(t[e]);
+        }
+        // every warp of the query filters against the retained k-th
+        K kth;
+        rsentinel(kth);
+        if (scur == k) {
+            Entry e = st[k - 1];
+            to_key<M>(e, kth);
+        }
+        // Candidates are scored 32 at a time (the next 32 are loaded while
+        // these are processed); those below the current k-th key are
+        // compacted into this warp's smem stage, which is sorted and merged
+        // whenever it holds 128 (and once at the end).
+        int fill = 0;
+        int nvalid = 0;
+        const int stride = 32 * wpq;
+        int pos = 32 * wq;
+        Cand cn = (pos + lane < m) ? cd[pos + lane] : Cand{-1, 0};
+        for (; pos < m; pos += stride) {
+            const Cand c = cn;
+            const int nx = pos + stride + lane;
+            cn = (nx < m) ? cd[nx] : Cand{-1, 0};
+            bool keep = false, valid = false;
+            K key;
             if (c.row >= 0) {  // row -1: slot of a masked-dense pass, filtered out
                 valid = true;
                 const Entry en = make_entry<M>(c, qq, qn, a.db_sqnorm, a.db_norm, a.row_ids);
                 to_key<M>(en, key);
                 keep = rlt(key, kth);
             }
+            nvalid += __popc(__ballot_sync(0xffffffffu, valid));
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) stage[fill + __popc(bal & ((1u << lane) - 1))] = key;
+            fill += __popc(bal);
+            const bool last = pos + stride >= m;
+            while (fill >= 128 || (last && fill > 0)) {
+                __syncwarp();
+                const int ns = min(fill, 128);
+                K s[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (e * 32 + lane < ns)
+                        s[e] = stage[e * 32 + lane];
+                    else
+                        rsentinel(s[e]);
+                }
+                __syncwarp();
+                if (fill > 128 && lane < fill - 128) stage[lane] = stage[128 + lane];
+                fill -= ns;
+                __syncwarp();
+                rsort128(s);
+                rmerge128(t, s);
+                cur = min(k, cur + ns);
+                const K kk = rget(t, k - 1);
+                kth = rsel(rlt(kk, kth), kk, kth);
+            }
         }
-        nvalid += __popc(__ballot_sync(0xffffffffu, valid));
-        const unsigned bal = __ballot_sync(0xffffffffu, keep);
-        if (keep) stage[fill + __popc(bal & ((1u << lane) - 1))] = key;
-        fill += __popc(bal);
-        const bool last = pos + 32 >= m;
-        while (fill >= 128 || (last && fill > 0)) {
+        if (lane == 0 && a.cand_count) atomicAdd(a.cand_count, (unsigned long long)nvalid);
+    }
+    if (wpq > 1) {
+        // merge the group's lists into its first warp
         __syncwarp();
-        const int ns = min(fill, 128);
-        K s[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            if (e * 32 + lane < ns)
-                s[e] = stage[e * 32 + lane];
-            else
-                rsentinel(s[e]);
-        }
-        __syncwarp();
-        if (fill > 128 && lane < fill - 128) stage[lane] = stage[128 + lane];
-        fill -= ns;
-        __syncwarp();
-        rsort128(s);
-        // reverse S (i -> 127 - i): lane -> 31 - lane, e -> 3 - e
-        K r[4];
+        for (int e = 0; e < 4; ++e) stage[e * 32 + lane] = t[e];
+        if (lane == 0) reinterpret_cast<int *>(stage + 128)[0] = cur;
+        __syncthreads();
+        if (active && wq == 0) {
+            for (int w = 1; w < wpq; ++w) {
+                const K *o = stage_all[warp + w];
+                K s[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) r[e] = rshfl(s[3 - e], 31);
-        // stride-128 step of the bitonic merge: T keeps the 128 smallest
-#pragma unroll
-        for (int e = 0; e < 4; ++e) t[e] = rsel(rlt(r[e], t[e]), r[e], t[e]);
-        // t is bitonic now: finish the merge with strides 64..1 (size 128,
-        // ascending everywhere)
-#pragma unroll
-        for (int stride = 64; stride > 0; stride >>= 1) rstage(t, 256, stride);
-        cur = min(k, cur + ns);
-        kth = rget(t, k - 1);
+                for (int e = 0; e < 4; ++e) s[e] = o[e * 32 + lane];
+                rmerge128(t, s);
+                cur = min(k, cur + reinterpret_cast<const int *>(o + 128)[0]);
+            }
         }
     }
+    if (!active || wq != 0) return;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
         const int i = e * 32 + lane;
@@ -429,10 +483,7 @@ __global__ void __launch_bounds__(256, QA_SEL_MINB) select_reg_kernel(SelectArgs
         const K v = rget(t, k - 1);
         if (lane == 0) a.thr[q] = threshold_of<M>(from_key(v), qq, qn);
     }
-    if (lane == 0) {
-        a.state_cnt[q] = cur;
-        if (a.cand_count) atomicAdd(a.cand_count, (unsigned long long)nvalid);
-    }
+    if (lane == 0) a.state_cnt[q] = cur;
 }
 
 __global__ void reset_kernel(int32_t *p, int64_t n, int32_t v) {
@@ -533,11 +584,17 @@ int pow2_at_least(int64_t v, int64_t cap) {
 template <int M>
 cudaError_t launch_select_t(const SelectArgs &a, cudaStream_t st) {
     if (a.k <= 128) {
-        const unsigned grid = (unsigned)((a.nq + 7) / 8);
+        // warps per query: enough warps in flight to cover ~5 blocks of 8
+        // per SM (the candidate stream is latency-bound per warp)
+        const int64_t slots = (int64_t)num_sms() * QA_SEL_MINB * 8;
+        int wpq = 1;
+        while (wpq < 8 && a.nq * wpq * 2 <= slots) wpq *= 2;
+        if (const char *v = getenv("QA_B200_SEL_WPQ")) wpq = atoi(v);  // diagnostics
+        const unsigned grid = (unsigned)((a.nq + (8 / wpq) - 1) / (8 / wpq));
         if constexpr (M == kAngular)
-            select_reg_kernel<M, RKey96><<<grid, 256, 0, st>>>(a);
+            select_reg_kernel<M, RKey96><<<grid, 256, 0, st>>>(a, wpq);
         else
-            select_reg_kernel<M, RKey64><<<grid, 256, 0, st>>>(a);
+            select_reg_kernel<M, RKey64><<<grid, 256, 0, st>>>(a, wpq);
         return cudaGetLastError();
     }
     const int kpad = (int)((a.k + 31) / 32 * 32);

@@ -392,3 +392,25 @@ def test_threshold_estimate_path_exact(oracle, monkeypatch, metric, force_j):
     np.testing.assert_array_equal(sc.cpu().numpy(), osc)
     if force_j:
         assert st["retries"] >= 1  # the recompute path ran
+
+
+# ------------------------------------------------ filter effectiveness --
+
+@pytest.mark.parametrize("metric", [0, 1])
+def test_filter_bounds_hold_on_large_dots(oracle, metric):
+    # SIFT-like codes under min/max calibration sit near -128, so dots are
+    # ~1e6 -- beyond one bias MMA's range (516k).  The filter must still
+    # reject most rows (a bound clamped to the bias range used to pass them
+    # all) and the L2 threshold estimate must hold (no recompute).
+    from paper_2110_08919_b200 import _lib
+    X, Q = synth.generate(2, n=300_000, nq=512)
+    index = qa.Int8Index.build(torch.from_numpy(X).cuda(), qa.Metric(metric), "minmax")
+    qc = index.encode_queries(torch.from_numpy(Q).cuda())
+    sc, ids = index.search_codes(qc, 100)
+    st = _lib.last_scan_stats()
+    assert st["retries"] == 0
+    assert st["candidates"] < 60 * 100 * 512, st
+    Xc = index.codes_in_input_order()
+    osc, oids = _scan_oracle(oracle, Xc, qc.to_host()[:16], 100, metric)
+    np.testing.assert_array_equal(ids[:16].cpu().numpy(), oids)
+    np.testing.assert_array_equal(sc[:16].cpu().numpy(), osc)

@@ -274,7 +274,11 @@ def run_cfg4(args):
                 lat = np.array(lat)
                 p50 = float(np.percentile(lat, 50))
                 byts = n * d + (4 * n if metric == qa.Metric.L2_SQUARED else 0) + B * d + B * k * 12
+                from paper_2110_08919_b200 import _lib
+                _lib.set_profiling(True)
                 sc, ids = index.search_codes(qc, k)
+                st = _lib.last_scan_stats()
+                _lib.set_profiling(False)
                 line = {
                     "config": c["name"], "n": n, "d": d, "metric": metric.short_name, "k": k,
                     "batch": B, "iters": args.iters,
@@ -286,6 +290,8 @@ def run_cfg4(args):
                                  "peak_gbs": hbm, "frac": byts / (p50 / 1e3) / 1e9 / hbm,
                                  "bytes_per_batch": byts, "peak_source": src},
                     "l2": "database (1.28 GB) > L2; not flushed",
+                    "scan_stats": {key: st[key] for key in ("rounds", "launches", "candidates",
+                                                            "filter_ms", "select_ms")},
                 }
                 if args.parity_rows:
                     line["parity_spot_check"] = parity_subset(index, qc, sc, ids, k, int(metric),
