@@ -73,7 +73,12 @@ constexpr int kBiasK = 32;       // K of the bias MMA (int8 columns)
 constexpr int kBiasA = 127;      // constant of the bias A tile
 constexpr int kSMin = -128 * kBiasK;  // digit-sum range
 constexpr int kSMax = 127 * kBiasK;
-constexpr int kMaxBiasReps = 8;  // bias MMAs per tile at most (|bias| <= 4.1M)
+constexpr int kMaxBiasReps = 8;
+// TMEM accumulators in flight: all 512 columns (N=256: 2, N=128: 4, N=64: 8).
+// With small query tiles the MMA of a tile is short, and two buffers left
+// the pipeline bound by the MMA -> epilogue -> MMA hand-off latency.
+template <int N>
+__host__ __device__ constexpr int nacc() { return 512 / N < 8 ? 512 / N : 8; }  // bias MMAs per tile at most (|bias| <= 4.1M)
 // try_wait suspend-time hint for the epilogue warps' waits (ns)
 constexpr int kWaitHintNs = 20000;
 
@@ -172,6 +177,14 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
         " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
         "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
+}
+
+// L2 prefetch of one database tile (no shared memory, no barrier)
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *map, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     (uint64_t)map),
+                 "r"(c0), "r"(c1)
+                 : "memory");
 }
 
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
@@ -408,6 +421,7 @@ struct Params {
     int stage_cap;          // survivor staging entries per slot
     int norm_bulk;          // norm arrays 16-byte aligned (bulk-copyable)
     int experiment;         // diagnostics only (QA_B200_EXPERIMENT); 0 in production
+    int l2_prefetch;        // database tiles prefetched into L2 ahead of the loads
 };
 
 // Work unit u -> (query tile t, row block b).  Query tiles vary fastest, so
@@ -432,6 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t u_first = blockIdx.x, u_step = gridDim.x;
+    constexpr int kNacc = nacc<N>();
 #ifdef QA_WAIT_STATS
     long long wst[kWst] = {};
     __shared__ unsigned long long wst_s[kWst];
@@ -469,8 +484,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *b_full = a_empty + p.stages;
     uint64_t *b_empty = b_full + 2;
     uint64_t *acc_full = b_empty + 2;
-    uint64_t *acc_empty = acc_full + 2;
-    uint64_t *bias_full = acc_empty + 2;
+    uint64_t *acc_empty = acc_full + kNacc;
+    uint64_t *bias_full = acc_empty + kNacc;
     uint64_t *bias_empty = bias_full + 2;
     uint64_t *stage_full = bias_empty + 2;
     uint64_t *stage_free = stage_full + 2;
@@ -488,14 +503,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < 2; ++s) {
             mbar_init(b_full + s, 1);
             mbar_init(b_empty + s, 1);
-            mbar_init(acc_full + s, 1);
-            mbar_init(acc_empty + s, kEpiWarps);
             mbar_init(bias_full + s, 1);
             mbar_init(bias_empty + s, 1 + kEpiWarps);  // MMA commit + epilogue warps
             mbar_init(stage_full + s, kEpiWarps);
             mbar_init(stage_free + s, 1);               // flush warp
             mbar_init(norm_full + s, 1);
             stage_n_all[s] = 0;
+        }
+        for (int s = 0; s < kNacc; ++s) {
+            mbar_init(acc_full + s, 1);
+            mbar_init(acc_empty + s, kEpiWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -506,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_base_s)),
-                     "n"(2 * N));
+                     "n"(kNacc * N));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     // constant bias A tile (every byte 127: any K-major layout reads the same)
@@ -525,6 +542,33 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t aph = 0;
             int it = 0;
+            // L2 prefetch cursor, p.l2_prefetch tiles ahead of the loads in
+            // this CTA's (unit, tile) sequence: the shared-memory ring alone
+            // holds too few bytes in flight to cover the HBM latency when the
+            // MMAs are short (small query batches: one query tile, every row
+            // read once)
+            int64_t pf_u = u_first, pf_tile = 0, pf_end = 0;
+            auto pf_unit = [&](int64_t uu) {
+                int64_t tt, bb;
+                unit_tb(p, uu, tt, bb);
+                pf_tile = bb * p.tiles_per_unit;
+                pf_end = min(p.n_tiles, pf_tile + p.tiles_per_unit);
+            };
+            auto pf_next = [&]() {
+                if (pf_u >= p.n_units) return;
+                if (pf_tile >= pf_end) {
+                    pf_u += u_step;
+                    if (pf_u >= p.n_units) return;
+                    pf_unit(pf_u);
+                }
+                for (int c = 0; c < p.kchunks; ++c)
+                    tma_prefetch_2d(&tm_db, c * SW, (int32_t)(a.r_lo + pf_tile * kBlockM));
+                ++pf_tile;
+            };
+            if (p.l2_prefetch > 0 && pf_u < p.n_units) {
+                pf_unit(pf_u);
+                for (int i = 0; i < p.l2_prefetch; ++i) pf_next();
+            }
             for (int64_t u = u_first; u < p.n_units; u += u_step, ++it) {
                 int64_t t, b;
                 unit_tb(p, u, t, b);
@@ -541,6 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int64_t tile0 = b * p.tiles_per_unit;
                 const int64_t tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
                 for (int64_t tile = tile0; tile < tile1; ++tile) {
+                    if (p.l2_prefetch > 0) pf_next();
                     // (experiment 10: always the same, L2-hot tile)
                     const int32_t row0 = (int32_t)(a.r_lo + (p.experiment == 10 ? 0 : tile) * kBlockM);
                     for (int c = 0; c < p.kchunks; ++c) {
@@ -624,7 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mma_bias_commit_elect(tmem_d, abias_desc, bbias_desc, idesc, no_bias ? 0u : 1u,
                                           smem_u32(acc_full + acc));
                 }
-                if (++acc == 2) {
+                if (++acc == kNacc) {
                     acc = 0;
                     accph ^= 1;
                 }
@@ -924,7 +969,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(acc_empty + acc);
-                    if (++acc == 2) {
+                    if (++acc == kNacc) {
                         acc = 0;
                         accph ^= 1;
                     }
@@ -1009,7 +1054,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(acc_empty + acc);
-                    if (++acc == 2) {
+                    if (++acc == kNacc) {
                         acc = 0;
                         accph ^= 1;
                     }
@@ -1083,7 +1128,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0 && acc_sync) mbar_arrive(acc_empty + acc);
-                    if (++acc == 2) {
+                    if (++acc == kNacc) {
                         acc = 0;
                         accph ^= 1;
                     }
@@ -1117,7 +1162,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 2) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                     "n"(2 * N));
+                     "n"(kNacc * N));
     }
 }
 
@@ -1156,7 +1201,7 @@ bool make_map(CUtensorMap *m, const int8_t *ptr, int64_t rows, int64_t cols, int
 // Diagnostics knobs, read once from the environment; production runs use
 // the defaults (QA_B200_EXPERIMENT=0: the real kernel).
 struct Knobs {
-    int experiment, stage_cap, max_stages, b_slots;
+    int experiment, stage_cap, max_stages, b_slots, l2_prefetch;
 };
 const Knobs &knobs() {
     static const Knobs k = [] {
@@ -1165,7 +1210,8 @@ const Knobs &knobs() {
             return (v && *v) ? atoi(v) : dflt;
         };
         return Knobs{env_int("QA_B200_EXPERIMENT", 0), env_int("QA_B200_STAGECAP", kStageCapDefault),
-                     env_int("QA_B200_MAXSTAGES", 12), env_int("QA_B200_BSLOTS", 2)};
+                     env_int("QA_B200_MAXSTAGES", 12), env_int("QA_B200_BSLOTS", 2),
+                     env_int("QA_B200_L2PF", 0)};  // measured: no gain (cfg4)
     }();
     return k;
 }
@@ -1191,6 +1237,9 @@ cudaError_t launch_t(const FilterArgs &a, cudaStream_t st) {
     p.n_units = ((p.n_tiles + tpu - 1) / tpu) * p.n_qtiles;
     const Knobs &kn = knobs();
     p.experiment = kn.experiment;
+    // one query tile: every database tile is read by one CTA once, so the
+    // stream is latency-bound on the shared-memory ring; prefetch ahead
+    p.l2_prefetch = p.n_qtiles == 1 ? kn.l2_prefetch : 0;
     p.stage_cap = kn.stage_cap;
     {
         const void *nrm = (M == kL2) ? (const void *)a.db_sqnorm : (const void *)a.db_norm;
@@ -1202,7 +1251,7 @@ cudaError_t launch_t(const FilterArgs &a, cudaStream_t st) {
                          kBlockM * kBiasK + 2 * (size_t)N * kBiasK +
                          2 * (size_t)p.stage_cap * sizeof(Staged) +
                          (M == kIP || !kExactInEpilogue ? 0 : 2 * (size_t)kUnitRowsMax * sizeof(int32_t)) +
-                         (7 * N + 2 * (N / 32)) * sizeof(int32_t) + 256;
+                         (7 * N + 2 * (N / 32)) * sizeof(int32_t) + 512;
     const size_t budget = 227 * 1024;
     const size_t stage_bytes = (size_t)kBlockM * SW;
     // each stage also costs two 8-byte mbarriers

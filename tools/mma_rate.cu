@@ -192,6 +192,18 @@ int main() {
     run<0, 128>("i8", sms, src, tiles);
     run<0, 128>("i8", sms);
     run<0, 64>("i8", sms);
+    run<0, 64, 1>("i8", sms);
+    run<0, 64, 2>("i8", sms);
+    run<0, 64>("i8", sms, src, tiles);
+    // streaming from HBM (1 GiB region, beyond L2) concurrently with the MMAs
+    int8_t *big;
+    const int btiles = 65536;
+    cudaMalloc(&big, (size_t)btiles * 16384);
+    cudaMemset(big, 1, (size_t)btiles * 16384);
+    printf("HBM stream:\n");
+    run<0, 64>("i8", sms, big, btiles);
+    run<0, 128>("i8", sms, big, btiles);
+    run<0, 256>("i8", sms, big, btiles);
     run<1, 256>("bf16", sms);
     run<1, 128>("bf16", sms);
     return 0;
