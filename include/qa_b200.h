@@ -64,6 +64,18 @@ int64_t qa_code_stride(int64_t d);
 int qa_minmax_f32(const float *x, int64_t n, int64_t d, int64_t ldx,
                   float *out_min, float *out_max, void *stream);
 
+/* The reference's full calibration statistics, estimate_stats
+ * (quantizer.py:176-222), bit-exact with its numpy evaluation: per-dimension
+ * mean and MLE sigma (sequential float64 sums over rows), min, max, the
+ * 0.1% / 99.9% order statistics (qlo/qhi, may be NULL) and the trimmed
+ * abs-max; pooled mean/sigma by numpy's pairwise summation over 64-column
+ * blocks.  x: DEVICE float32 [n, ldx]; every output a HOST array of d doubles
+ * (two scalars for pooled).  Synchronous.  n < 2 -> QA_EINVAL (TooFewSamples
+ * is raised one level up, quantizer.py:181-182). */
+int qa_estimate_stats_f32(const float *x, int64_t n, int64_t d, int64_t ldx, double *mu,
+                          double *sigma, double *mn, double *mx, double *tam, double *qlo,
+                          double *qhi, double *pooled_mu, double *pooled_sigma, void *stream);
+
 /* ---- encode (quantizer.py:291-300 _quantize_matrix; 303-320 callers) ----
  * codes[i, j] = Eq. 1 code of x[i, j] under per-dim window (k, sb, se) with
  * `bits` in [1, 8], bit-exact with numpy's float32 evaluation order.  codes

@@ -81,6 +81,7 @@ SIGNATURES = {
     "qa_vecs_read": (c_int, [ctypes.c_char_p, c_int, c_i64, c_i64, c_i64, c_vp, c_i64, c_int,
                              c_int, c_vp]),
     "qa_vecs_write": (c_int, [ctypes.c_char_p, c_int, c_vp, c_i64, c_i64, c_i64]),
+    "qa_estimate_stats_f32": (c_int, [c_vp, c_i64, c_i64, c_i64] + [c_vp] * 9 + [c_vp]),
     "qa_merge_topk": (c_int, [c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "qa_debug_dots_i8": (c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_int, c_vp, c_vp]),
     "qa_last_scan_stats": (c_int, [ctypes.POINTER(ScanStats)]),

@@ -718,6 +718,28 @@ int qa_scan_topk_f32(const float *db, int64_t n, int64_t d, int64_t ldd, const f
     return QA_OK;
 }
 
+int qa_estimate_stats_f32(const float *x, int64_t n, int64_t d, int64_t ldx, double *mu,
+                          double *sigma, double *mn, double *mx, double *tam, double *qlo,
+                          double *qhi, double *pooled_mu, double *pooled_sigma, void *stream) {
+    if (n < 2) return set_err(QA_EINVAL, "need at least 2 vectors, got %lld", (long long)n);
+    if (d < 1 || ldx < d) return set_err(QA_EINVAL, "bad shape");
+    if (!mu || !sigma || !mn || !mx || !tam || !pooled_mu || !pooled_sigma)
+        return set_err(QA_EINVAL, "null output");
+    std::vector<double> lo_buf, hi_buf;
+    if (!qlo) {
+        lo_buf.resize((size_t)d);
+        qlo = lo_buf.data();
+    }
+    if (!qhi) {
+        hi_buf.resize((size_t)d);
+        qhi = hi_buf.data();
+    }
+    QA_TRY(launch_estimate_stats(x, n, d, ldx, mu, sigma, mn, mx, tam, qlo, qhi, pooled_mu,
+                                 pooled_sigma, (cudaStream_t)stream),
+           "estimate_stats");
+    return QA_OK;
+}
+
 int qa_order_rows_by_norm(const int32_t *sqnorm, int64_t n, int32_t *perm, void *stream) {
     if (n < 0 || n > INT32_MAX) return set_err(QA_EINVAL, "bad shape");
     if (n == 0) return QA_OK;

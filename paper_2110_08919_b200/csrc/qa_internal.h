@@ -123,6 +123,13 @@ cudaError_t launch_norms_f32(const float *x, int64_t n, int64_t d, int64_t ldx, 
                              cudaStream_t st);
 size_t f32_select_smem(int64_t k);
 
+// estimate_stats (qa_stats.cu): x on the device, every output on the HOST;
+// synchronous on st.  qlo/qhi: the trimming quantiles per dimension.
+cudaError_t launch_estimate_stats(const float *x, int64_t n, int64_t d, int64_t ldx, double *mu,
+                                  double *sigma, double *mn, double *mx, double *tam,
+                                  double *qlo, double *qhi, double *pooled_mu,
+                                  double *pooled_sigma, cudaStream_t st);
+
 // Largest list the select kernel sorts in shared memory at once.
 constexpr int64_t kSortMax = 8192;
 // Largest k served (k + one candidate chunk must fit kSortMax).

@@ -3,7 +3,9 @@
 //
 // What numpy computes (verified against numpy 2.3 in tests/golden):
 //   mu[j]    = (sequential float64 sum over rows of x[i, j]) / n
-//              (an axis-0 reduction of a C-contiguous block adds row by row)
+//              (an axis-0 reduction of a C-contiguous block adds row by row;
+//              a block one column wide is contiguous along the reduction and
+//              numpy sums it pairwise instead -- d % 64 == 1)
 //   sigma[j] = sqrt((sequential sum of round(c*c), c = x - mu[j]) / n)
 //   min/max  = order-free (NaN propagates)
 //   qlo/qhi  = exact order statistics: sorted column at floor((n-1)*0.001)
@@ -309,6 +311,34 @@ double pw_combine(int64_t m, const double *vals, size_t &idx) {
     return a + b;
 }
 
+// numpy pairwise sum of the m flattened elements of v (synchronous)
+cudaError_t pairwise_sum(const BlockView &v, int64_t m, cudaStream_t st, double *out) {
+    std::vector<int64_t> offs, lens;
+    pw_split(0, m, offs, lens);
+    const int64_t nodes = (int64_t)offs.size();
+    int64_t *doff = nullptr, *dlen = nullptr;
+    double *dnodes = nullptr;
+    std::vector<double> vals((size_t)nodes);
+    cudaError_t e;
+    if ((e = cudaMalloc(&doff, nodes * 8)) == cudaSuccess &&
+        (e = cudaMalloc(&dlen, nodes * 8)) == cudaSuccess &&
+        (e = cudaMalloc(&dnodes, nodes * 8)) == cudaSuccess &&
+        (e = cudaMemcpyAsync(doff, offs.data(), nodes * 8, cudaMemcpyHostToDevice, st)) == cudaSuccess &&
+        (e = cudaMemcpyAsync(dlen, lens.data(), nodes * 8, cudaMemcpyHostToDevice, st)) == cudaSuccess) {
+        pw_nodes_kernel<<<(unsigned)((nodes + 127) / 128), 128, 0, st>>>(v, doff, dlen, nodes, dnodes);
+        if ((e = cudaGetLastError()) == cudaSuccess &&
+            (e = cudaMemcpyAsync(vals.data(), dnodes, nodes * 8, cudaMemcpyDeviceToHost, st)) == cudaSuccess &&
+            (e = cudaStreamSynchronize(st)) == cudaSuccess) {
+            size_t idx = 0;
+            *out = pw_combine(m, vals.data(), idx);
+        }
+    }
+    cudaFree(doff);
+    cudaFree(dlen);
+    cudaFree(dnodes);
+    return e;
+}
+
 }  // namespace
 
 // Full estimate_stats.  x: device float32 [n, ldx]; outputs: HOST arrays of
@@ -323,14 +353,12 @@ cudaError_t launch_estimate_stats(const float *x, int64_t n, int64_t d, int64_t 
     unsigned long long *dtam = nullptr;
     SelState *dsel = nullptr;
     unsigned int *dhist = nullptr;
-    double *dnodes = nullptr;
-    int64_t *doff = nullptr, *dlen = nullptr;
     std::vector<SelState> hsel((size_t)d);
     std::vector<int> hnan((size_t)d), hkept((size_t)d);
     std::vector<unsigned long long> htam((size_t)d);
     const int64_t klo = (int64_t)std::floor((double)(n - 1) * 0.001);
     const int64_t khi = (int64_t)std::ceil((double)(n - 1) * 0.999);
-    double flat_sum = 0.0, pooled_var = 0.0;
+    double flat_sum = 0.0, pooled_var = 0.0, last_mu = 0.0, last_sigma = 0.0;
 #define QA_CK(x)                         \
     do {                                 \
         if ((e = (x)) != cudaSuccess) goto done; \
@@ -347,8 +375,23 @@ cudaError_t launch_estimate_stats(const float *x, int64_t n, int64_t d, int64_t 
     {
         const unsigned g = (unsigned)((d + kColBlock - 1) / kColBlock);
         colsum_kernel<<<g, kColBlock, 0, st>>>(x, n, d, ldx, dmu, dmn, dmx, dnan);
+        QA_CK(cudaGetLastError());
+        if (d % kStatsChunk == 1) {
+            // the last 64-column block is one column wide: numpy's axis-0
+            // reduction of an [n, 1] block runs along contiguous memory and
+            // uses pairwise summation instead of the row-by-row order
+            double s1 = 0.0;
+            QA_CK(pairwise_sum(BlockView{x, ldx, d - 1, 1, 0.0, 0}, n, st, &s1));
+            last_mu = s1 / (double)n;
+            QA_CK(cudaMemcpyAsync(dmu + d - 1, &last_mu, 8, cudaMemcpyHostToDevice, st));
+        }
         colvar_kernel<<<g, kColBlock, 0, st>>>(x, n, d, ldx, dmu, dsig);
         QA_CK(cudaGetLastError());
+        if (d % kStatsChunk == 1) {
+            double s2 = 0.0;
+            QA_CK(pairwise_sum(BlockView{x, ldx, d - 1, 1, last_mu, 1}, n, st, &s2));
+            last_sigma = std::sqrt(s2 / (double)n);
+        }
     }
     // order statistics, one 64-column chunk at a time (64 KiB of histograms)
     for (int64_t j = 0; j < d; ++j) hsel[j] = SelState{{0u, 0u}, {klo, khi}};
@@ -386,6 +429,7 @@ cudaError_t launch_estimate_stats(const float *x, int64_t n, int64_t d, int64_t 
     QA_CK(cudaMemcpyAsync(hkept.data(), dkept, d * 4, cudaMemcpyDeviceToHost, st));
     QA_CK(cudaMemcpyAsync(htam.data(), dtam, d * 8, cudaMemcpyDeviceToHost, st));
     QA_CK(cudaStreamSynchronize(st));
+    if (d % kStatsChunk == 1) sigma[d - 1] = last_sigma;
     for (int64_t j = 0; j < d; ++j) {
         auto kf = [](uint32_t k) {
             const uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
@@ -406,32 +450,12 @@ cudaError_t launch_estimate_stats(const float *x, int64_t n, int64_t d, int64_t 
         const double shift = pass == 0 ? 0.0 : flat_sum / (double)(n * d);
         for (int64_t c0 = 0; c0 < d; c0 += kStatsChunk) {
             const int64_t c = std::min<int64_t>(kStatsChunk, d - c0);
-            std::vector<int64_t> offs, lens;
-            pw_split(0, n * c, offs, lens);
-            const int64_t nodes = (int64_t)offs.size();
-            cudaFree(doff);
-            cudaFree(dlen);
-            cudaFree(dnodes);
-            doff = dlen = nullptr;
-            dnodes = nullptr;
-            QA_CK(cudaMalloc(&doff, nodes * 8));
-            QA_CK(cudaMalloc(&dlen, nodes * 8));
-            QA_CK(cudaMalloc(&dnodes, nodes * 8));
-            QA_CK(cudaMemcpyAsync(doff, offs.data(), nodes * 8, cudaMemcpyHostToDevice, st));
-            QA_CK(cudaMemcpyAsync(dlen, lens.data(), nodes * 8, cudaMemcpyHostToDevice, st));
-            BlockView v{x, ldx, c0, c, shift, pass};
-            pw_nodes_kernel<<<(unsigned)((nodes + 127) / 128), 128, 0, st>>>(v, doff, dlen, nodes,
-                                                                             dnodes);
-            QA_CK(cudaGetLastError());
-            std::vector<double> vals((size_t)nodes);
-            QA_CK(cudaMemcpyAsync(vals.data(), dnodes, nodes * 8, cudaMemcpyDeviceToHost, st));
-            QA_CK(cudaStreamSynchronize(st));
-            size_t idx = 0;
-            const double s = pw_combine(n * c, vals.data(), idx);
+            double sblk = 0.0;
+            QA_CK(pairwise_sum(BlockView{x, ldx, c0, c, shift, pass}, n * c, st, &sblk));
             if (pass == 0)
-                flat_sum += s;
+                flat_sum += sblk;
             else
-                pooled_var += s;
+                pooled_var += sblk;
         }
     }
     *pooled_mu = flat_sum / (double)(n * d);
@@ -448,9 +472,6 @@ done:
     cudaFree(dtam);
     cudaFree(dsel);
     cudaFree(dhist);
-    cudaFree(doff);
-    cudaFree(dlen);
-    cudaFree(dnodes);
     return e;
 }
 

@@ -12,9 +12,10 @@ reductions and the Eq. 1 encode -- run on the GPU (libqa_b200):
 * ``quantize_dataset`` / ``quantize_query`` encode through the fused encode
   kernel, bit-exact with numpy's float32 evaluation order.
 
-Out of scope this round: the reference's
-``estimate_stats`` mean/sigma/quantile-trimmed statistics, whose float64
-summation order would have to be reproduced on the GPU.
+* ``estimate_stats`` the reference's full statistics (mean, sigma, trimmed
+  abs-max, pooled) for its own SIGMA_CLAMP / ABS_MAX / UNIFORM_SIGMA_CLAMP
+  modes, reproducing numpy's float64 summation orders on the GPU
+  (csrc/qa_stats.cu).
 """
 
 from __future__ import annotations
@@ -196,6 +197,46 @@ def minmax_stats(data) -> RangeStats:
         raise TooFewSamples(f"need at least 2 vectors, got {n}")
     mn, mx = dev.minmax(t)
     return RangeStats(min=mn.double().cpu().numpy(), max=mx.double().cpu().numpy(), count=n)
+
+
+def estimate_stats(data) -> DimensionStats:
+    """The reference's calibration statistics (quantizer.py:176-222), on the
+    GPU and bit-exact with its numpy evaluation (csrc/qa_stats.cu): per-dim
+    mean, MLE sigma, min, max, 0.1%/99.9%-trimmed abs-max, pooled mean and
+    sigma.  ``data``: float32 DenseDataset, numpy [n, d] array or CUDA tensor."""
+    import ctypes
+
+    import torch
+
+    from . import device as dev
+    from ._lib import check, lib
+
+    if isinstance(data, DenseDataset):
+        if data.elem is not ElemKind.FLOAT32:
+            raise ElementKindMismatch("statistics are estimated on Float32 corpora")
+        data = data.data
+    if isinstance(data, np.ndarray):
+        if data.dtype != np.float32 or data.ndim != 2:
+            raise ElementKindMismatch("statistics are estimated on Float32 corpora")
+        t = torch.from_numpy(np.array(data, copy=True)).to(dev.default_device())
+    else:
+        t = data
+    if t.dtype != torch.float32 or t.dim() != 2:
+        raise ElementKindMismatch("statistics are estimated on Float32 corpora")
+    n, d = t.shape
+    if n < 2:
+        raise TooFewSamples(f"need at least 2 vectors, got {n}")
+    t = t if t.stride(1) == 1 else t.contiguous()
+    out = {k: np.empty(d, dtype=np.float64) for k in ("mu", "sigma", "min", "max", "tam")}
+    pm, ps = ctypes.c_double(0.0), ctypes.c_double(0.0)
+    check(lib.qa_estimate_stats_f32(t.data_ptr(), n, d, t.stride(0), out["mu"].ctypes.data,
+                                    out["sigma"].ctypes.data, out["min"].ctypes.data,
+                                    out["max"].ctypes.data, out["tam"].ctypes.data, None, None,
+                                    ctypes.addressof(pm), ctypes.addressof(ps),
+                                    torch.cuda.current_stream(t.device).cuda_stream))
+    return DimensionStats(mu=out["mu"], sigma=out["sigma"], min=out["min"], max=out["max"],
+                          trimmed_absmax=out["tam"], pooled_mu=float(pm.value),
+                          pooled_sigma=float(ps.value), count=int(n))
 
 
 def _range_fit(center: np.ndarray, half: np.ndarray, count: int, bits: int) -> FitResult:

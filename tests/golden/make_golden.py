@@ -206,6 +206,63 @@ def vecs_cases():
     return len(cases)
 
 
+def stats_inputs():
+    """Seeded inputs of the estimate_stats known answers (regenerated by the
+    tests from the same seeds; only the reference's outputs are stored)."""
+    def gen(seed, n, d, kind):
+        rng = np.random.default_rng(seed)
+        if kind == "normal":
+            x = rng.normal(size=(n, d)) * rng.uniform(0.01, 50, size=d) + rng.normal(0, 5, size=d)
+        elif kind == "ints":   # heavy ties: order statistics on repeated values
+            x = rng.integers(-3, 4, size=(n, d)).astype(np.float64)
+        elif kind == "sift":
+            x = np.clip(np.round(np.abs(rng.normal(0, 40, size=(n, d)))), 0, 255)
+            x[rng.random((n, d)) < 0.1] = 0
+        elif kind == "const":  # zero-width dimensions
+            x = rng.normal(size=(n, d))
+            x[:, ::3] = 1.25
+        elif kind == "nan":
+            x = rng.normal(size=(n, d))
+            x[rng.integers(0, n), 0] = np.nan
+        elif kind == "tiny":   # denormals and signed zeros
+            x = rng.normal(size=(n, d)) * 1e-39
+            x[::5] = -0.0
+        else:
+            raise ValueError(kind)
+        return x.astype(np.float32)
+
+    specs = [("s_normal_small", 1, 2, 1, "normal"), ("s_normal_7", 2, 7, 3, "normal"),
+             ("s_normal_9", 3, 9, 5, "normal"), ("s_normal_129", 4, 129, 70, "normal"),
+             ("s_normal_5000", 5, 5000, 70, "normal"), ("s_ints", 6, 3001, 65, "ints"),
+             ("s_sift_100k", 7, 100_000, 128, "sift"), ("s_const", 8, 1000, 10, "const"),
+             ("s_nan", 9, 500, 4, "nan"), ("s_tiny", 10, 777, 33, "tiny"),
+             ("s_wide", 11, 300, 200, "normal"), ("s_glove", 12, 50_000, 100, "normal")]
+    return [(name, gen(seed, n, d, kind)) for name, seed, n, d, kind in specs], specs
+
+
+def stats_cases():
+    from quantann import DenseDataset
+    from quantann.quantizer import QuantMode, estimate_stats, fit
+
+    arrays = {}
+    cases, specs = stats_inputs()
+    for (name, x), spec in zip(cases, specs):
+        st = estimate_stats(DenseDataset(x))
+        arrays[f"{name}__spec"] = np.array(spec[1:4], dtype=np.int64)
+        arrays[f"{name}__kind"] = np.array(spec[4])
+        for f in ("mu", "sigma", "min", "max", "trimmed_absmax"):
+            arrays[f"{name}__{f}"] = getattr(st, f)
+        arrays[f"{name}__pooled"] = np.array([st.pooled_mu, st.pooled_sigma])
+        for mode in (QuantMode.SIGMA_CLAMP, QuantMode.ABS_MAX, QuantMode.UNIFORM_SIGMA_CLAMP):
+            try:
+                p = fit(st, 8, mode).params
+                arrays[f"{name}__fit{int(mode)}"] = np.stack([p.k, p.sb, p.se])
+            except Exception:  # noqa: BLE001 - e.g. NaN windows are rejected
+                pass
+    np.savez_compressed(OUT / "stats_cases.npz", **arrays)
+    return len(cases)
+
+
 def cfg_minis(qa, core):
     """BASELINE cfg0 (L2, min/max) and cfg1 (angular, symmetric) at reduced
     size through the reference pipeline: constructed stats -> fit(ABS_MAX)
@@ -251,11 +308,12 @@ def main():
     if len(sys.argv) > 1:   # regenerate only the named fixtures, e.g. scan_f32
         for name in sys.argv[1:]:
             fn = {"encode": lambda: encode_cases(qa), "scan": lambda: scan_cases(core),
-                  "scan_f32": lambda: scan_f32_cases(core), "vecs": vecs_cases, "cfg": lambda: cfg_minis(qa, core)}[name]
+                  "scan_f32": lambda: scan_f32_cases(core), "vecs": vecs_cases, "stats": stats_cases, "cfg": lambda: cfg_minis(qa, core)}[name]
             print(name, fn())
         return
     nf = scan_f32_cases(core)
     vecs_cases()
+    stats_cases()
     ne = encode_cases(qa)
     ns = scan_cases(core)
     cfg_minis(qa, core)
