@@ -158,10 +158,15 @@ int qa_vecs_write(const char *path, int itemsize, const void *src, int64_t n, in
                   int64_t ld_bytes);
 
 /* ---- index layout ----
- * perm = rows ordered by ascending squared norm (stable), and the gather
- * that applies it to codes + norms (norm/norm_out may be NULL).  An index
- * stored in this order gives the filter pass tight per-warp bounds. */
-int qa_order_rows_by_norm(const int32_t *sqnorm, int64_t n, int32_t *perm, void *stream);
+ * perm = the stored row order of an index (qa_layout.cu): rows stably sorted
+ * by squared norm, cut into 4096-row norm bands stored interleaved (tight
+ * per-unit filter bounds, every prefix spread over the bands); with
+ * `stratify` the first 32768 stored rows are a stratified sample of all bands
+ * (the search's threshold estimate treats that prefix as a sample; used for
+ * L2).  qa_permute_rows_i8 applies it to codes + norms (norm/norm_out may be
+ * NULL). */
+int qa_order_rows_by_norm(const int32_t *sqnorm, int64_t n, int stratify, int32_t *perm,
+                          void *stream);
 int qa_permute_rows_i8(const int8_t *codes, const int32_t *sqnorm, const float *norm,
                        int64_t n, int64_t ldc, const int32_t *perm, int8_t *codes_out,
                        int32_t *sqnorm_out, float *norm_out, void *stream);

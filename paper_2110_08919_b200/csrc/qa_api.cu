@@ -167,6 +167,9 @@ struct ScanPlan {
     // rows are scanned in ONE pass with the est_j-th best prefix score as the
     // bound (0 = off)
     int64_t est_rows, est_j;
+    // two-level estimate: after round 0 the prefix [r0, est_rows) is also
+    // scanned in one pass, bounded by the est1_j-th best of round 0 (0 = off)
+    int64_t est1_j;
 };
 
 // Smallest j with P(Poisson(lambda) >= j) <= tail.
@@ -207,6 +210,7 @@ ScanPlan plan_scan(int64_t n, int64_t nq, int64_t keff, int64_t cap_min, bool al
     // instead of ~k per doubling round.
     p.est_rows = 0;
     p.est_j = 0;
+    p.est1_j = 0;
     if (allow_estimate) {
         int64_t P = 32768;
         if (const char *v = getenv("QA_B200_EST_ROWS")) P = atoll(v);
@@ -222,6 +226,21 @@ ScanPlan plan_scan(int64_t n, int64_t nq, int64_t keff, int64_t cap_min, bool al
                 p.est_rows = P;
                 p.est_j = j;
                 p.cap = std::max<int64_t>(p.cap, 4 * j * (n / P));
+                // the same estimate one level down: round 0's j1-th best
+                // bounds the rest of the prefix (replaces the doubling rounds)
+                static const bool two_level = [] {
+                    const char *v = getenv("QA_B200_EST2");
+                    return !(v && strcmp(v, "0") == 0);
+                }();
+                if (two_level && p.r0 < P) {
+                    const double l1 = (double)keff * (double)p.r0 / (double)P;
+                    int64_t j1 = std::max<int64_t>(8, poisson_quantile(l1, tail));
+                    if (const char *v = getenv("QA_B200_EST1_J")) j1 = std::max<int64_t>(1, atoll(v));
+                    if (j1 < keff) {
+                        p.est1_j = j1;
+                        p.cap = std::max<int64_t>(p.cap, 4 * j1 * (P / p.r0));
+                    }
+                }
             }
         }
     }
@@ -303,6 +322,7 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
         g_stats.launches += 1;
         int64_t r_lo = 0, r_hi = pl.r0;
         bool first = true, estimated = false;
+        int64_t cur_j = 0;  // estimate rank of the pass in flight (0: k-th bound)
         for (;;) {
             FilterArgs fa;
             fa.db = db;
@@ -336,7 +356,7 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             fa.ld_dots = 0;
             // ~k new candidates per doubling of the rows seen; the estimated
             // final pass admits ~est_j per prefix-sized slice
-            fa.exp_cands = estimated ? (double)pl.est_j * (double)(r_hi - r_lo) / (double)r_lo
+            fa.exp_cands = cur_j ? (double)cur_j * (double)(r_hi - r_lo) / (double)r_lo
                                      : (double)keff * (double)(r_hi - r_lo) / (double)std::max<int64_t>(r_lo, 1);
             QA_TRY(launch_fill(ccount, m, mode != 0 ? (int32_t)(r_hi - r_lo) : 0, st), "fill");
             cudaError_t e = cudaErrorNotSupported;
@@ -380,13 +400,28 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
                 trace_prev = cnt;
             }
             if (r_hi >= n) break;
-            first = false;
             r_lo = r_hi;
+            if (pl.est1_j > 0 && first && r_hi < pl.est_rows) {
+                // one pass over the rest of the prefix with round 0's
+                // est1_j-th best as the bound
+                QA_TRY(launch_estimate(state, state_cnt, thr, est, m, keff, pl.est1_j, metric,
+                                       q_sqnorm ? q_sqnorm + c0 : nullptr,
+                                       q_norm ? q_norm + c0 : nullptr, false, st),
+                       "estimate");
+                g_stats.launches += 1;
+                estimated = true;
+                cur_j = pl.est1_j;
+                first = false;
+                r_hi = pl.est_rows;
+                continue;
+            }
+            first = false;
             if (pl.est_rows > 0 && r_hi >= pl.est_rows) {
                 // one pass over the rest with the estimated bound
+                cur_j = pl.est_j;
                 QA_TRY(launch_estimate(state, state_cnt, thr, est, m, keff, pl.est_j, metric,
                                        q_sqnorm ? q_sqnorm + c0 : nullptr,
-                                       q_norm ? q_norm + c0 : nullptr, st),
+                                       q_norm ? q_norm + c0 : nullptr, estimated, st),
                        "estimate");
                 g_stats.launches += 1;
                 estimated = true;
@@ -740,16 +775,18 @@ int qa_estimate_stats_f32(const float *x, int64_t n, int64_t d, int64_t ldx, dou
     return QA_OK;
 }
 
-int qa_order_rows_by_norm(const int32_t *sqnorm, int64_t n, int32_t *perm, void *stream) {
+int qa_order_rows_by_norm(const int32_t *sqnorm, int64_t n, int stratify, int32_t *perm,
+                          void *stream) {
     if (n < 0 || n > INT32_MAX) return set_err(QA_EINVAL, "bad shape");
     if (n == 0) return QA_OK;
     cudaStream_t st = (cudaStream_t)stream;
     Workspace &ws = g_ws[current_device() % kMaxDevices];
     std::lock_guard<std::mutex> lock(ws.mu);
     size_t need = 0;
-    QA_TRY(launch_order_by_key(sqnorm, n, perm, nullptr, 0, &need, st), "order");
+    QA_TRY(launch_order_by_key(sqnorm, n, stratify != 0, perm, nullptr, 0, &need, st), "order");
     QA_TRY(ws.scratch.reserve(need), "workspace");
-    QA_TRY(launch_order_by_key(sqnorm, n, perm, ws.scratch.ptr, ws.scratch.bytes, &need, st),
+    QA_TRY(launch_order_by_key(sqnorm, n, stratify != 0, perm, ws.scratch.ptr, ws.scratch.bytes,
+                              &need, st),
            "order");
     return QA_OK;
 }

@@ -84,10 +84,12 @@ cudaError_t launch_select(const SelectArgs &a, cudaStream_t st);
 cudaError_t launch_init_state(int32_t *state_cnt, int32_t *thr, int64_t nq, int metric,
                               cudaStream_t st);
 cudaError_t launch_fill(int32_t *p, int64_t n, int32_t v, cudaStream_t st);
-// thr[q] := threshold of the j-th kept entry (est[q] = its order key)
+// thr[q] := threshold of the j-th kept entry; est[q] := its order key, or with
+// `combine` the tighter of that and the previous est[q] (two-level estimate)
 cudaError_t launch_estimate(const Entry *state, const int32_t *state_cnt, int32_t *thr,
                             unsigned long long *est, int64_t nq, int64_t k, int64_t j, int metric,
-                            const int32_t *q_sqnorm, const float *q_norm, cudaStream_t st);
+                            const int32_t *q_sqnorm, const float *q_norm, bool combine,
+                            cudaStream_t st);
 // redo[q] := 1 where the k-th kept entry is worse than est[q]
 cudaError_t launch_check_estimate(const Entry *state, const int32_t *state_cnt,
                                   const unsigned long long *est, int64_t nq, int64_t k,
@@ -100,7 +102,8 @@ cudaError_t launch_finalize(const Entry *state, int64_t nq, int64_t k, int64_t k
 cudaError_t launch_group_ranges(int metric, const int32_t *sqnorm, const float *norm, int64_t n,
                                 int32_t *lo, int32_t *hi, int64_t groups, cudaStream_t st);
 // stable ascending order of rows by int32 key (CUB radix sort); perm[i] = row
-cudaError_t launch_order_by_key(const int32_t *key, int64_t n, int32_t *perm, void *scratch,
+cudaError_t launch_order_by_key(const int32_t *key, int64_t n, bool stratify, int32_t *perm,
+                                void *scratch,
                                 size_t scratch_bytes, size_t *needed, cudaStream_t st);
 cudaError_t launch_permute_rows(const int8_t *src, const int32_t *sq_in, const float *n_in,
                                 int64_t n, int64_t ld, const int32_t *perm, int8_t *dst,

@@ -32,7 +32,9 @@ namespace {
 // their density).  Main-region blocks start at multiples of 4096 rows, so
 // every filter work unit (<= 32 tiles, aligned) stays inside one band.
 // Indexes too small for the estimate (< 4 sample regions) skip the sample
-// region.
+// region, and so do angular indexes (the caller's choice): their code norms
+// span a narrow range, the estimate holds without stratification, and the
+// prefix passes keep tight per-unit bounds.
 constexpr int64_t kSampleTiles = 256;  // 32768 rows = the plan's estimate prefix
 
 __device__ __forceinline__ int64_t sampled_le(int64_t x, int64_t S, int64_t Tn) {
@@ -154,7 +156,8 @@ cudaError_t launch_group_ranges(int metric, const int32_t *sqnorm, const float *
     return cudaGetLastError();
 }
 
-cudaError_t launch_order_by_key(const int32_t *key, int64_t n, int32_t *perm, void *scratch,
+cudaError_t launch_order_by_key(const int32_t *key, int64_t n, bool stratify, int32_t *perm,
+                                void *scratch,
                                 size_t scratch_bytes, size_t *needed, cudaStream_t st) {
     // layout of scratch: [keys_out n*4][vals_in n*4][cub temp]
     size_t temp = 0;
@@ -174,7 +177,7 @@ cudaError_t launch_order_by_key(const int32_t *key, int64_t n, int32_t *perm, vo
                                         keys_out, vals_in, sorted, (int)n, 0, 32, st);
     if (e != cudaSuccess) return e;
     const int64_t Tn = n / 128;
-    const int64_t S = Tn >= 4 * kSampleTiles ? kSampleTiles : 0;
+    const int64_t S = (stratify && Tn >= 4 * kSampleTiles) ? kSampleTiles : 0;
     const int64_t T = (n - S * 128) / 4096;
     layout_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sorted, n, Tn, S, coprime_step(S),
                                                                T, coprime_step(T), perm);

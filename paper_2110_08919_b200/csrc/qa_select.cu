@@ -636,18 +636,22 @@ __global__ void estimate_kernel(const Entry *__restrict__ state,
                                 const int32_t *__restrict__ state_cnt, int32_t *__restrict__ thr,
                                 unsigned long long *__restrict__ est, int64_t nq, int64_t k,
                                 int64_t j, const int32_t *__restrict__ q_sqnorm,
-                                const float *__restrict__ q_norm) {
+                                const float *__restrict__ q_norm, bool combine) {
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
     if (state_cnt[q] < j) {
-        est[q] = ~0ull;
+        if (!combine) est[q] = ~0ull;
         return;
     }
     const Entry e = state[q * k + j - 1];
     const int32_t qq = (M == kL2) ? q_sqnorm[q] : 0;
     const float qn = (M == kAngular) ? q_norm[q] : 1.0f;
     thr[q] = threshold_of<M>(e, qq, qn);
-    est[q] = e.skey;
+    // rows that failed an earlier estimated pass are only known to be worse
+    // than THAT estimate: the final check needs the k-th at least as good as
+    // every estimate used
+    const unsigned long long prev = est[q];
+    est[q] = (combine && prev != ~0ull && prev < e.skey) ? prev : e.skey;
 }
 
 // After the final pass: the result is exact iff the k-th kept score is at
@@ -671,21 +675,22 @@ __global__ void check_estimate_kernel(const Entry *__restrict__ state,
 
 cudaError_t launch_estimate(const Entry *state, const int32_t *state_cnt, int32_t *thr,
                             unsigned long long *est, int64_t nq, int64_t k, int64_t j, int metric,
-                            const int32_t *q_sqnorm, const float *q_norm, cudaStream_t st) {
+                            const int32_t *q_sqnorm, const float *q_norm, bool combine,
+                            cudaStream_t st) {
     if (nq == 0) return cudaSuccess;
     const unsigned grid = (unsigned)((nq + 255) / 256);
     switch (metric) {
         case kIP:
             estimate_kernel<kIP><<<grid, 256, 0, st>>>(state, state_cnt, thr, est, nq, k, j,
-                                                       q_sqnorm, q_norm);
+                                                       q_sqnorm, q_norm, combine);
             break;
         case kL2:
             estimate_kernel<kL2><<<grid, 256, 0, st>>>(state, state_cnt, thr, est, nq, k, j,
-                                                       q_sqnorm, q_norm);
+                                                       q_sqnorm, q_norm, combine);
             break;
         default:
             estimate_kernel<kAngular><<<grid, 256, 0, st>>>(state, state_cnt, thr, est, nq, k, j,
-                                                            q_sqnorm, q_norm);
+                                                            q_sqnorm, q_norm, combine);
     }
     return cudaGetLastError();
 }

@@ -97,12 +97,13 @@ class DeviceCodes:
         ids = None if self.ids is None else self.ids[lo:hi]
         return DeviceCodes(self.codes[lo:hi], self.d, self.sqnorm[lo:hi], self.norm[lo:hi], ids)
 
-    def sorted_by_norm(self) -> "DeviceCodes":
+    def sorted_by_norm(self, stratify: bool = True) -> "DeviceCodes":
         """Copy with rows in ascending-norm order (stable) and ``ids`` mapping
         each stored row back to its position in this matrix.  The scan's
         per-warp bounds are tight on such a layout (qa_layout.cu)."""
         perm = torch.empty((self.n,), dtype=torch.int32, device=self.device)
-        check(lib.qa_order_rows_by_norm(_p(self.sqnorm), self.n, _p(perm), _stream()))
+        check(lib.qa_order_rows_by_norm(_p(self.sqnorm), self.n, 1 if stratify else 0, _p(perm),
+                                        _stream()))
         out = DeviceCodes.empty(self.n, self.d, self.device)
         check(lib.qa_permute_rows_i8(_p(self.codes), _p(self.sqnorm), _p(self.norm), self.n,
                                      self.ld, _p(perm), _p(out.codes), _p(out.sqnorm),

@@ -49,7 +49,9 @@ class Int8Index:
                      for a in (params.k, params.sb, params.se))
         codes = dev.encode(x, k, sb, se, params.bits)
         if sort_rows and Metric(metric) != Metric.INNER_PRODUCT:
-            codes = codes.sorted_by_norm()
+            # L2: a stratified sample region first (qa_layout.cu); angular
+            # norms are narrow and keep plain norm bands
+            codes = codes.sorted_by_norm(stratify=Metric(metric) == Metric.L2_SQUARED)
         return cls(params, Metric(metric), codes, k, sb, se, id_offset)
 
     def codes_in_input_order(self) -> np.ndarray:

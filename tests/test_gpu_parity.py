@@ -343,16 +343,18 @@ def test_virtual_shards_merge_equals_full(oracle, G):
 
 
 @pytest.mark.parametrize("metric", [0, 1, 2])
-def test_norm_sorted_index_equals_unsorted(oracle, metric):
-    # The index stores rows sorted by norm (tight per-warp filter bounds) and
-    # reports/tie-breaks by the caller's ids via row_ids: results must be
-    # identical to the unsorted layout and to the oracle.
+@pytest.mark.parametrize("stratify", [False, True])
+def test_norm_sorted_index_equals_unsorted(oracle, metric, stratify):
+    # The index stores rows in norm bands (tight per-unit filter bounds; with
+    # `stratify` after a stratified sample region, which needs >= 131072
+    # rows) and reports/tie-breaks by the caller's ids via row_ids: results
+    # must be identical to the unsorted layout and to the oracle.
     rng = np.random.default_rng(31 + metric)
-    X = _rand_codes(rng, 30_011, 64, -20, 21, nonzero=True)
+    X = _rand_codes(rng, 140_011, 64, -20, 21, nonzero=True)
     Q = _rand_codes(rng, 300, 64, -20, 21, nonzero=True)
     db = dev.DeviceCodes.from_host(X)
     qs = dev.DeviceCodes.from_host(Q)
-    srt = db.sorted_by_norm()
+    srt = db.sorted_by_norm(stratify=stratify)
     ids = srt.ids.cpu().numpy()
     assert sorted(ids.tolist()) == list(range(X.shape[0]))
     sq = srt.sqnorm.cpu().numpy()
@@ -414,3 +416,30 @@ def test_filter_bounds_hold_on_large_dots(oracle, metric):
     osc, oids = _scan_oracle(oracle, Xc, qc.to_host()[:16], 100, metric)
     np.testing.assert_array_equal(ids[:16].cpu().numpy(), oids)
     np.testing.assert_array_equal(sc[:16].cpu().numpy(), osc)
+
+
+@pytest.mark.parametrize("metric", [0, 1, 2])
+@pytest.mark.parametrize("force_j1", [None, "1"])
+def test_two_level_estimate_exact(oracle, monkeypatch, metric, force_j1):
+    # Two-level estimate: round 0's j1-th best bounds the rest of the
+    # prefix, the prefix's j-th best bounds the rest of the index, and the
+    # final check needs the k-th at least as good as both.  j1 = 1 makes the
+    # first level fail for many queries (recompute path); exact either way.
+    from paper_2110_08919_b200 import _lib
+
+    monkeypatch.setenv("QA_B200_EST_ROWS", "8192")
+    if force_j1:
+        monkeypatch.setenv("QA_B200_EST1_J", force_j1)
+    rng = np.random.default_rng(500 + metric)
+    X = _rand_codes(rng, 60_000, 64, -30, 31, nonzero=True)
+    Q = _rand_codes(rng, 300, 64, -30, 31, nonzero=True)
+    db = dev.DeviceCodes.from_host(X).sorted_by_norm()
+    qs = dev.DeviceCodes.from_host(Q)
+    sc, ids = dev.scan_topk(db, qs, 20, metric)
+    st = _lib.last_scan_stats()
+    osc, oids = _scan_oracle(oracle, X, Q, 20, metric)
+    np.testing.assert_array_equal(ids.cpu().numpy(), oids)
+    np.testing.assert_array_equal(sc.cpu().numpy(), osc)
+    assert st["rounds"] <= 3 + (3 * st["retries"] + 20)
+    if force_j1:
+        assert st["retries"] >= 1
