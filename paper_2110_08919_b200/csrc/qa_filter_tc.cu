@@ -78,7 +78,13 @@ constexpr int kMaxBiasReps = 8;
 // With small query tiles the MMA of a tile is short, and two buffers left
 // the pipeline bound by the MMA -> epilogue -> MMA hand-off latency.
 template <int N>
-__host__ __device__ constexpr int nacc() { return 512 / N < 8 ? 512 / N : 8; }  // bias MMAs per tile at most (|bias| <= 4.1M)
+__host__ __device__ constexpr int nacc() { return 512 / N < 8 ? 512 / N : 8; }
+// Small query tiles (N = 64, the HBM-bound small-batch regime) skip the bias
+// MMAs: each epilogue thread holds its 16 columns' bounds in registers and
+// compares directly.  The tensor pipe then runs 4 MMAs per tile instead of
+// 4 + reps (measured -20 % per tile with the bias MMAs removed).
+template <int N>
+__host__ __device__ constexpr bool direct_bounds() { return N == 64; }  // bias MMAs per tile at most (|bias| <= 4.1M)
 // try_wait suspend-time hint for the epilogue warps' waits (ns)
 constexpr int kWaitHintNs = 20000;
 
@@ -478,7 +484,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int32_t *exc_s = bias_s + 2 * N;                                // [2][N/32] flags
     int32_t *qcnt_all = exc_s + 2 * (N / 32);                       // [2][N] staged per query
     int32_t *qbase = qcnt_all + 2 * N;                              // [N] (flush warp)
-    uint64_t *bars = (uint64_t *)(qbase + N);
+    int32_t *bnd_all = qbase + N;                                   // [2][N] direct bounds
+    uint64_t *bars = (uint64_t *)(bnd_all + 2 * N);
     uint64_t *a_full = bars;
     uint64_t *a_empty = a_full + p.stages;
     uint64_t *b_full = a_empty + p.stages;
@@ -666,7 +673,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (!no_bias)
                         for (int r = 1; r < reps; ++r)
                             mma_bias_elect(tmem_d, abias_desc, bbias_desc, idesc);
-                    mma_bias_commit_elect(tmem_d, abias_desc, bbias_desc, idesc, no_bias ? 0u : 1u,
+                    mma_bias_commit_elect(tmem_d, abias_desc, bbias_desc, idesc,
+                                          (no_bias || reps == 0) ? 0u : 1u,
                                           smem_u32(acc_full + acc));
                 }
                 if (++acc == kNacc) {
@@ -790,8 +798,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) need = max(need, __shfl_xor_sync(0xffffffffu, need, o));
-            const int reps = filtered ? max(1, need) : 1;
-            const long long unit_a = (long long)kBiasA * reps;
+            constexpr bool kDirect = direct_bounds<N>();
+            const int reps = kDirect ? 0 : (filtered ? max(1, need) : 1);
+            const long long unit_a = (long long)kBiasA * (reps > 0 ? reps : 1);
+            int32_t *bnd_out = bnd_all + slot * N;
 #pragma unroll
             for (int i = 0; i < kQPL; ++i) {
                 const int q = i * 32 + lane;
@@ -801,7 +811,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 thr_out[q] = (filtered && q < nqt)
                                  ? Tq[i]
                                  : ((M == kIP) ? INT32_MAX : (M == kL2 ? INT32_MIN : 0x7fc00000));
-                if (!filtered) {
+                if constexpr (kDirect) {
+                    // dot >= bnd; |dot| < 2^30, so dot - bnd never wraps
+                    const long long B = !filtered ? -(1ll << 30)
+                                                  : (q < nqt ? Bq[i] : (1ll << 30));
+                    bnd_out[q] = (int32_t)(B < -(1ll << 30) ? -(1ll << 30)
+                                                            : (B > (1ll << 30) ? (1ll << 30) : B));
+                    S = 0;
+                } else if (!filtered) {
                     S = 0;  // dense / diagnostic passes: plain dots
                 } else if (q < nqt) {
                     // smallest S with reps*127*S >= -B
@@ -814,7 +831,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (s < kSMin) s = kSMin;
                     S = (int)s;
                 }
-                bias_out[q] = (int32_t)(unit_a * S);
+                // direct mode: the epilogue adds bias_q = -bound in registers
+                bias_out[q] = kDirect ? -bnd_out[q] : (int32_t)(unit_a * S);
                 // spread S over 32 int8 digits: base + (j < rem)
                 const int base = (S >= 0) ? S / kBiasK : -((-S + kBiasK - 1) / kBiasK);
                 const int rem = S - base * kBiasK;  // 0 .. 31
@@ -956,6 +974,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int ci = 0; ci < kCB / kC; ++ci)
                     if ((excm >> ci) & 1u) excg |= ((1u << (kC / 8)) - 1u) << (ci * (kC / 8));
                 int32_t row = wrow0 + lane;
+                constexpr bool kDirect = direct_bounds<N>();
+                int32_t bq[kDirect ? kCB : 1];
+                if constexpr (kDirect) {
+#pragma unroll
+                    for (int c = 0; c < kCB; ++c) bq[c] = lds32(bias_addr + 4u * (uint32_t)(col0 + c));
+                }
                 for (int ti = 0; ti < ntl; ++ti, row += kBlockM) {
                     WSTAT(11, mbar_wait(acc_full + acc, accph));
                     tc_fence_after();
@@ -972,6 +996,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (++acc == kNacc) {
                         acc = 0;
                         accph ^= 1;
+                    }
+                    if constexpr (kDirect) {  // the bias the MMA did not add
+#pragma unroll
+                        for (int ci = 0; ci < kCB / kC; ++ci)
+#pragma unroll
+                            for (int j = 0; j < kC; ++j) v[ci][j] += bq[ci * kC + j];
                     }
                     uint32_t hit = 0;
 #pragma unroll
@@ -1071,9 +1101,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                             if (a.mode == 1) {
                                 out = Cand{row, v[ci][j]};
                             } else {
-                                const int32_t dot = (int32_t)((uint32_t)v[ci][j] -
-                                                              (uint32_t)lds32(bias_addr + 4u * (uint32_t)c));
-                                out = (v[ci][j] >= 0 || exc) ? Cand{row, dot} : Cand{-1, 0};
+                                const int32_t bias_c = lds32(bias_addr + 4u * (uint32_t)c);
+                                // direct mode: TMEM holds the plain dot
+                                const int32_t biased = direct_bounds<N>() ? v[ci][j] + bias_c : v[ci][j];
+                                const int32_t dot = (int32_t)((uint32_t)biased - (uint32_t)bias_c);
+                                out = (biased >= 0 || exc) ? Cand{row, dot} : Cand{-1, 0};
                             }
                             dst[(int64_t)c * a.cap] = out;
                         }
@@ -1251,7 +1283,7 @@ cudaError_t launch_t(const FilterArgs &a, cudaStream_t st) {
                          kBlockM * kBiasK + 2 * (size_t)N * kBiasK +
                          2 * (size_t)p.stage_cap * sizeof(Staged) +
                          (M == kIP || !kExactInEpilogue ? 0 : 2 * (size_t)kUnitRowsMax * sizeof(int32_t)) +
-                         (7 * N + 2 * (N / 32)) * sizeof(int32_t) + 512;
+                         (9 * N + 2 * (N / 32)) * sizeof(int32_t) + 512;
     const size_t budget = 227 * 1024;
     const size_t stage_bytes = (size_t)kBlockM * SW;
     // each stage also costs two 8-byte mbarriers
@@ -1284,6 +1316,12 @@ cudaError_t dispatch_n(const FilterArgs &a, cudaStream_t st) {
     // Largest query tile whose B buffer fits 64 KiB, no larger than the query
     // chunk needs.
     int nmax = (int)(65536 / a.kdim);
+    static const int force_n = [] {  // diagnostics: QA_B200_TILE_N=128 / 64
+        const char *v = getenv("QA_B200_TILE_N");
+        return v ? atoi(v) : 0;
+    }();
+    if (force_n == 128 && nmax >= 128) return dispatch_metric<SW, 128>(a, st);
+    if (force_n == 64 && nmax >= 64) return dispatch_metric<SW, 64>(a, st);
     if (a.nq > 128 && nmax >= 256) return dispatch_metric<SW, 256>(a, st);
     if (a.nq > 64 && nmax >= 128) return dispatch_metric<SW, 128>(a, st);
     if (nmax >= 64) return dispatch_metric<SW, 64>(a, st);
