@@ -1003,19 +1003,25 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                             for (int j = 0; j < kC; ++j) v[ci][j] += bq[ci * kC + j];
                     }
-                    uint32_t hit = 0;
+                    // one AND over all of this lane's values first: most
+                    // lane-tiles hold no candidate, and the per-group mask
+                    // below is only built for the others
+                    int32_t g8s[kCB / 8];
 #pragma unroll
                     for (int ci = 0; ci < kCB / kC; ++ci)
 #pragma unroll
                         for (int h = 0; h < kC / 8; ++h) {
                             const int32_t *c8 = v[ci] + 8 * h;
-                            const int32_t g8 = (c8[0] & c8[1] & c8[2]) & (c8[3] & c8[4] & c8[5]) &
-                                               (c8[6] & c8[7]);
-                            hit |= ((uint32_t)~g8 >> 31) << (ci * (kC / 8) + h);
+                            g8s[ci * (kC / 8) + h] = (c8[0] & c8[1] & c8[2]) &
+                                                     (c8[3] & c8[4] & c8[5]) & (c8[6] & c8[7]);
                         }
-                    hit = row < r_hi ? (hit | excg) : 0u;
-                    if (!hit) continue;
-                    if (p.experiment == 8) continue;  // diagnostics: drop survivors
+                    int32_t gall = g8s[0];
+#pragma unroll
+                    for (int g = 1; g < kCB / 8; ++g) gall &= g8s[g];
+                    if ((gall < 0 && !excg) || row >= r_hi) continue;
+                    uint32_t hit = excg;
+#pragma unroll
+                    for (int g = 0; g < kCB / 8; ++g) hit |= ((uint32_t)~g8s[g] >> 31) << g;
                     // slow path (lanes with a candidate group only): exact
                     // test of every non-negative column of a hit group
                     const int rowrel = row - unit_row0;
