@@ -102,7 +102,10 @@ int qa_norms_i8(const int8_t *codes, int64_t n, int64_t d, int64_t ldc,
  * ids.  Writes keff = min(k, n) entries per query, ascending by
  * (score, id): out_scores float64[nq, keff], out_ids int32[nq, keff] where
  * id = (row_ids ? row_ids[row] : row) + id_offset.  Synchronises `stream`
- * once at the end (overflow check of the candidate buffers). */
+ * once at the end (overflow check of the candidate buffers).  keff <= 2048
+ * runs the tensor-core filter + select; 2048 < keff <= 15360 runs the
+ * float64-exact scan on the codes (bit-identical results, slower); larger
+ * keff returns QA_EUNSUPPORTED. */
 int qa_scan_topk_i8(const int8_t *db, int64_t n, int64_t d, int64_t ldd,
                     const int32_t *db_sqnorm, const float *db_norm,
                     const int32_t *row_ids,
@@ -131,7 +134,7 @@ int qa_scan_topk_i8_host(const int8_t *data, int64_t n, int64_t d,
  * explicit round-to-nearest adds); rows ascending by (score, id), ids + id_offset.
  * db_norm/q_norm (float32, the caller's) are read for metric 2 only.  Inputs
  * must be finite (the reference's heap order with NaN scores is
- * insertion-order dependent).  keff = min(k, n) <= 2048.  Asynchronous. */
+ * insertion-order dependent).  keff = min(k, n) <= 15360.  Asynchronous. */
 int qa_scan_topk_f32(const float *db, int64_t n, int64_t d, int64_t ldd,
                      const float *db_norm, const float *q, int64_t nq, int64_t ldq,
                      const float *q_norm, int64_t k, int metric, int64_t id_offset,

@@ -463,6 +463,55 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
     return QA_OK;
 }
 
+// Body of qa_scan_topk_f32 (validated arguments, workspace lock held).
+int f32_impl(Workspace &ws, const float *db, int64_t n, int64_t d, int64_t ldd,
+             const float *db_norm, const float *q, int64_t nq, int64_t ldq, const float *q_norm,
+             int64_t keff, int metric, int64_t id_offset, double *out_scores, int32_t *out_ids,
+             cudaStream_t st) {
+    if (keff > kMaxKF32) return set_err(QA_EUNSUPPORTED, "k above this build's limit");
+    if (n > INT32_MAX || d > INT32_MAX) return set_err(QA_EUNSUPPORTED, "shape above this build's limit");
+    constexpr int64_t kF32Rows = 16384, kF32Queries = 1024;
+    const int64_t R = std::min(n, kF32Rows);
+    const int64_t qc = std::min(nq, kF32Queries);
+    QA_TRY(ws.f32_scores.reserve((size_t)qc * R * 8), "workspace");
+    QA_TRY(ws.f32_ss.reserve((size_t)qc * keff * 8), "workspace");
+    QA_TRY(ws.f32_si.reserve((size_t)qc * keff * 4), "workspace");
+    QA_TRY(ws.f32_sn.reserve((size_t)qc * 4), "workspace");
+    double *sc = (double *)ws.f32_scores.ptr, *ss = (double *)ws.f32_ss.ptr;
+    int32_t *si = (int32_t *)ws.f32_si.ptr, *sn = (int32_t *)ws.f32_sn.ptr;
+    for (int64_t c0 = 0; c0 < nq; c0 += qc) {
+        const int64_t m = std::min(qc, nq - c0);
+        QA_TRY(cudaMemsetAsync(sn, 0, (size_t)m * 4, st), "memset");
+        for (int64_t r0 = 0; r0 < n; r0 += R) {
+            const int64_t rows = std::min(R, n - r0);
+            QA_TRY(launch_f32_scores(db, ldd, q + c0 * ldq, ldq, d, m, r0, rows, metric, db_norm,
+                                     q_norm ? q_norm + c0 : nullptr, sc, R, st),
+                   "f32 scores");
+            QA_TRY(launch_f32_select(sc, R, rows, r0, ss, si, sn, m, keff, st), "f32 select");
+        }
+        QA_TRY(launch_f32_finalize(ss, si, m, keff, id_offset, out_scores + c0 * keff,
+                                   out_ids + c0 * keff, st),
+               "f32 finalize");
+    }
+    return QA_OK;
+}
+
+// int8 codes [n, ld] (stored order, row_ids -> caller order) as float32
+// [n, d] rows in CALLER order; norms likewise.  Every int8 dot, l2 and
+// angular score is an exact float64 computation on these values, so the
+// float32 scan reproduces the int8 path bit for bit (used for k beyond the
+// int8 select's limit).
+__global__ void codes_to_f32_kernel(const int8_t *__restrict__ codes, int64_t n, int64_t d,
+                                    int64_t ld, const int32_t *__restrict__ row_ids,
+                                    const float *__restrict__ norm_in, float *__restrict__ out,
+                                    float *__restrict__ norm_out) {
+    const int64_t r = blockIdx.x;
+    if (r >= n) return;
+    const int64_t dst = row_ids ? (int64_t)row_ids[r] : r;
+    for (int64_t j = threadIdx.x; j < d; j += blockDim.x) out[dst * d + j] = (float)codes[r * ld + j];
+    if (threadIdx.x == 0 && norm_in) norm_out[dst] = norm_in[r];
+}
+
 int scan_entry(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_t *db_sqnorm,
                const float *db_norm, const int32_t *row_ids, const int8_t *q, int64_t nq, int64_t ldq,
                const int32_t *q_sqnorm, const float *q_norm, int64_t k, int metric,
@@ -481,9 +530,9 @@ int scan_entry(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_
         return set_err(QA_EINVAL, "angular metric needs data and query norms");
     if (metric == kL2 && (!db_sqnorm || !q_sqnorm))
         return set_err(QA_EINVAL, "L2 metric needs data and query squared norms");
-    if (keff > kMaxK)
+    if (keff > kMaxKF32)
         return set_err(QA_EUNSUPPORTED, "k=%lld above this build's limit %lld", (long long)keff,
-                       (long long)kMaxK);
+                       (long long)kMaxKF32);
     // int32 exactness: |dot| <= d*128^2 and l2 <= d*255^2 must stay < 2^31
     // (the reference accumulates in C int as well, _core.pyx:49-63).
     if (d > 131071 || (metric == kL2 && d > 33025))
@@ -492,6 +541,34 @@ int scan_entry(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_
     if (n > INT32_MAX) return set_err(QA_EUNSUPPORTED, "n exceeds int32 ids");
     Workspace &ws = g_ws[current_device() % kMaxDevices];
     std::lock_guard<std::mutex> lock(ws.mu);
+    if (keff > kMaxK) {
+        // large k: the float64-exact scan on the codes as float32 (bit-exact
+        // with the int8 path, see codes_to_f32_kernel), caller row order
+        float *xf = nullptr, *qf = nullptr, *xn = nullptr;
+        int rc = QA_OK;
+        cudaError_t e = cudaMalloc(&xf, (size_t)n * d * 4 + 16);
+        if (e == cudaSuccess) e = cudaMalloc(&qf, (size_t)nq * d * 4 + 16);
+        if (e == cudaSuccess) e = cudaMalloc(&xn, (size_t)n * 4 + 16);
+        if (e == cudaSuccess) {
+            codes_to_f32_kernel<<<(unsigned)n, 128, 0, st>>>(db, n, d, ld, row_ids,
+                                                             metric == kAngular ? db_norm : nullptr,
+                                                             xf, xn);
+            codes_to_f32_kernel<<<(unsigned)nq, 128, 0, st>>>(q, nq, d, ld, nullptr, nullptr, qf,
+                                                              nullptr);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess)
+            rc = f32_impl(ws, xf, n, d, d, metric == kAngular ? xn : nullptr, qf, nq, d,
+                          metric == kAngular ? q_norm : nullptr, keff, metric, id_offset,
+                          out_scores, out_ids, st);
+        else
+            rc = cuda_err(e, "large-k path");
+        if (rc == QA_OK && (e = cudaStreamSynchronize(st)) != cudaSuccess) rc = cuda_err(e, "large-k path");
+        cudaFree(xf);
+        cudaFree(qf);
+        cudaFree(xn);
+        return rc;
+    }
     std::vector<int32_t> ovf;
     g_timer.reset();
     int rc = scan_impl(ws, db, n, d, ld, db_sqnorm, db_norm, row_ids, q, nq, q_sqnorm, q_norm, keff, metric,
@@ -722,35 +799,10 @@ int qa_scan_topk_f32(const float *db, int64_t n, int64_t d, int64_t ldd, const f
     if (n == 0 || nq == 0 || keff == 0) return QA_OK;
     if (metric == kAngular && (!db_norm || !q_norm))
         return set_err(QA_EINVAL, "angular metric needs data and query norms");
-    if (keff > kMaxK) return set_err(QA_EUNSUPPORTED, "k above this build's limit");
-    if (n > INT32_MAX || d > INT32_MAX) return set_err(QA_EUNSUPPORTED, "shape above this build's limit");
-    cudaStream_t st = (cudaStream_t)stream;
     Workspace &ws = g_ws[current_device() % kMaxDevices];
     std::lock_guard<std::mutex> lock(ws.mu);
-    constexpr int64_t kF32Rows = 16384, kF32Queries = 1024;
-    const int64_t R = std::min(n, kF32Rows);
-    const int64_t qc = std::min(nq, kF32Queries);
-    QA_TRY(ws.f32_scores.reserve((size_t)qc * R * 8), "workspace");
-    QA_TRY(ws.f32_ss.reserve((size_t)qc * keff * 8), "workspace");
-    QA_TRY(ws.f32_si.reserve((size_t)qc * keff * 4), "workspace");
-    QA_TRY(ws.f32_sn.reserve((size_t)qc * 4), "workspace");
-    double *sc = (double *)ws.f32_scores.ptr, *ss = (double *)ws.f32_ss.ptr;
-    int32_t *si = (int32_t *)ws.f32_si.ptr, *sn = (int32_t *)ws.f32_sn.ptr;
-    for (int64_t c0 = 0; c0 < nq; c0 += qc) {
-        const int64_t m = std::min(qc, nq - c0);
-        QA_TRY(cudaMemsetAsync(sn, 0, (size_t)m * 4, st), "memset");
-        for (int64_t r0 = 0; r0 < n; r0 += R) {
-            const int64_t rows = std::min(R, n - r0);
-            QA_TRY(launch_f32_scores(db, ldd, q + c0 * ldq, ldq, d, m, r0, rows, metric, db_norm,
-                                     q_norm ? q_norm + c0 : nullptr, sc, R, st),
-                   "f32 scores");
-            QA_TRY(launch_f32_select(sc, R, rows, r0, ss, si, sn, m, keff, st), "f32 select");
-        }
-        QA_TRY(launch_f32_finalize(ss, si, m, keff, id_offset, out_scores + c0 * keff,
-                                   out_ids + c0 * keff, st),
-               "f32 finalize");
-    }
-    return QA_OK;
+    return f32_impl(ws, db, n, d, ldd, db_norm, q, nq, ldq, q_norm, keff, metric, id_offset,
+                    out_scores, out_ids, (cudaStream_t)stream);
 }
 
 int qa_estimate_stats_f32(const float *x, int64_t n, int64_t d, int64_t ldx, double *mu,

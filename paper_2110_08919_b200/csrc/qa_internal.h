@@ -135,7 +135,11 @@ cudaError_t launch_estimate_stats(const float *x, int64_t n, int64_t d, int64_t 
 
 // Largest list the select kernel sorts in shared memory at once.
 constexpr int64_t kSortMax = 8192;
-// Largest k served (k + one candidate chunk must fit kSortMax).
+// Largest k served by the int8 select (k + one candidate chunk must fit
+// kSortMax); larger k (up to kMaxKF32) take the float64-exact scan on the
+// codes, which sorts state + a 1024-candidate chunk of 12-byte entries in
+// shared memory (16384 entries = 192 KiB).
 constexpr int64_t kMaxK = 2048;
+constexpr int64_t kMaxKF32 = 16384 - 1024;
 
 }  // namespace qa

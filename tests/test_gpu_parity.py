@@ -443,3 +443,23 @@ def test_two_level_estimate_exact(oracle, monkeypatch, metric, force_j1):
     assert st["rounds"] <= 3 + (3 * st["retries"] + 20)
     if force_j1:
         assert st["retries"] >= 1
+
+
+@pytest.mark.parametrize("metric", [0, 1, 2])
+def test_large_k_beyond_int8_select(oracle, metric):
+    # k above the int8 select's limit (2048) runs the float64-exact scan on
+    # the codes (norm-sorted index: stored rows are scattered back to caller
+    # order first) -- results identical to the reference order.
+    rng = np.random.default_rng(900 + metric)
+    X = _rand_codes(rng, 9000, 40, -6, 7, nonzero=True)   # heavy ties
+    Q = _rand_codes(rng, 7, 40, -6, 7, nonzero=True)
+    db = dev.DeviceCodes.from_host(X).sorted_by_norm()
+    qs = dev.DeviceCodes.from_host(Q)
+    for k in (2049, 5000, 9000):
+        sc, ids = dev.scan_topk(db, qs, k, metric, id_offset=3)
+        osc, oids = _scan_oracle(oracle, X, Q, k, metric)
+        np.testing.assert_array_equal(ids.cpu().numpy(), oids + 3)
+        np.testing.assert_array_equal(sc.cpu().numpy(), osc)
+    with pytest.raises(NotImplementedError):
+        big = dev.DeviceCodes.from_host(_rand_codes(rng, 20_000, 8))
+        dev.scan_topk(big, dev.DeviceCodes.from_host(_rand_codes(rng, 1, 8)), 16_000, metric)
