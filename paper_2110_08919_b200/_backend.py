@@ -11,6 +11,8 @@ Surface (host numpy in, host numpy out, reference semantics):
 * ``scan_topk(data, queries, k, metric, data_norms=None, query_norms=None)``
   -> (float64 [nq, keff], int32 [nq, keff]), _core.pyx:333-365;
 * ``norms(mat)`` -> float32 [n], _core.pyx:137-157;
+* ``dot(a, b)`` / ``l2sq(a, b)`` -- single pairs, _core.pyx:99-134 (through
+  the same kernels with n = nq = 1; the batch paths are the hot ones);
 * ``quantize(values, k, sb, se, bits)`` -> int8 [n, d] -- the encode hook the
   reference lacks (its quantizer.py:291-300 calls numpy directly).
 
@@ -76,6 +78,31 @@ def scan_topk(data, queries, k, metric, data_norms=None, query_norms=None):
         qn = torch.from_numpy(np.ascontiguousarray(query_norms, dtype=np.float32)).to(dev)
     scores, ids = _dev.scan_topk(db, qs, int(k), int(metric), dn, qn)
     return scores.cpu().numpy(), ids.cpu().numpy()
+
+
+def _pair(a, b, metric: int) -> float:
+    """One pair through the exhaustive-scan kernels (n = nq = 1, k = 1)."""
+    if a.shape[0] != b.shape[0]:
+        raise ValueError("length mismatch")
+    if a.dtype != b.dtype:
+        raise ValueError("dtype mismatch")
+    if a.shape[0] == 0:
+        return 0.0
+    x = np.ascontiguousarray(b).reshape(1, -1)
+    q = np.ascontiguousarray(a).reshape(1, -1)
+    scores, _ = scan_topk(x, q, 1, metric)
+    return float(scores[0, 0])
+
+
+def dot(a, b):
+    """Inner product of two 1-D vectors of equal dtype (_core.pyx:99-115):
+    float32 -> float64 sequential sum, int8 -> exact int32 sum, as float."""
+    return -_pair(a, b, 0) + 0.0   # score = -dot; + 0.0 turns -0.0 into 0.0
+
+
+def l2sq(a, b):
+    """Squared Euclidean distance of two 1-D vectors (_core.pyx:118-134)."""
+    return _pair(a, b, 1)
 
 
 def norms(mat):

@@ -463,3 +463,39 @@ def test_large_k_beyond_int8_select(oracle, metric):
     with pytest.raises(NotImplementedError):
         big = dev.DeviceCodes.from_host(_rand_codes(rng, 20_000, 8))
         dev.scan_topk(big, dev.DeviceCodes.from_host(_rand_codes(rng, 1, 8)), 16_000, metric)
+
+
+def test_pair_distances_backend_and_module():
+    # reference test_distances.py:32-54 hand values, through _backend.dot /
+    # l2sq (the seam's pair kernels) and the distances module wrappers
+    from paper_2110_08919_b200 import distances as D
+    assert _backend.dot(np.int8([1, 2, 3]), np.int8([4, 5, 6])) == 32.0
+    assert _backend.dot(np.int8([127] * 3), np.int8([127] * 3)) == 48387.0
+    assert _backend.l2sq(np.int8([-128]), np.int8([127])) == 65025.0
+    assert _backend.l2sq(np.int8([1, 2]), np.int8([4, 6])) == 25.0
+    assert _backend.dot(np.int8([]), np.int8([])) == 0.0
+    assert D.dot_i8(np.int8([1, -2]), np.int8([3, 4])) == -5
+    with pytest.raises(ValueError, match="length mismatch"):
+        _backend.dot(np.int8([1]), np.int8([1, 2]))
+    with pytest.raises(ValueError, match="dtype mismatch"):
+        _backend.l2sq(np.int8([1]), np.float32([1]))
+    with pytest.raises(qa.DimensionMismatch):
+        D.dot_f32(np.float32([1]), np.float32([1, 2]))
+    rng = np.random.default_rng(3)
+    for _ in range(5):
+        a = rng.normal(size=77).astype(np.float32)
+        b = rng.normal(size=77).astype(np.float32)
+        acc = 0.0
+        for x, y in zip(a.tolist(), b.tolist()):
+            acc += x * y                        # float64, sequential: _dot_f
+        assert D.dot_f32(a, b) == acc
+        l2 = 0.0
+        for x, y in zip(a.tolist(), b.tolist()):
+            t = x - y
+            l2 += t * t
+        assert D.l2sq_f32(a, b) == l2
+        assert D.distance(qa.Metric.INNER_PRODUCT, a, b) == -acc
+        na, nb = float(np.sqrt(D.dot_f32(a, a))), float(np.sqrt(D.dot_f32(b, b)))
+        assert D.angular(a, b) == 1.0 - acc / (na * nb)
+    with pytest.raises(qa.ZeroNorm):
+        D.angular(np.int8([0, 0]), np.int8([1, 1]))
