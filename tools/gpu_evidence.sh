@@ -10,5 +10,5 @@ timeout -s KILL 900 python tools/bench_configs.py --config 4 --iters 200 --parit
 B="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
 timeout -s KILL 300 $B > gpurun_out/ev_b1.log 2>&1 && \
 timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ev_launches.csv $B > gpurun_out/ev_ncu1.log 2>&1; echo "launch list rc=$?"
-timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:filter_tc -s 27 -c 1 -o gpurun_out/ev_filter $B > gpurun_out/ev_ncu2.log 2>&1; echo "ncu filter rc=$?"
-timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:select -s 27 -c 1 -o gpurun_out/ev_select $B > gpurun_out/ev_ncu3.log 2>&1; echo "ncu select rc=$?"
+timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:filter_tc -s 11 -c 1 -o gpurun_out/ev_filter $B > gpurun_out/ev_ncu2.log 2>&1; echo "ncu filter rc=$?"
+timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:select -s 11 -c 1 -o gpurun_out/ev_select $B > gpurun_out/ev_ncu3.log 2>&1; echo "ncu select rc=$?"
