@@ -38,8 +38,9 @@ namespace {
 constexpr int64_t kSampleTiles = 256;  // 32768 rows = the plan's estimate prefix
 
 __device__ __forceinline__ int64_t sampled_le(int64_t x, int64_t S, int64_t Tn) {
-    // number of k in [0, S) with floor(k * Tn / S) <= x
-    if (x < 0) return 0;
+    // number of k in [0, S) with floor(k * Tn / S) <= x (S == 0: no sample
+    // region, and Tn may be 0 then)
+    if (x < 0 || S == 0) return 0;
     const int64_t c = ((x + 1) * S + Tn - 1) / Tn;
     return c < S ? c : S;
 }

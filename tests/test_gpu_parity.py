@@ -499,3 +499,35 @@ def test_pair_distances_backend_and_module():
         assert D.angular(a, b) == 1.0 - acc / (na * nb)
     with pytest.raises(qa.ZeroNorm):
         D.angular(np.int8([0, 0]), np.int8([1, 1]))
+
+
+def test_index_angular_rejects_zero_norm_codes():
+    # reference exact.py:67-69: angular needs nonzero vectors (ZeroNorm)
+    X = np.zeros((300, 8), np.float32)
+    X[:, 0] = np.linspace(0.0, 1.0, 300, dtype=np.float32)   # row 0 (all zero) -> code norm 0
+    idx = qa.Int8Index.build(torch.from_numpy(X).cuda(), qa.Metric.ANGULAR, "symmetric")
+    zero_rows = int((idx.codes.sqnorm == 0).sum())
+    q = torch.from_numpy(np.ones((2, 8), np.float32)).cuda()
+    if zero_rows:
+        with pytest.raises(qa.ZeroNorm):
+            idx.search(q, 5)
+    qz = torch.zeros((1, 8), dtype=torch.float32, device="cuda")
+    X2 = np.ones((50, 8), np.float32)
+    idx2 = qa.Int8Index.build(torch.from_numpy(X2).cuda(), qa.Metric.ANGULAR, "symmetric")
+    with pytest.raises(qa.ZeroNorm):
+        idx2.search(qz, 5)
+
+
+@pytest.mark.parametrize("n", [1, 50, 127, 128, 129, 300])
+def test_sorted_index_tiny(oracle, n):
+    # layouts of indexes smaller than one tile / one norm block
+    rng = np.random.default_rng(n)
+    X = _rand_codes(rng, n, 8, nonzero=True)
+    Q = _rand_codes(rng, 3, 8, nonzero=True)
+    for stratify in (False, True):
+        db = dev.DeviceCodes.from_host(X).sorted_by_norm(stratify=stratify)
+        assert sorted(db.ids.cpu().numpy().tolist()) == list(range(n))
+        sc, ids = dev.scan_topk(db, dev.DeviceCodes.from_host(Q), 5, 1)
+        osc, oids = _scan_oracle(oracle, X, Q, 5, 1)
+        np.testing.assert_array_equal(ids.cpu().numpy(), oids)
+        np.testing.assert_array_equal(sc.cpu().numpy(), osc)
