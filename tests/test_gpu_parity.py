@@ -194,7 +194,9 @@ def test_heavy_ties_exercise_overflow_retry(oracle, metric):
 def test_many_queries_and_edge_shapes(oracle):
     rng = np.random.default_rng(9)
     for n, nq, d, k in ((1, 5, 3, 1), (1, 5, 3, 10), (129, 513, 16, 128), (5000, 1500, 40, 30),
-                        (300, 2, 200, 300), (257, 3, 64, 2048)):
+                        (300, 2, 200, 300), (257, 3, 64, 2048),
+                        (3000, 70, 1024, 10),    # widest tensor-core K (64-query tiles)
+                        (2000, 7, 1500, 10)):    # K > 1024: the dp4a filter
         for metric in (0, 1, 2):
             X = _rand_codes(rng, n, d, nonzero=True)
             Q = _rand_codes(rng, nq, d, nonzero=True)
