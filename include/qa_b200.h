@@ -44,7 +44,8 @@ enum {
     QA_EIO = 5,          /* OSError (open/read/write failed) */
     QA_ETRUNCATED = 6,   /* TruncatedRecord (errors.py) */
     QA_ENONPOSITIVE = 7, /* NonPositiveDim */
-    QA_EDIM = 8          /* DimensionMismatch */
+    QA_EDIM = 8,         /* DimensionMismatch */
+    QA_EZERONORM = 9     /* ZeroNorm: angular with a norm <= 0 (exact.py:67-69) */
 };
 
 /* Library identification. */
@@ -102,7 +103,9 @@ int qa_norms_i8(const int8_t *codes, int64_t n, int64_t d, int64_t ldc,
  * ids.  Writes keff = min(k, n) entries per query, ascending by
  * (score, id): out_scores float64[nq, keff], out_ids int32[nq, keff] where
  * id = (row_ids ? row_ids[row] : row) + id_offset.  Synchronises `stream`
- * once at the end (overflow check of the candidate buffers).  keff <= 2048
+ * once at the end (overflow check of the candidate buffers).  Angular with a
+ * norm <= 0 returns QA_EZERONORM (the reference's exact.py raises ZeroNorm
+ * before its scan; its raw _core would order NaN/inf scores).  keff <= 2048
  * runs the tensor-core filter + select; 2048 < keff <= 15360 runs the
  * float64-exact scan on the codes (bit-identical results, slower); larger
  * keff returns QA_EUNSUPPORTED. */

@@ -27,6 +27,7 @@ QA_EIO = 5
 QA_ETRUNCATED = 6
 QA_ENONPOSITIVE = 7
 QA_EDIM = 8
+QA_EZERONORM = 9
 
 c_i64 = ctypes.c_int64
 c_int = ctypes.c_int
@@ -119,6 +120,9 @@ def check(rc: int) -> None:
         raise ValueError(msg)
     if rc == QA_EUNSUPPORTED:
         raise NotImplementedError(msg)
+    if rc == QA_EZERONORM:
+        from .errors import ZeroNorm
+        raise ZeroNorm(msg)
     if rc in (QA_ETRUNCATED, QA_ENONPOSITIVE, QA_EDIM):
         from . import errors
         raise {QA_ETRUNCATED: errors.TruncatedRecord, QA_ENONPOSITIVE: errors.NonPositiveDim,

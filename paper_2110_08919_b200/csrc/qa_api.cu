@@ -277,6 +277,16 @@ __global__ void scatter_results_kernel(const double *__restrict__ s, const int32
     out_i[(int64_t)idx[r] * keff + j] = i[t];
 }
 
+// flag[0] := 1 when any angular norm is <= 0 (or NaN): the reference raises
+// ZeroNorm before scanning (exact.py:67-69); here the check rides on the
+// scan's one end-of-search readback
+__global__ void zero_norm_kernel(const float *__restrict__ a, int64_t na,
+                                 const float *__restrict__ b, int64_t nb, int32_t *flag) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const float v = i < na ? a[i] : (i < na + nb ? b[i - na] : 1.0f);
+    if (!(v > 0.0f)) *flag = 1;
+}
+
 // One complete search with a given minimum candidate capacity.  Returns
 // QA_OK; *overflowed receives the list of queries whose lists overflowed
 // (their output rows are invalid and must be recomputed).
@@ -307,6 +317,11 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
     int32_t *flags = (int32_t *)ws.flags.ptr;  // [0] any overflow, [4:6) candidate counter
     QA_TRY(cudaMemsetAsync(ovf, 0, (size_t)nq * 4, st), "memset");
     QA_TRY(cudaMemsetAsync(flags, 0, 64, st), "memset");
+    if (metric == kAngular) {
+        zero_norm_kernel<<<(unsigned)((n + nq + 255) / 256), 256, 0, st>>>(db_norm, n, q_norm, nq,
+                                                                           flags + 2);
+        QA_TRY(cudaGetLastError(), "norm check");
+    }
     const bool simt = use_simt_filter(ld);
     // norm range of every 128-row tile (per-unit filter bounds)
     const int64_t groups = (n + 127) / 128;
@@ -448,6 +463,8 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
     QA_TRY(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, st),
            "overflow check");
     QA_TRY(cudaStreamSynchronize(st), "sync");
+    if (hflags[2])
+        return set_err(QA_EZERONORM, "angular metric needs nonzero corpus and query vectors");
     const int32_t any = hflags[0];
     unsigned long long cands = 0;
     std::memcpy(&cands, hflags + 4, sizeof(cands));
@@ -556,6 +573,22 @@ int scan_entry(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_
             codes_to_f32_kernel<<<(unsigned)nq, 128, 0, st>>>(q, nq, d, ld, nullptr, nullptr, qf,
                                                               nullptr);
             e = cudaGetLastError();
+        }
+        if (e == cudaSuccess && metric == kAngular) {
+            int32_t zf = 0;
+            QA_TRY(ws.flags.reserve(64), "workspace");
+            int32_t *dflag = (int32_t *)ws.flags.ptr + 2;
+            cudaMemsetAsync(dflag, 0, 4, st);
+            zero_norm_kernel<<<(unsigned)((n + nq + 255) / 256), 256, 0, st>>>(db_norm, n, q_norm,
+                                                                               nq, dflag);
+            cudaMemcpyAsync(&zf, dflag, 4, cudaMemcpyDeviceToHost, st);
+            e = cudaStreamSynchronize(st);
+            if (e == cudaSuccess && zf) {
+                cudaFree(xf);
+                cudaFree(qf);
+                cudaFree(xn);
+                return set_err(QA_EZERONORM, "angular metric needs nonzero corpus and query vectors");
+            }
         }
         if (e == cudaSuccess)
             rc = f32_impl(ws, xf, n, d, d, metric == kAngular ? xn : nullptr, qf, nq, d,

@@ -75,21 +75,10 @@ class Int8Index:
         return dev.encode(q, self.k_dev, self.sb_dev, self.se_dev, self.params.bits, out=out)
 
     def search_codes(self, qc: dev.DeviceCodes, k: int, out=None):
-        if self.metric == Metric.ANGULAR:
-            self._require_positive_norms(qc)
+        """Angular with a zero code norm raises ZeroNorm (checked on the device
+        inside the scan, reference exact.py:67-69)."""
         return dev.scan_topk(self.codes, qc, k, int(self.metric), id_offset=self.id_offset,
                              out=out)
-
-    def _require_positive_norms(self, qc: dev.DeviceCodes) -> None:
-        """Angular needs strictly positive code norms (reference exact.py:67-69
-        raises ZeroNorm before scanning).  The corpus check runs once."""
-        from .errors import ZeroNorm
-        if not getattr(self, "_corpus_norms_ok", False):
-            if self.codes.n and bool((self.codes.sqnorm <= 0).any()):
-                raise ZeroNorm("angular metric needs nonzero corpus vectors")
-            object.__setattr__(self, "_corpus_norms_ok", True)
-        if qc.n and bool((qc.sqnorm <= 0).any()):
-            raise ZeroNorm("angular metric needs nonzero query vectors")
 
     def search(self, q: torch.Tensor, k: int):
         """fp32 query batch on the device -> (scores f64, ids i32) on the device."""
