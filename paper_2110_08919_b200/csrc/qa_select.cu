@@ -455,20 +455,29 @@ __global__ void __launch_bounds__(256, QA_SEL_MINB) select_reg_kernel(SelectArgs
         if (lane == 0 && a.cand_count) atomicAdd(a.cand_count, (unsigned long long)nvalid);
     }
     if (wpq > 1) {
-        // merge the group's lists into its first warp
+        // merge the group's lists into its first warp: a pairwise tree
+        // (log2 wpq levels; at each level warp wq merges warp wq + step's
+        // list), not a chain -- the merges are serial shuffle networks
         __syncwarp();
 #pragma unroll
         for (int e = 0; e < 4; ++e) stage[e * 32 + lane] = t[e];
         if (lane == 0) reinterpret_cast<int *>(stage + 128)[0] = cur;
-        __syncthreads();
-        if (active && wq == 0) {
-            for (int w = 1; w < wpq; ++w) {
-                const K *o = stage_all[warp + w];
+        for (int step = 1; step < wpq; step <<= 1) {
+            __syncthreads();  // this level's lists are written
+            const bool merger = active && (wq % (2 * step)) == 0;
+            if (merger) {
+                const K *o = stage_all[warp + step];
                 K s[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) s[e] = o[e * 32 + lane];
                 rmerge128(t, s);
                 cur = min(k, cur + reinterpret_cast<const int *>(o + 128)[0]);
+            }
+            __syncthreads();  // every read of this level is done
+            if (merger && 2 * step < wpq) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) stage[e * 32 + lane] = t[e];
+                if (lane == 0) reinterpret_cast<int *>(stage + 128)[0] = cur;
             }
         }
     }
