@@ -288,25 +288,25 @@ __device__ __forceinline__ RKey96 rbcast(const RKey96 &a, int src) {
     return RKey96{__shfl_sync(0xffffffffu, a.k, src), __shfl_sync(0xffffffffu, a.id, src)};
 }
 
-// element i of x[4] (i = e*32 + lane), broadcast to the whole warp
-template <typename K>
-__device__ __forceinline__ K rget(const K (&x)[4], int i) {
+// element i of x[R] (i = e*32 + lane), broadcast to the whole warp
+template <typename K, int R>
+__device__ __forceinline__ K rget(const K (&x)[R], int i) {
     K v = x[0];
 #pragma unroll
-    for (int e = 1; e < 4; ++e) v = rsel((i >> 5) == e, x[e], v);
+    for (int e = 1; e < R; ++e) v = rsel((i >> 5) == e, x[e], v);
     return rbcast(v, i & 31);
 }
 
-// one compare-exchange stage over x[4] (i = e*32 + lane) for (size, stride)
-template <typename K>
-__device__ __forceinline__ void rstage(K (&x)[4], int size, int stride) {
+// one compare-exchange stage over x[R] (i = e*32 + lane) for (size, stride)
+template <typename K, int R>
+__device__ __forceinline__ void rstage(K (&x)[R], int size, int stride) {
     const int lane = threadIdx.x & 31;
     if (stride >= 32) {
         const int es = stride >> 5;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
+        for (int e = 0; e < R; ++e) {
             const int p = e ^ es;
-            if (p > e) {
+            if (p > e && p < R) {
                 const bool up = (((e * 32 + lane) & size) == 0);
                 const bool sw = up ? rlt(x[p], x[e]) : rlt(x[e], x[p]);
                 const K lo = rsel(sw, x[p], x[e]);
@@ -318,7 +318,7 @@ __device__ __forceinline__ void rstage(K (&x)[4], int size, int stride) {
     } else {
         const bool lower = (lane & stride) == 0;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
+        for (int e = 0; e < R; ++e) {
             const bool up = (((e * 32 + lane) & size) == 0);
             const K o = rshfl(x[e], stride);
             // the lower index of an ascending pair keeps the min
@@ -328,29 +328,29 @@ __device__ __forceinline__ void rstage(K (&x)[4], int size, int stride) {
     }
 }
 
-template <typename K>
-__device__ __forceinline__ void rsort128(K (&x)[4]) {
+template <typename K, int R>
+__device__ __forceinline__ void rsort(K (&x)[R]) {
 #pragma unroll
-    for (int size = 2; size <= 128; size <<= 1)
+    for (int size = 2; size <= 32 * R; size <<= 1)
 #pragma unroll
         for (int stride = size >> 1; stride > 0; stride >>= 1) rstage(x, size, stride);
 }
 
-// S (sorted ascending, 128) merged into T (sorted ascending, 128): T keeps
-// the 128 smallest of both, sorted.
-template <typename K>
-__device__ __forceinline__ void rmerge128(K (&t)[4], const K (&s)[4]) {
-    // reverse S (i -> 127 - i): lane -> 31 - lane, e -> 3 - e
-    K r[4];
+// S (sorted ascending, W = 32R) merged into T (sorted ascending, W): T keeps
+// the W smallest of both, sorted.
+template <typename K, int R>
+__device__ __forceinline__ void rmerge(K (&t)[R], const K (&s)[R]) {
+    // reverse S (i -> W-1-i): lane -> 31 - lane, e -> R-1-e
+    K r[R];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) r[e] = rshfl(s[3 - e], 31);
-    // stride-128 step of the bitonic merge: T keeps the 128 smallest
+    for (int e = 0; e < R; ++e) r[e] = rshfl(s[R - 1 - e], 31);
+    // stride-W step of the bitonic merge: T keeps the W smallest
 #pragma unroll
-    for (int e = 0; e < 4; ++e) t[e] = rsel(rlt(r[e], t[e]), r[e], t[e]);
-    // t is bitonic now: finish the merge with strides 64..1 (size 128,
-    // ascending everywhere)
+    for (int e = 0; e < R; ++e) t[e] = rsel(rlt(r[e], t[e]), r[e], t[e]);
+    // t is bitonic now: finish the merge with strides W/2..1 (ascending
+    // everywhere: size 2W)
 #pragma unroll
-    for (int stride = 64; stride > 0; stride >>= 1) rstage(t, 256, stride);
+    for (int stride = 16 * R; stride > 0; stride >>= 1) rstage(t, 64 * R, stride);
 }
 
 // wpq warps per query (1, 2, 4 or 8; a block = 8 warps): with few queries
@@ -359,8 +359,9 @@ __device__ __forceinline__ void rmerge128(K (&t)[4], const K (&s)[4]) {
 // the group's lists are merged through shared memory at the end.  One warp
 // per query is latency-bound on its candidate stream when few warps are
 // resident.
-template <int M, typename K>
+template <int M, typename K, int R>
 __global__ void __launch_bounds__(256, QA_SEL_MINB) select_reg_kernel(SelectArgs a, int wpq) {
+    constexpr int W = 32 * R;  // retained-list / chunk width (k <= W)
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int wq = warp % wpq;  // this warp's part of its query
@@ -369,9 +370,9 @@ __global__ void __launch_bounds__(256, QA_SEL_MINB) select_reg_kernel(SelectArgs
     K *stage = stage_all[warp];
     const bool active = q < a.nq && a.ccount[q] > 0;
     const int k = (int)a.k;
-    K t[4];
+    K t[R];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) rsentinel(t[e]);
+    for (int e = 0; e < R; ++e) rsentinel(t[e]);
     int cur = 0;
     int32_t qq = 0;
     float qn = 1.0f;
@@ -390,7 +391,7 @@ __global__ void __launch_bounds__(256, QA_SEL_MINB) select_reg_kernel(SelectArgs
         const int scur = a.state_cnt[q];
         cur = wq == 0 ? scur : 0;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
+        for (int e = 0; e < R; ++e) {
             const int i = e * 32 + lane;
             if (i < cur)
                 to_key<M>(st[i], t[e]);
@@ -430,23 +431,23 @@ __global__ void __launch_bounds__(256, QA_SEL_MINB) select_reg_kernel(SelectArgs
             if (keep) stage[fill + __popc(bal & ((1u << lane) - 1))] = key;
             fill += __popc(bal);
             const bool last = pos + stride >= m;
-            while (fill >= 128 || (last && fill > 0)) {
+            while (fill >= W || (last && fill > 0)) {
                 __syncwarp();
-                const int ns = min(fill, 128);
-                K s[4];
+                const int ns = min(fill, W);
+                K s[R];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
+                for (int e = 0; e < R; ++e) {
                     if (e * 32 + lane < ns)
                         s[e] = stage[e * 32 + lane];
                     else
                         rsentinel(s[e]);
                 }
                 __syncwarp();
-                if (fill > 128 && lane < fill - 128) stage[lane] = stage[128 + lane];
+                if (fill > W && lane < fill - W) stage[lane] = stage[W + lane];
                 fill -= ns;
                 __syncwarp();
-                rsort128(s);
-                rmerge128(t, s);
+                rsort(s);
+                rmerge(t, s);
                 cur = min(k, cur + ns);
                 const K kk = rget(t, k - 1);
                 kth = rsel(rlt(kk, kth), kk, kth);
@@ -460,30 +461,30 @@ __global__ void __launch_bounds__(256, QA_SEL_MINB) select_reg_kernel(SelectArgs
         // list), not a chain -- the merges are serial shuffle networks
         __syncwarp();
 #pragma unroll
-        for (int e = 0; e < 4; ++e) stage[e * 32 + lane] = t[e];
-        if (lane == 0) reinterpret_cast<int *>(stage + 128)[0] = cur;
+        for (int e = 0; e < R; ++e) stage[e * 32 + lane] = t[e];
+        if (lane == 0) reinterpret_cast<int *>(stage + W)[0] = cur;
         for (int step = 1; step < wpq; step <<= 1) {
             __syncthreads();  // this level's lists are written
             const bool merger = active && (wq % (2 * step)) == 0;
             if (merger) {
                 const K *o = stage_all[warp + step];
-                K s[4];
+                K s[R];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) s[e] = o[e * 32 + lane];
-                rmerge128(t, s);
-                cur = min(k, cur + reinterpret_cast<const int *>(o + 128)[0]);
+                for (int e = 0; e < R; ++e) s[e] = o[e * 32 + lane];
+                rmerge(t, s);
+                cur = min(k, cur + reinterpret_cast<const int *>(o + W)[0]);
             }
             __syncthreads();  // every read of this level is done
             if (merger && 2 * step < wpq) {
 #pragma unroll
-                for (int e = 0; e < 4; ++e) stage[e * 32 + lane] = t[e];
-                if (lane == 0) reinterpret_cast<int *>(stage + 128)[0] = cur;
+                for (int e = 0; e < R; ++e) stage[e * 32 + lane] = t[e];
+                if (lane == 0) reinterpret_cast<int *>(stage + W)[0] = cur;
             }
         }
     }
     if (!active || wq != 0) return;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < R; ++e) {
         const int i = e * 32 + lane;
         if (i < cur) st[i] = from_key(t[e]);
     }
@@ -600,10 +601,19 @@ cudaError_t launch_select_t(const SelectArgs &a, cudaStream_t st) {
         while (wpq < 8 && a.nq * wpq * 2 <= slots) wpq *= 2;
         if (const char *v = getenv("QA_B200_SEL_WPQ")) wpq = atoi(v);  // diagnostics
         const unsigned grid = (unsigned)((a.nq + (8 / wpq) - 1) / (8 / wpq));
-        if constexpr (M == kAngular)
-            select_reg_kernel<M, RKey96><<<grid, 256, 0, st>>>(a, wpq);
-        else
-            select_reg_kernel<M, RKey64><<<grid, 256, 0, st>>>(a, wpq);
+        // k <= 32: one register per lane (32-wide sort networks, ~8x fewer
+        // instructions than the 128-wide ones)
+        if (a.k <= 32) {
+            if constexpr (M == kAngular)
+                select_reg_kernel<M, RKey96, 1><<<grid, 256, 0, st>>>(a, wpq);
+            else
+                select_reg_kernel<M, RKey64, 1><<<grid, 256, 0, st>>>(a, wpq);
+        } else {
+            if constexpr (M == kAngular)
+                select_reg_kernel<M, RKey96, 4><<<grid, 256, 0, st>>>(a, wpq);
+            else
+                select_reg_kernel<M, RKey64, 4><<<grid, 256, 0, st>>>(a, wpq);
+        }
         return cudaGetLastError();
     }
     const int kpad = (int)((a.k + 31) / 32 * 32);

@@ -288,7 +288,11 @@ def run_cfg4(args):
                     "queries_per_s": B / (p50 / 1e3),
                     "roofline": {"bound": "hbm", "achieved_gbs": byts / (p50 / 1e3) / 1e9,
                                  "peak_gbs": hbm, "frac": byts / (p50 / 1e3) / 1e9 / hbm,
-                                 "bytes_per_batch": byts, "peak_source": src},
+                                 "bytes_per_batch": byts, "peak_source": src,
+                                 # the dominant kernel alone: the filter launches
+                                 # (CUDA events around them), same algorithmic bytes
+                                 "filter_kernel_gbs": byts / (st["filter_ms"] / 1e3) / 1e9,
+                                 "filter_kernel_frac": byts / (st["filter_ms"] / 1e3) / 1e9 / hbm},
                     "l2": "database (1.28 GB) > L2; not flushed",
                     "scan_stats": {key: st[key] for key in ("rounds", "launches", "candidates",
                                                             "filter_ms", "select_ms")},
