@@ -315,13 +315,6 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
     int32_t *ccount = (int32_t *)ws.ccount.ptr;
     int32_t *ovf = (int32_t *)ws.ovf.ptr;
     int32_t *flags = (int32_t *)ws.flags.ptr;  // [0] any overflow, [4:6) candidate counter
-    QA_TRY(cudaMemsetAsync(ovf, 0, (size_t)nq * 4, st), "memset");
-    QA_TRY(cudaMemsetAsync(flags, 0, 64, st), "memset");
-    if (metric == kAngular) {
-        zero_norm_kernel<<<(unsigned)((n + nq + 255) / 256), 256, 0, st>>>(db_norm, n, q_norm, nq,
-                                                                           flags + 2);
-        QA_TRY(cudaGetLastError(), "norm check");
-    }
     const bool simt = use_simt_filter(ld);
     // norm range of every 128-row tile (per-unit filter bounds)
     const int64_t groups = (n + 127) / 128;
@@ -333,8 +326,17 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
     unsigned long long trace_prev = 0;
     for (int64_t c0 = 0; c0 < nq; c0 += qc) {
         const int64_t m = std::min(qc, nq - c0);
-        QA_TRY(launch_init_state(state_cnt, thr, m, metric, st), "init");
+        // state, thresholds, this chunk's overflow flags and (chunk 0) the
+        // search flags in one launch
+        QA_TRY(launch_init_state_full(state_cnt, thr, m, metric, ovf + c0, c0 == 0 ? flags : nullptr,
+                                      st),
+               "init");
         g_stats.launches += 1;
+        if (c0 == 0 && metric == kAngular) {
+            zero_norm_kernel<<<(unsigned)((n + nq + 255) / 256), 256, 0, st>>>(db_norm, n, q_norm,
+                                                                               nq, flags + 2);
+            QA_TRY(cudaGetLastError(), "norm check");
+        }
         int64_t r_lo = 0, r_hi = pl.r0;
         bool first = true, estimated = false;
         int64_t cur_j = 0;  // estimate rank of the pass in flight (0: k-th bound)
@@ -400,6 +402,22 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             sa.overflow = ovf + c0;
             sa.any_overflow = flags;
             sa.cand_count = reinterpret_cast<unsigned long long *>(flags + 4);
+            // the estimate that follows this round (if any) runs inside the
+            // select when the register select serves k
+            int64_t est_now = 0;
+            int est_comb = 0;
+            if (r_hi < n) {
+                if (pl.est1_j > 0 && first && r_hi < pl.est_rows) {
+                    est_now = pl.est1_j;
+                } else if (pl.est_rows > 0 && r_hi >= pl.est_rows) {
+                    est_now = pl.est_j;
+                    est_comb = estimated ? 1 : 0;
+                }
+            }
+            const bool est_fused = est_now > 0 && keff <= 128;
+            sa.est_j = est_fused ? est_now : 0;
+            sa.est = est;
+            sa.est_combine = est_comb;
             g_timer.begin(1, st);
             QA_TRY(launch_select(sa, st), "select");
             g_timer.end(st);
@@ -419,11 +437,13 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             if (pl.est1_j > 0 && first && r_hi < pl.est_rows) {
                 // one pass over the rest of the prefix with round 0's
                 // est1_j-th best as the bound
-                QA_TRY(launch_estimate(state, state_cnt, thr, est, m, keff, pl.est1_j, metric,
-                                       q_sqnorm ? q_sqnorm + c0 : nullptr,
-                                       q_norm ? q_norm + c0 : nullptr, false, st),
-                       "estimate");
-                g_stats.launches += 1;
+                if (!est_fused) {
+                    QA_TRY(launch_estimate(state, state_cnt, thr, est, m, keff, pl.est1_j, metric,
+                                           q_sqnorm ? q_sqnorm + c0 : nullptr,
+                                           q_norm ? q_norm + c0 : nullptr, false, st),
+                           "estimate");
+                    g_stats.launches += 1;
+                }
                 estimated = true;
                 cur_j = pl.est1_j;
                 first = false;
@@ -434,11 +454,13 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             if (pl.est_rows > 0 && r_hi >= pl.est_rows) {
                 // one pass over the rest with the estimated bound
                 cur_j = pl.est_j;
-                QA_TRY(launch_estimate(state, state_cnt, thr, est, m, keff, pl.est_j, metric,
-                                       q_sqnorm ? q_sqnorm + c0 : nullptr,
-                                       q_norm ? q_norm + c0 : nullptr, estimated, st),
-                       "estimate");
-                g_stats.launches += 1;
+                if (!est_fused) {
+                    QA_TRY(launch_estimate(state, state_cnt, thr, est, m, keff, pl.est_j, metric,
+                                           q_sqnorm ? q_sqnorm + c0 : nullptr,
+                                           q_norm ? q_norm + c0 : nullptr, estimated, st),
+                           "estimate");
+                    g_stats.launches += 1;
+                }
                 estimated = true;
                 r_hi = n;
             } else {
@@ -448,14 +470,11 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
                 if (pl.est_rows > 0 && r_lo < pl.est_rows) r_hi = std::min(r_hi, pl.est_rows);
             }
         }
-        if (estimated) {
-            // queries whose k-th score fell short of the estimate are redone
-            QA_TRY(launch_check_estimate(state, state_cnt, est, m, keff, ovf + c0, flags, st),
-                   "estimate check");
-            g_stats.launches += 1;
-        }
+        // results, and (estimated plans) the check that queries whose k-th
+        // score fell short of an estimate are redone
         QA_TRY(launch_finalize(state, m, keff, keff, metric, id_offset, out_scores + c0 * keff,
-                               out_ids + c0 * keff, st),
+                               out_ids + c0 * keff, st, state_cnt, estimated ? est : nullptr,
+                               ovf + c0, flags),
                "finalize");
         g_stats.launches += 1;
     }

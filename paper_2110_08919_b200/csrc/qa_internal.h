@@ -78,6 +78,12 @@ struct SelectArgs {
     int32_t *overflow;   // [nq] sticky per-query flag: candidate list overflowed
     int32_t *any_overflow;
     unsigned long long *cand_count;  // statistics: valid candidates seen (may be NULL)
+    // fused threshold estimate (0 = none; the register select only): after
+    // the merge, thr := threshold of the est_j-th kept entry and est[q] := its
+    // order key (with est_combine, the tighter of that and the previous one)
+    int64_t est_j = 0;
+    unsigned long long *est = nullptr;
+    int est_combine = 0;
 };
 
 cudaError_t launch_select(const SelectArgs &a, cudaStream_t st);
@@ -94,9 +100,16 @@ cudaError_t launch_estimate(const Entry *state, const int32_t *state_cnt, int32_
 cudaError_t launch_check_estimate(const Entry *state, const int32_t *state_cnt,
                                   const unsigned long long *est, int64_t nq, int64_t k,
                                   int32_t *redo, int32_t *any_redo, cudaStream_t st);
+// est != NULL: also the estimate check of launch_check_estimate (fused)
 cudaError_t launch_finalize(const Entry *state, int64_t nq, int64_t k, int64_t keff, int metric,
                             int64_t id_offset, double *out_scores, int32_t *out_ids,
-                            cudaStream_t st);
+                            cudaStream_t st, const int32_t *state_cnt = nullptr,
+                            const unsigned long long *est = nullptr, int32_t *redo = nullptr,
+                            int32_t *any_redo = nullptr);
+// state_cnt := 0, thr := pass-all for nq queries; also zeroes ovf[nq] and
+// flags[16] when given (fused memsets)
+cudaError_t launch_init_state_full(int32_t *state_cnt, int32_t *thr, int64_t nq, int metric,
+                                   int32_t *ovf, int32_t *flags, cudaStream_t st);
 // Norm range of every 32-row group, padded to `groups` entries (groups past
 // n never pass a filter bound).
 cudaError_t launch_group_ranges(int metric, const int32_t *sqnorm, const float *norm, int64_t n,

