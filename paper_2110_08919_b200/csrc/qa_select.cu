@@ -646,6 +646,11 @@ cudaError_t launch_select_t(const SelectArgs &a, cudaStream_t st) {
                 select_reg_kernel<M, RKey96, 1><<<grid, 256, 0, st>>>(a, wpq);
             else
                 select_reg_kernel<M, RKey64, 1><<<grid, 256, 0, st>>>(a, wpq);
+        } else if (a.k <= 64) {
+            if constexpr (M == kAngular)
+                select_reg_kernel<M, RKey96, 2><<<grid, 256, 0, st>>>(a, wpq);
+            else
+                select_reg_kernel<M, RKey64, 2><<<grid, 256, 0, st>>>(a, wpq);
         } else {
             if constexpr (M == kAngular)
                 select_reg_kernel<M, RKey96, 4><<<grid, 256, 0, st>>>(a, wpq);

@@ -165,7 +165,7 @@ def test_self_query_property():
 
 
 @pytest.mark.parametrize("metric", [0, 1, 2])
-@pytest.mark.parametrize("k", [1, 10, 100, 1000])
+@pytest.mark.parametrize("k", [1, 10, 32, 33, 64, 65, 100, 128, 129, 1000])
 def test_scan_mid_size_vs_oracle(oracle, metric, k):
     rng = np.random.default_rng(10 * metric + k)
     X = _rand_codes(rng, 20_000, 96, nonzero=True)
