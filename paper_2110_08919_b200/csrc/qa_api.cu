@@ -329,7 +329,7 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
         // state, thresholds, this chunk's overflow flags and (chunk 0) the
         // search flags in one launch
         QA_TRY(launch_init_state_full(state_cnt, thr, m, metric, ovf + c0, c0 == 0 ? flags : nullptr,
-                                      st),
+                                      ccount, (int32_t)std::min(n, pl.r0), st),
                "init");
         g_stats.launches += 1;
         if (c0 == 0 && metric == kAngular) {
@@ -339,6 +339,7 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
         }
         int64_t r_lo = 0, r_hi = pl.r0;
         bool first = true, estimated = false;
+        bool counts_preset = true;  // init set round 0's (dense) counts
         int64_t cur_j = 0;  // estimate rank of the pass in flight (0: k-th bound)
         for (;;) {
             FilterArgs fa;
@@ -375,7 +376,12 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             // final pass admits ~est_j per prefix-sized slice
             fa.exp_cands = cur_j ? (double)cur_j * (double)(r_hi - r_lo) / (double)r_lo
                                      : (double)keff * (double)(r_hi - r_lo) / (double)std::max<int64_t>(r_lo, 1);
-            QA_TRY(launch_fill(ccount, m, mode != 0 ? (int32_t)(r_hi - r_lo) : 0, st), "fill");
+            // candidate counts of this round: preset by init (round 0) or by
+            // the previous round's register select; otherwise here
+            if (!counts_preset) {
+                QA_TRY(launch_fill(ccount, m, mode != 0 ? (int32_t)(r_hi - r_lo) : 0, st), "fill");
+                g_stats.launches += 1;
+            }
             cudaError_t e = cudaErrorNotSupported;
             g_timer.begin(0, st);
             if (!simt) e = launch_filter_tc(fa, st);
@@ -418,10 +424,30 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             sa.est_j = est_fused ? est_now : 0;
             sa.est = est;
             sa.est_combine = est_comb;
+            // the next round's rows (and so its candidate-count preset, which
+            // the register select writes when it is done with this round's)
+            int64_t next_hi = n;
+            if (r_hi < n) {
+                if (pl.est1_j > 0 && first && r_hi < pl.est_rows) {
+                    next_hi = pl.est_rows;
+                } else if (pl.est_rows > 0 && r_hi >= pl.est_rows) {
+                    next_hi = n;
+                } else {
+                    next_hi = std::min(n, round_up(r_hi * pl.ratio, 128));
+                    if (pl.est_rows > 0 && r_hi < pl.est_rows)
+                        next_hi = std::min(next_hi, pl.est_rows);
+                }
+            }
+            const bool next_masked = (next_hi - r_hi) <= std::min<int64_t>(pl.cap, masked_max);
+            const int32_t next_fill = next_masked ? (int32_t)(next_hi - r_hi) : 0;
+            const bool fill_fused = keff <= 128 && r_hi < n;
+            sa.next_fill = fill_fused ? next_fill : -1;
+            sa.ccount_reset = ccount;
             g_timer.begin(1, st);
             QA_TRY(launch_select(sa, st), "select");
             g_timer.end(st);
-            g_stats.launches += 3;
+            counts_preset = fill_fused;
+            g_stats.launches += 2;  // filter + select
             g_stats.rounds += 1;
             if (trace_enabled()) {  // diagnostics: per-round survivors (synchronises)
                 unsigned long long cnt = 0;

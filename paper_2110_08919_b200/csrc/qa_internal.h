@@ -84,6 +84,10 @@ struct SelectArgs {
     int64_t est_j = 0;
     unsigned long long *est = nullptr;
     int est_combine = 0;
+    // fused fill (register select only): ccount_reset[q] := next_fill once the
+    // round's candidates are consumed (-1 = leave)
+    int32_t next_fill = -1;
+    int32_t *ccount_reset = nullptr;
 };
 
 cudaError_t launch_select(const SelectArgs &a, cudaStream_t st);
@@ -109,7 +113,8 @@ cudaError_t launch_finalize(const Entry *state, int64_t nq, int64_t k, int64_t k
 // state_cnt := 0, thr := pass-all for nq queries; also zeroes ovf[nq] and
 // flags[16] when given (fused memsets)
 cudaError_t launch_init_state_full(int32_t *state_cnt, int32_t *thr, int64_t nq, int metric,
-                                   int32_t *ovf, int32_t *flags, cudaStream_t st);
+                                   int32_t *ovf, int32_t *flags, int32_t *ccount, int32_t fill0,
+                                   cudaStream_t st);
 // Norm range of every 32-row group, padded to `groups` entries (groups past
 // n never pass a filter bound).
 cudaError_t launch_group_ranges(int metric, const int32_t *sqnorm, const float *norm, int64_t n,

@@ -483,6 +483,7 @@ __global__ void __launch_bounds__(256, QA_SEL_MINB) select_reg_kernel(SelectArgs
         }
     }
     if (q >= a.nq || wq != 0) return;
+    if (a.next_fill >= 0 && lane == 0) a.ccount_reset[q] = a.next_fill;
     if (active) {
 #pragma unroll
         for (int e = 0; e < R; ++e) {
@@ -528,12 +529,14 @@ __global__ void reset_kernel(int32_t *p, int64_t n, int32_t v) {
 }
 
 __global__ void init_state_kernel(int32_t *state_cnt, int32_t *thr, int64_t nq,
-                                  int32_t pass_all, int32_t *ovf, int32_t *flags) {
+                                  int32_t pass_all, int32_t *ovf, int32_t *flags,
+                                  int32_t *ccount = nullptr, int32_t fill0 = 0) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < nq) {
         state_cnt[i] = 0;
         thr[i] = pass_all;
         if (ovf) ovf[i] = 0;
+        if (ccount) ccount[i] = fill0;
     }
     if (flags && i < 16) flags[i] = 0;
 }
@@ -677,7 +680,10 @@ cudaError_t launch_select_t(const SelectArgs &a, cudaStream_t st) {
 cudaError_t launch_select(const SelectArgs &a_in, cudaStream_t st) {
     if (a_in.nq == 0) return cudaSuccess;
     SelectArgs a = a_in;
-    if (a.k > 128) a.est_j = 0;  // the shared-memory select has no fused estimate
+    if (a.k > 128) {  // the shared-memory select has no fused estimate / fill
+        a.est_j = 0;
+        a.next_fill = -1;
+    }
     switch (a.metric) {
         case kIP: return launch_select_t<kIP>(a, st);
         case kL2: return launch_select_t<kL2>(a, st);
@@ -779,12 +785,13 @@ cudaError_t launch_init_state(int32_t *state_cnt, int32_t *thr, int64_t nq, int 
 }
 
 cudaError_t launch_init_state_full(int32_t *state_cnt, int32_t *thr, int64_t nq, int metric,
-                                   int32_t *ovf, int32_t *flags, cudaStream_t st) {
+                                   int32_t *ovf, int32_t *flags, int32_t *ccount, int32_t fill0,
+                                   cudaStream_t st) {
     int32_t pass = metric == kIP ? kThrPassIP
                                  : (metric == kL2 ? kThrPassL2 : (int32_t)kThrPassAngBits);
     const int64_t m = nq > 16 ? nq : 16;
     init_state_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(state_cnt, thr, nq, pass, ovf,
-                                                                   flags);
+                                                                   flags, ccount, fill0);
     return cudaGetLastError();
 }
 
