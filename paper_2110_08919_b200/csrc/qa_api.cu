@@ -215,6 +215,10 @@ ScanPlan plan_scan(int64_t n, int64_t nq, int64_t keff, int64_t cap_min, bool al
         int64_t P = 32768;
         if (const char *v = getenv("QA_B200_EST_ROWS")) P = atoll(v);
         while (P < 64 * keff) P *= 2;
+        // small indexes (e.g. one GPU's row shard): a smaller prefix rather
+        // than no estimate at all (which costs a doubling round per 2x rows)
+        if (!getenv("QA_B200_EST_ROWS"))
+            while (P > 0 && 4 * P > n && P / 2 >= std::max<int64_t>(64 * keff, 4 * p.r0)) P /= 2;
         if (P > 0 && 4 * P <= n) {
             const double lambda = (double)keff * (double)P / (double)n;
             double tail = 1e-4;
