@@ -68,7 +68,6 @@ constexpr int kBiasWarp = 3;
 constexpr int kEpiWarp0 = 4;
 constexpr int kEpiThreads = 512;
 constexpr int kStageCapDefault = 2048;  // survivors staged in smem per work unit
-constexpr int kEpiBarrier = 1;   // named barrier id for the epilogue warps
 constexpr int kBiasK = 32;       // K of the bias MMA (int8 columns)
 constexpr int kBiasA = 127;      // constant of the bias A tile
 constexpr int kSMin = -128 * kBiasK;  // digit-sum range
@@ -174,7 +173,9 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
 #else
 #define WSTAT(i, stmt) stmt
 #endif
+#ifdef QA_WAIT_STATS
 constexpr int kWst = 16;
+#endif
 
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar,
                                             int32_t c0, int32_t c1) {
@@ -216,17 +217,6 @@ __device__ __forceinline__ void tc_commit(uint64_t *bar) {
         : "memory");
 }
 
-__device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                          uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t"
-        ".reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
-        "}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
 
 // One K chunk of a tile, issued by one elected lane of a converged warp:
 // KSTEPS MMAs of K=32 bytes (descriptor start addresses step by 32 B = 2 in
@@ -366,9 +356,6 @@ __device__ __forceinline__ int32_t lds32(uint32_t addr) {
     return r;
 }
 
-__device__ __forceinline__ void epi_barrier() {
-    asm volatile("bar.sync %0, %1;" ::"n"(kEpiBarrier), "n"(kEpiThreads) : "memory");
-}
 
 // UMMA shared-memory descriptor, K-major, swizzle SW bytes (32/64/128):
 // start>>4 [0,14), LBO>>4 [16,30) (unused for swizzled K-major: 1),
@@ -387,10 +374,6 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
 __host__ __device__ constexpr uint32_t make_idesc(int N) {
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
            ((uint32_t)(kBlockM >> 4) << 24);
-}
-
-__device__ __forceinline__ int32_t clamp_i64(long long v) {
-    return v > INT32_MAX ? INT32_MAX : (v < INT32_MIN ? INT32_MIN : (int32_t)v);
 }
 
 // 1 when any of v[0..C) is >= 0: sign bit of the AND of all values
