@@ -53,16 +53,22 @@ namespace qa {
 namespace {
 
 constexpr int kBlockM = 128;
-// Exact threshold test of bias-bound survivors in the epilogue.  Off: the
-// bias bound alone decides (it admits ~3 % more candidates on cfg1) and the
-// select kernel, which scores every candidate exactly anyway, drops them;
-// the survivor path gets shorter (-0.1 ms / step).  -DQA_EXACT_IN_EPILOGUE
-// restores it.
-#ifdef QA_EXACT_IN_EPILOGUE
-constexpr bool kExactInEpilogue = true;
+// Exact threshold test of bias-bound survivors in the epilogue, per metric.
+// Angular and IP: off -- the bias bound alone decides (angular admits ~5 %
+// more candidates on cfg1), the select scores every candidate exactly
+// anyway, and the shorter survivor path wins (exact test: -3 % on cfg1, -2 %
+// on cfg3).  L2: on -- its bound carries the bias granularity (127 x reps,
+// reps ~3 for SIFT-like codes) and the unit's smallest norm; on cfg2 it
+// admitted 57 % more than the exact test (627k vs 398k per 1024-query pass)
+// and the exact test is +24 % q/s.  -DQA_EXACT_IN_EPILOGUE=0/1 forces it.
+template <int M>
+__host__ __device__ constexpr bool exact_epi() {
+#if defined(QA_EXACT_IN_EPILOGUE)
+    return QA_EXACT_IN_EPILOGUE != 0;
 #else
-constexpr bool kExactInEpilogue = false;
+    return M == kL2;
 #endif
+}
 constexpr int kThreads = 640;
 constexpr int kBiasWarp = 3;
 constexpr int kEpiWarp0 = 4;
@@ -460,6 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     Staged *stage_all = (Staged *)(sBbias + 2 * N * kBiasK);        // [2][stage_cap]
     // row norms of the unit (L2: sqnorm, angular: float bits), staged by the
     // bias warp for the exact test
+    constexpr bool kExactInEpilogue = exact_epi<M>();
     constexpr int kNormSlots = (M == kIP || !kExactInEpilogue) ? 0 : 2;
     int32_t *norm_all = (int32_t *)(stage_all + 2 * stage_cap);     // [2][kUnitRowsMax]
     int32_t *thr_all = norm_all + kNormSlots * kUnitRowsMax;        // [2][N] thresholds
@@ -1271,7 +1278,7 @@ cudaError_t launch_t(const FilterArgs &a, cudaStream_t st) {
     const size_t fixed = 1024 /*align slack*/ + (size_t)p.b_slots * N * a.kdim +
                          kBlockM * kBiasK + 2 * (size_t)N * kBiasK +
                          2 * (size_t)p.stage_cap * sizeof(Staged) +
-                         (M == kIP || !kExactInEpilogue ? 0 : 2 * (size_t)kUnitRowsMax * sizeof(int32_t)) +
+                         (M == kIP || !exact_epi<M>() ? 0 : 2 * (size_t)kUnitRowsMax * sizeof(int32_t)) +
                          (9 * N + 2 * (N / 32)) * sizeof(int32_t) + 512;
     const size_t budget = 227 * 1024;
     const size_t stage_bytes = (size_t)kBlockM * SW;
