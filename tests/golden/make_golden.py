@@ -263,6 +263,35 @@ def stats_cases():
     return len(cases)
 
 
+def gate4_case():
+    """The reference's acceptance gate 4 pipeline (test_acceptance.py:176-193,
+    synthetic corpus): float32 ground truth, estimate_stats -> fit(ABS_MAX)
+    -> quantize_dataset -> int8 ground truth, recall@100 -- run by the
+    reference (compiled backend) and stored for an end-to-end GPU check."""
+    import importlib
+    sys.path.insert(0, str(REF_SRC))
+    import quantann
+    from quantann import (DenseDataset, Metric, QuantMode, batch_ground_truth, estimate_stats,
+                          fit, generate_synthetic, quantize_dataset, recall_at_k)
+    # the compiled kernels from oracle/_ref stand in for the package's own build
+    core = load_reference()[1]
+    import quantann._backend as be
+    be.scan_topk, be.norms, be.BACKEND = core.scan_topk, core.norms, core.BACKEND
+    import quantann.exact as ex
+    importlib.reload(ex)
+    corpus = generate_synthetic(50_000, 64, 0.0, 0.05, 2)
+    queries = generate_synthetic(100, 64, 0.0, 0.05, 1002)
+    gt = ex.batch_ground_truth(corpus, queries, 100, Metric.INNER_PRODUCT)
+    params = fit(estimate_stats(corpus), 8, QuantMode.ABS_MAX).params
+    ci8 = quantize_dataset(corpus, params)
+    qi8 = quantize_dataset(queries, params)
+    approx = ex.batch_ground_truth(ci8, qi8, 100, Metric.INNER_PRODUCT)
+    rec = recall_at_k(gt, approx, 100).mean
+    np.savez_compressed(OUT / "gate4.npz", gt=gt.ids, approx=approx.ids, recall=np.float64(rec),
+                        k=params.k, sb=params.sb, se=params.se)
+    return rec
+
+
 def cfg_minis(qa, core):
     """BASELINE cfg0 (L2, min/max) and cfg1 (angular, symmetric) at reduced
     size through the reference pipeline: constructed stats -> fit(ABS_MAX)
@@ -308,12 +337,13 @@ def main():
     if len(sys.argv) > 1:   # regenerate only the named fixtures, e.g. scan_f32
         for name in sys.argv[1:]:
             fn = {"encode": lambda: encode_cases(qa), "scan": lambda: scan_cases(core),
-                  "scan_f32": lambda: scan_f32_cases(core), "vecs": vecs_cases, "stats": stats_cases, "cfg": lambda: cfg_minis(qa, core)}[name]
+                  "scan_f32": lambda: scan_f32_cases(core), "vecs": vecs_cases, "stats": stats_cases, "gate4": gate4_case, "cfg": lambda: cfg_minis(qa, core)}[name]
             print(name, fn())
         return
     nf = scan_f32_cases(core)
     vecs_cases()
     stats_cases()
+    gate4_case()
     ne = encode_cases(qa)
     ns = scan_cases(core)
     cfg_minis(qa, core)

@@ -533,3 +533,27 @@ def test_sorted_index_tiny(oracle, n):
         osc, oids = _scan_oracle(oracle, X, Q, 5, 1)
         np.testing.assert_array_equal(ids.cpu().numpy(), oids)
         np.testing.assert_array_equal(sc.cpu().numpy(), osc)
+
+
+def test_acceptance_gate4_pipeline_matches_reference():
+    # The reference's gate 4 (test_acceptance.py:176-193, synthetic corpus),
+    # every step on the GPU: float32 ground truth (float64-exact scan),
+    # estimate_stats -> fit(ABS_MAX) -> quantize_dataset (encode kernel) ->
+    # int8 ground truth (tensor-core scan) -> recall@100.  Ids, windows and
+    # recall equal the reference's own run (tests/golden/gate4.npz).
+    from pathlib import Path
+    g = np.load(Path(__file__).resolve().parent / "golden" / "gate4.npz")
+    corpus = qa.generate_synthetic(50_000, 64, 0.0, 0.05, 2)
+    queries = qa.generate_synthetic(100, 64, 0.0, 0.05, 1002)
+    gt = qa.batch_ground_truth(corpus, queries, 100, qa.Metric.INNER_PRODUCT)
+    np.testing.assert_array_equal(gt.ids, g["gt"])
+    params = qa.fit(qa.estimate_stats(corpus), 8, qa.QuantMode.ABS_MAX).params
+    np.testing.assert_array_equal(params.k, g["k"])
+    np.testing.assert_array_equal(params.sb, g["sb"])
+    np.testing.assert_array_equal(params.se, g["se"])
+    ci8 = qa.quantize_dataset(corpus, params)
+    qi8 = qa.quantize_dataset(queries, params)
+    approx = qa.batch_ground_truth(ci8, qi8, 100, qa.Metric.INNER_PRODUCT)
+    np.testing.assert_array_equal(approx.ids, g["approx"])
+    rec = qa.recall_at_k(gt, approx, 100).mean
+    assert rec == float(g["recall"]) and rec >= 0.95
