@@ -131,3 +131,29 @@ def test_recall_at_k():
         qa.recall_at_k(exp, act[:1], 3)
     with pytest.raises(ValueError):
         qa.recall_at_k(exp, act, 4)
+
+
+def test_acceptance_gate1_quantizer_order_range_reconstruction():
+    # reference test_acceptance.py:77-113 (gate 1), through this package's
+    # scalar quantize_value / dequantize_value
+    rng = np.random.default_rng(11)
+    checked = 0
+    for _ in range(100):
+        bits = int(rng.integers(1, 9))
+        c = np.float32(rng.uniform(-5.0, 5.0))
+        h = np.float32(rng.uniform(1e-3, 5.0))
+        sb, se = np.float32(c - h), np.float32(c + h)
+        k = np.float32((float(sb) + float(se)) / 2.0)
+        p = qa.QuantizerParams(bits=bits, mode=qa.QuantMode.SIGMA_CLAMP, k=np.array([k]),
+                               sb=np.array([sb]), se=np.array([se]))
+        width = float(se) - float(sb)
+        xs = np.sort(rng.uniform(float(c) - 3 * float(h), float(c) + 3 * float(h), size=(100, 2)),
+                     axis=1)
+        for x, y in xs:
+            qx, qy = qa.quantize_value(float(x), 0, p), qa.quantize_value(float(y), 0, p)
+            assert qx <= qy and p.lo_code <= qx <= p.hi_code and p.lo_code <= qy <= p.hi_code
+            checked += 1
+        for x in rng.uniform(float(sb), float(se), size=50):
+            q = qa.quantize_value(float(x), 0, p)
+            assert abs(qa.dequantize_value(q, 0, p) - float(x)) <= width / (1 << bits)
+    assert checked == 10_000
