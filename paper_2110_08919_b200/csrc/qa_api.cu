@@ -326,6 +326,7 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
     int32_t *grp_lo = (int32_t *)ws.grp.ptr, *grp_hi = grp_lo + groups;
     QA_TRY(launch_group_ranges(metric, db_sqnorm, db_norm, n, grp_lo, grp_hi, groups, st),
            "group ranges");
+    if (metric != kIP && groups) g_stats.launches += 1;
 
     unsigned long long trace_prev = 0;
     for (int64_t c0 = 0; c0 < nq; c0 += qc) {
@@ -340,6 +341,7 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             zero_norm_kernel<<<(unsigned)((n + nq + 255) / 256), 256, 0, st>>>(db_norm, n, q_norm,
                                                                                nq, flags + 2);
             QA_TRY(cudaGetLastError(), "norm check");
+            g_stats.launches += 1;
         }
         int64_t r_lo = 0, r_hi = pl.r0;
         bool first = true, estimated = false;
