@@ -1,31 +1,42 @@
-"""Benchmark: int8 exhaustive k=100 search on the BASELINE config-1 workload.
+"""Benchmark: int8 exhaustive k=100 search, BASELINE config 2 by default.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
-                    [--config 1] [--nq 10000] [--n N]
+                    [--config 2] [--n N] [--nq NQ] [--batch B]
 
-Workload (BASELINE.json configs[1], the config the metric is quoted on):
-1,000,000 x 100 fp32 database (GloVe-like generator, rows L2-normalised),
-10,000 queries, symmetric per-dimension int8 quantization, angular
-distance, k = 100.  Synthetic data from paper_2110_08919_b200.synth (seed 1).
+Workload (BASELINE.json configs[2], the config whose text carries the
+metric's "1/2/4/8 B200"): a 1,000,000 x 128 fp32 database (SIFT-like law:
+round(|N(0, 40^2)|) clipped to [0, 255], 10 % zeros), 10,000 queries of the
+same law issued in batches of 1,024, per-dimension min/max int8
+quantization, L2, k = 100.  Seeded synthetic data from ``synth.py`` (the
+public SIFT set is not available offline).
 
-One STEP = one pass of the hot path over the whole 10,000-query set:
-encode the fp32 queries with the corpus window (encode kernel), then the
-tensor-core exhaustive scan with exact top-k (filter + select kernels); the
-int8 database index (codes + norms) is resident in HBM, built once before
-timing.  ``value`` is queries/s with the fp32 queries already in HBM;
-``e2e`` is the same through the host-buffer public path: pinned fp32
-queries -> H2D -> encode -> scan -> D2H of ids + scores, all inside the
-timed region.  L2 is flushed (256 MiB write) before every timed step,
-outside the step's CUDA events.
+One STEP = the whole 10,000-query set, batch after batch: encode the fp32
+batch with the corpus window (encode kernel), then the tensor-core
+exhaustive scan with exact top-k (filter + select kernels).  The int8 index
+(codes + norms, norm-sorted layout) is built once before timing.
 
-N > 1 (torchrun): the database is row-sharded over the ranks, queries are
-replicated, each rank scans its shard and the per-rank top-k lists are
-all-gathered over NCCL and merged on the GPU (``sharded.py``).  Step time =
-max over ranks of the CUDA-event time.
+* ``value``: queries/s with the fp32 queries already in HBM;
+* ``e2e``: the same through the public host-buffer path, per batch: pinned
+  fp32 queries -> H2D -> encode -> scan -> D2H of scores + ids;
+* ``e2e_reference_api``: the reference-shaped API
+  ``batch_ground_truth(corpus, queries, k, metric)`` (reference
+  exact.py:105-117) with host int8 DenseDatasets, per batch; the frozen
+  corpus stays resident on the device between calls.
+
+L2 is flushed (256 MiB write) before every timed step, outside its events.
+
+N > 1 (torchrun): rows are sharded contiguously; each rank generates and
+encodes only its own shard (calibration = NCCL MIN/MAX all-reduce of the
+per-shard ranges, so every rank derives the identical window); queries are
+replicated; per batch each rank scans its shard and the per-rank top-k lists
+are all-gathered over NCCL and merged on the GPU (``sharded.py``).  Step
+time = max over ranks of the CUDA-event time.
 
 ``--impl reference``: the reference's own CPU kernel (quantann._core
 scan_topk compiled from /root/reference into oracle/_ref) on all host cores
-(forked workers over query slices), each step a bounded query sample.
+(forked workers over query slices); each step scans a bounded sample of the
+query set; value = queries scanned / seconds, summed over the timed steps.
+This process never imports the B200 package or loads its library.
 """
 
 from __future__ import annotations
@@ -46,17 +57,19 @@ sys.path.insert(0, str(ROOT))
 METRIC_NAME = "int8 exhaustive k=100 queries/s at 1/2/4/8 B200; % of INT8 TC / HBM roofline"
 PEAKS_PATH = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+MMA_I8_TOPS = 4430.0  # tools/mma_rate.cu on this pool: 128 cycles per M128.N256.K32 kind::i8
 
 
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--nq", type=int, default=None)
+    ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--k", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -69,24 +82,45 @@ def load_peaks():
     return FALLBACK_PEAKS, "fallback (B200_PROFILING.md)"
 
 
-# --------------------------------------------------------------- workload --
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-def make_workload(cfg: int, n: int | None, nq: int | None):
-    from paper_2110_08919_b200 import synth
 
-    c = dict(synth.CONFIGS[cfg])
-    X, Q = synth.generate(cfg, n=n, nq=nq)
-    c["n"], c["nq"] = X.shape[0], Q.shape[0]
-    return c, X, Q
+def workload(args):
+    import synth
+
+    c = dict(synth.CONFIGS[args.config])
+    if args.n is not None:
+        c["n"] = args.n
+    if args.nq is not None:
+        c["nq"] = args.nq
+    if args.batch is not None:
+        c["batch"] = args.batch
+    c["batch"] = min(c["batch"], c["nq"])
+    return c
 
 
 def workload_desc(c, k):
     metric = ("ip", "l2", "angular")[c["metric"]]
     return (f"{c['name']}: {c['n']}x{c['d']} fp32 db -> int8 ({c['calibration']}), "
-            f"{c['nq']} queries, {metric}, k={k}")
+            f"{c['nq']} queries in batches of {c['batch']}, {metric}, k={k}")
+
+
+def batches(nq, B):
+    return [(lo, min(nq, lo + B)) for lo in range(0, nq, B)]
 
 
 # ---------------------------------------------------------- CPU reference --
+#
+# Only numpy, the C oracle (setup: the encode the reference's numpy
+# quantizer performs, quantizer.py:291-300) and the reference's own compiled
+# _core are used here -- never the B200 package.
 
 _REF = {}
 
@@ -94,17 +128,16 @@ _REF = {}
 def _ref_worker(span):
     lo, hi = span
     qn = _REF["qn"][lo:hi] if _REF["qn"] is not None else None
-    _REF["core"].scan_topk(_REF["Xc"], _REF["Qc"][lo:hi], _REF["k"], _REF["metric"], _REF["xn"],
-                           qn)
+    _REF["core"].scan_topk(_REF["Xc"], _REF["Qc"][lo:hi], _REF["k"], _REF["metric"], _REF["xn"], qn)
     return hi - lo
 
 
 class CpuReference:
     """The reference's compiled kernel (quantann._core.scan_topk, built from
-    /root/reference into oracle/_ref) on all host cores: one forked worker
-    per core, each scanning a contiguous query slice of the sample."""
+    /root/reference into oracle/_ref) on `procs` host cores: one forked
+    worker per core, each scanning a contiguous query slice."""
 
-    def __init__(self, c, X, Q, k):
+    def __init__(self, c, X, Q, k, procs):
         import multiprocessing as mp
 
         from oracle import qa_oracle as o
@@ -124,35 +157,55 @@ class CpuReference:
                     xn=core.norms(Xc) if metric == 2 else None,
                     qn=core.norms(Qc) if metric == 2 else None)
         self.nq = Qc.shape[0]
-        self.cores = os.cpu_count() or 1
-        self.pool = mp.get_context("fork").Pool(self.cores)
+        self.procs = procs
+        self.pool = mp.get_context("fork").Pool(procs) if procs > 1 else None
         self.cursor = 0
 
-    def step(self, sample: int) -> float:
-        """Scan `sample` queries (rotating through the query set) on all
-        cores; returns wall seconds."""
-        lo = self.cursor % self.nq
+    def step(self, sample: int) -> tuple[int, float]:
+        """Scan `sample` queries (a contiguous slice, rotating through the
+        query set); returns (queries scanned, wall seconds)."""
+        lo = self.cursor
         hi = min(self.nq, lo + sample)
-        self.cursor = hi
-        per = -(-(hi - lo) // self.cores)
-        spans = [(i, min(hi, i + per)) for i in range(lo, hi, per)]
+        self.cursor = 0 if hi >= self.nq else hi
         t0 = time.perf_counter()
-        done = sum(self.pool.map(_ref_worker, spans))
+        if self.pool is None:
+            done = _ref_worker((lo, hi))
+        else:
+            per = -(-(hi - lo) // self.procs)
+            spans = [(i, min(hi, i + per)) for i in range(lo, hi, per)]
+            done = sum(self.pool.map(_ref_worker, spans))
         dt = time.perf_counter() - t0
         assert done == hi - lo
-        self.last = hi - lo
-        return dt
+        return done, dt
 
     def close(self):
-        self.pool.close()
-        self.pool.join()
+        if self.pool is not None:
+            self.pool.close()
+            self.pool.join()
 
 
-def reference_sample_size(c, cores: int, seconds: float) -> int:
-    """Queries per sample so the reference spends ~`seconds` of wall time.
-    Single-thread int8 scan rate measured in the survey: ~25e6 rows/s."""
-    per_query = c["n"] / 25e6 * (c["d"] / 100.0)
-    return int(max(cores, min(c["nq"], seconds * cores / max(per_query, 1e-6))))
+def reference_sample(c, procs: int, seconds: float) -> int:
+    """Queries per step so the reference spends about `seconds` of wall
+    time (single-thread int8 scan rate measured in the survey: ~25e6
+    rows/s at d=128)."""
+    per_query = c["n"] / 25e6 * (c["d"] / 128.0)
+    return int(max(procs, min(c["nq"], seconds * procs / max(per_query, 1e-9))))
+
+
+def measure_reference(c, X, Q, k, procs, seconds, steps=1, warmup=0):
+    ref = CpuReference(c, X, Q, k, procs)
+    try:
+        sample = reference_sample(c, procs, seconds)
+        for _ in range(warmup):
+            ref.step(procs)
+        done, secs = 0, 0.0
+        for _ in range(steps):
+            q, s = ref.step(sample)
+            done += q
+            secs += s
+    finally:
+        ref.close()
+    return done / secs, done, secs
 
 
 # ----------------------------------------------------------------- clocks --
@@ -201,6 +254,7 @@ def run_gpu(args):
     import torch.distributed as dist
 
     import paper_2110_08919_b200 as qa
+    import synth
     from paper_2110_08919_b200 import _lib, device as dev, sharded
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -211,33 +265,49 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks, peaks_src = load_peaks()
 
-    c, X, Q = make_workload(args.config, args.n, args.nq)
-    n, d, nq, k = c["n"], c["d"], c["nq"], args.k
+    c = workload(args)
+    n, d, nq, k, B = c["n"], c["d"], c["nq"], args.k, c["batch"]
     metric = qa.Metric(c["metric"])
 
-    # ---- index build (not timed): calibrate on the full corpus, encode this
-    # rank's shard.  Calibration is per-dimension min/max -- exact and
-    # order-free -- so every rank derives the identical window.
-    x_full = torch.from_numpy(X).cuda()
-    stats = qa.minmax_stats(x_full)
-    fr = qa.fit_symmetric(stats) if c["calibration"] == "symmetric" else qa.fit_minmax(stats)
+    # ---- index build (not timed): this rank generates and encodes only its
+    # own row shard; the per-dimension window comes from the exact min/max of
+    # the whole corpus (NCCL MIN/MAX all-reduce of the shard ranges).
     lo, hi = sharded.shard_bounds(n, world, rank)
-    index = qa.Int8Index.from_params(x_full[lo:hi].contiguous(), fr.params, metric, id_offset=lo)
-    del x_full
+    X_shard = synth.rows(args.config, lo, hi)
+    Q = synth.queries(args.config, nq)
+    x_dev = torch.from_numpy(X_shard).cuda()
+    mn, mx = dev.minmax(x_dev)
+    if world > 1:
+        dist.all_reduce(mn, op=dist.ReduceOp.MIN)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    stats = qa.RangeStats(min=mn.double().cpu().numpy(), max=mx.double().cpu().numpy(), count=n)
+    fr = qa.fit_symmetric(stats) if c["calibration"] == "symmetric" else qa.fit_minmax(stats)
+    index = qa.Int8Index.from_params(x_dev, fr.params, metric, id_offset=lo)
+    del x_dev
+    torch.cuda.empty_cache()
+    spans = batches(nq, B)
     q_dev = torch.from_numpy(Q).cuda()
     q_host = torch.from_numpy(Q).pin_memory()
-    qcodes = dev.DeviceCodes.empty(nq, d)
+    qcodes = [dev.DeviceCodes.empty(b - a, d) for a, b in spans]
     keff = min(k, n)
+    outs = [(torch.empty((b - a, keff), dtype=torch.float64, device="cuda"),
+             torch.empty((b - a, keff), dtype=torch.int32, device="cuda")) for a, b in spans]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
 
-    def search_step(queries_dev):
-        index.encode_queries(queries_dev, out=qcodes)
+    def search_batch(i, queries_dev):
+        index.encode_queries(queries_dev, out=qcodes[i])
         if world == 1:
-            return index.search_codes(qcodes, k)
-        return sharded.sharded_search(lambda off: index.search_codes(qcodes, k), n, k)
+            return index.search_codes(qcodes[i], k, out=outs[i])
+        return sharded.sharded_search(lambda off: index.search_codes(qcodes[i], k), n, k)
 
-    def timed(fn, steps, e2e=False):
+    def device_step():
+        for i, (a, b) in enumerate(spans):
+            search_batch(i, q_dev[a:b])
+
+    launches_per_step = [0]
+
+    def timed(fn, steps):
         times, launches = [], 0
         for _ in range(steps):
             flush.zero_()
@@ -245,6 +315,7 @@ def run_gpu(args):
                 dist.barrier()
             torch.cuda.synchronize()
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            _lib.reset_scan_totals()
             ev0.record(stream)
             fn()
             ev1.record(stream)
@@ -255,41 +326,68 @@ def run_gpu(args):
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 ms = float(t.item())
             times.append(ms)
-            st = _lib.last_scan_stats()
-            launches += 1 + st["launches"] + (1 if world > 1 else 0)
+            tot = _lib.scan_totals()
+            # encode launches + the scan's own launches (+ merge per batch when sharded)
+            launches += len(spans) + tot["launches"] + (len(spans) if world > 1 else 0)
+        launches_per_step[0] = launches // max(1, steps)
         return times, launches
-
-    out_host = (torch.empty((nq, keff), dtype=torch.float64).pin_memory(),
-                torch.empty((nq, keff), dtype=torch.int32).pin_memory())
-
-    def e2e_step():
-        qd = q_host.to("cuda", non_blocking=True)
-        s, i = search_step(qd)
-        out_host[0].copy_(s, non_blocking=True)
-        out_host[1].copy_(i, non_blocking=True)
 
     # warm-up
     for _ in range(max(3, args.warmup)):
-        search_step(q_dev)
+        device_step()
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
     clocks.start()
     _lib.set_profiling(True)
-    step_ms, launches = timed(lambda: search_step(q_dev), args.steps)
-    st = _lib.last_scan_stats()   # last step's kernel-level event timings
+    step_ms, launches = timed(device_step, args.steps)
+    tot = _lib.scan_totals()  # last step's kernel-level event timings (all batches)
     _lib.set_profiling(False)
     clk = clocks.stop()
 
-    e2e = None
+    e2e = e2e_api = None
     if not args.no_e2e:
+        host_out = [(torch.empty((b - a, keff), dtype=torch.float64).pin_memory(),
+                     torch.empty((b - a, keff), dtype=torch.int32).pin_memory()) for a, b in spans]
+
+        def e2e_step():
+            for i, (a, b) in enumerate(spans):
+                qd = q_host[a:b].to("cuda", non_blocking=True)
+                s, ids = search_batch(i, qd)
+                host_out[i][0].copy_(s, non_blocking=True)
+                host_out[i][1].copy_(ids, non_blocking=True)
+
         for _ in range(2):
             e2e_step()
-        e2e_ms, _ = timed(e2e_step, args.steps, e2e=True)
+        e2e_ms, _ = timed(e2e_step, args.steps)
         e2e = {"value": nq / (float(np.mean(e2e_ms)) / 1e3), "unit": "queries/s",
                "h2d_bytes_per_step": int(nq * d * 4),
                "d2h_bytes_per_step": int(nq * keff * (8 + 4)),
-               "ms_per_step": float(np.mean(e2e_ms))}
+               "ms_per_step": float(np.mean(e2e_ms)),
+               "path": "Int8Index.encode_queries + search_codes per batch, pinned host fp32 "
+                       "queries in, pinned host scores + ids out"}
+        if world == 1:
+            # the reference-facing API: host int8 DenseDatasets in, GroundTruth
+            # out (exact.py:105-117); the corpus is the frozen host code array
+            corpus = qa.DenseDataset(index.codes_in_input_order())
+            qcode_host = [qa.DenseDataset(qc.to_host()) for qc in qcodes]
+            for _ in range(2):
+                for qs in qcode_host:
+                    qa.batch_ground_truth(corpus, qs, k, metric)
+            api_ms = []
+            for _ in range(args.steps):
+                flush.zero_()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                for qs in qcode_host:
+                    qa.batch_ground_truth(corpus, qs, k, metric)
+                api_ms.append((time.perf_counter() - t0) * 1e3)
+            e2e_api = {"value": nq / (float(np.mean(api_ms)) / 1e3), "unit": "queries/s",
+                       "h2d_bytes_per_step": int(nq * d),
+                       "d2h_bytes_per_step": int(nq * keff * 4),
+                       "ms_per_step": float(np.mean(api_ms)),
+                       "path": "batch_ground_truth(DenseDataset int8 corpus, int8 query batch, "
+                               "k, metric) per batch (host wall clock; corpus resident)"}
 
     # correctness spot check of the last result on a few queries (oracle);
     # outside every timed region
@@ -298,13 +396,13 @@ def run_gpu(args):
         try:
             from oracle import qa_oracle as o
 
-            s, i = index.search_codes(qcodes, k)
-            sub = min(8, nq)
+            s, ids = index.search_codes(qcodes[0], k)
+            sub = min(8, qcodes[0].n)
             Xc = index.codes_in_input_order()
-            Qc = qcodes.to_host()[:sub]
+            Qc = qcodes[0].to_host()[:sub]
             osc, oids = o.scan_topk_i8(Xc, Qc, k, int(metric), o.norms_i8(Xc), o.norms_i8(Qc))
             parity = {"queries_checked": sub,
-                      "ids_equal": bool(np.array_equal(i[:sub].cpu().numpy(), oids)),
+                      "ids_equal": bool(np.array_equal(ids[:sub].cpu().numpy(), oids)),
                       "scores_equal": bool(np.array_equal(s[:sub].cpu().numpy(), osc))}
         except Exception as exc:  # pragma: no cover
             parity = {"error": str(exc)[:200]}
@@ -313,63 +411,64 @@ def run_gpu(args):
     value = nq / (ms / 1e3)
     # roofline of the dominant kernel (the fused tcgen05 filter pass):
     # algorithmic ops = 2 * nq * rows * d (unpadded d) per launch, divided by
-    # the CUDA-event time of those launches on their stream.
+    # the CUDA-event time of those launches on their stream, summed over the
+    # step's batches
     peak_tops = 2.0 * float(peaks["bf16_tflops"])
-    # DRAM traffic of the dominant launch (the final, estimated-bound pass)
-    # from the committed ncu --set full capture of this workload; compare to
-    # its algorithmic bytes (the database rows it scans, once)
-    traffic, traffic_note = None, "no committed ncu capture"
-    tfile = ROOT / "profiles" / "r01_filter_traffic.json"
-    if tfile.exists() and args.config == 1 and args.n is None and args.nq is None:
+    traffic, traffic_note = None, "no committed ncu capture for this workload"
+    tfile = ROOT / "profiles" / f"r02_filter_traffic_cfg{args.config}.json"
+    if tfile.exists() and args.n is None and args.nq is None and world == 1:
         tj = json.loads(tfile.read_text())
         traffic = tj["dram_bytes_read"] + tj["dram_bytes_write"]
-        traffic_note = (f"bytes per launch of the final filter pass ({tj['source']}); "
-                        f"algorithmic bytes {tj['algorithmic_db_bytes']}")
-    achieved = (st["filter_ops"] / (st["filter_ms"] / 1e3) / 1e12) if st["filter_ms"] > 0 else None
+        traffic_note = (f"DRAM bytes per launch of the main filter pass ({tj['source']}); "
+                        f"algorithmic bytes per launch {tj['algorithmic_bytes']}")
+    achieved = (tot["filter_ops"] / (tot["filter_ms"] / 1e3) / 1e12) if tot["filter_ms"] > 0 else None
     roofline = {
-        "bound": "tensor", "kernel": "filter_tc_kernel (tcgen05 kind::i8 + fused threshold top-k epilogue)",
+        "bound": "tensor", "kernel": "filter_tc_kernel (tcgen05 kind::i8 + fused threshold epilogue)",
         "achieved": achieved, "peak": peak_tops, "unit": "TOP/s",
         "frac": (achieved / peak_tops) if achieved else None,
-        "peak_source": f"2 x dense bf16 {peaks_src} (int8 dense = 2x bf16 on B200; "
-                       f"spec 4500 TOP/s)",
+        "peak_source": f"2 x dense bf16 {peaks_src} (int8 dense = 2x bf16 on B200)",
+        "frac_of_measured_kind_i8": (achieved / MMA_I8_TOPS) if achieved else None,
         "frac_of_spec_4500": (achieved / 4500.0) if achieved else None,
         "traffic": traffic,
         "traffic_note": traffic_note,
-        "filter_ms_per_step": st["filter_ms"], "select_ms_per_step": st["select_ms"],
-        "filter_launches_per_step": st["filter_launches"],
-        "filter_share_of_step": st["filter_ms"] / ms if ms else None,
-        "scan_stats": {key: st[key] for key in ("rounds", "launches", "retries", "candidates")},
+        "whole_step_tops": 2.0 * nq * (n / world) * d / (ms / 1e3) / 1e12,
+        "filter_ms_per_step": tot["filter_ms"], "select_ms_per_step": tot["select_ms"],
+        "filter_launches_per_step": tot["filter_launches"],
+        "filter_share_of_step": tot["filter_ms"] / ms if ms else None,
+        "scan_stats": {key: tot[key] for key in ("rounds", "launches", "retries", "candidates")},
     }
     line = {
         "metric": METRIC_NAME, "value": value, "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int8",
-        "data": f"synthetic (paper_2110_08919_b200.synth config {args.config}, seed {c['seed']})",
-        "config": {"workload": workload_desc(c, k), "n": n, "d": d, "nq": nq, "k": k,
+        "data": f"synthetic (synth.py config {args.config}, seed {c['seed']}; "
+                f"stand-in for the paper's dataset)",
+        "config": {"workload": workload_desc(c, k), "n": n, "d": d, "nq": nq, "batch": B, "k": k,
                    "metric": metric.short_name, "calibration": c["calibration"],
-                   "parallelism": f"row-shard x{world}, queries replicated, NCCL all-gather of "
-                                  f"top-k" if world > 1 else "single GPU",
+                   "parallelism": (f"row-shard x{world}, queries replicated, NCCL all-gather of "
+                                   f"top-k" if world > 1 else "single GPU"),
                    "l2": "flushed (256 MiB write) before every timed step"},
         "database_vectors_per_s": value * n,
         "roofline": roofline,
         "e2e": e2e,
+        "e2e_reference_api": e2e_api,
         "gpu_launches": launches,
+        "gpu_launches_per_step": launches_per_step[0],
         "clocks": clk,
         "parity_spot_check": parity,
         "impl": "b200",
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            ref = CpuReference(c, X, Q, k)
-            sample = reference_sample_size(c, ref.cores, 15.0)
-            secs = ref.step(sample)
-            sample = ref.last
-            ref.close()
-            line["cpu_baseline"] = {"value": sample / secs, "unit": "queries/s", "cores": ref.cores,
-                                    "kind": "reference",
-                                    "sample": f"{sample} of the {nq} queries against the full "
-                                              f"{n}x{d} int8 db (reference _core.scan_topk, "
-                                              f"{ref.cores} forked workers)"}
+            cores = os.cpu_count() or 1
+            v1, q1, s1 = measure_reference(c, X_shard, Q, k, 1, 6.0)
+            vp, qp, sp = measure_reference(c, X_shard, Q, k, cores, 12.0)
+            line["cpu_baseline"] = {
+                "value": vp, "unit": "queries/s", "cores": cores, "kind": "reference",
+                "sample": f"{qp} of the {nq} queries against the full {n}x{d} int8 db "
+                          f"(reference quantann._core.scan_topk, {cores} forked workers)",
+                "single_thread": {"value": v1, "queries": q1, "seconds": s1},
+                "cpu_model": cpu_model()}
         except Exception as exc:  # pragma: no cover
             line["cpu_baseline"] = {"error": str(exc)[:200]}
     if rank == 0:
@@ -380,33 +479,46 @@ def run_gpu(args):
 
 
 def run_reference(args):
+    """The reference arm: its own CPU kernel on this box's host cores.  Only
+    rank 0 works (the path is host-only); other ranks exit at once."""
+    import synth
+
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    c, X, Q = make_workload(args.config, args.n, args.nq)
+    c = workload(args)
     k = args.k
-    ref = CpuReference(c, X, Q, k)
-    sample = reference_sample_size(c, ref.cores, 8.0)
+    X, Q = synth.rows(args.config, 0, c["n"]), synth.queries(args.config, c["nq"])
+    cores = os.cpu_count() or 1
+    ref = CpuReference(c, X, Q, k, cores)
+    sample = reference_sample(c, cores, 6.0)
     for _ in range(args.warmup):
-        ref.step(min(sample, ref.cores))
-    secs = [ref.step(sample) for _ in range(args.steps)]
-    sample = ref.last
+        ref.step(cores)
+    done, secs = 0, 0.0
+    for _ in range(args.steps):
+        q, s = ref.step(sample)
+        done += q
+        secs += s
     ref.close()
-    value = sample / float(np.mean(secs))
+    value = done / secs
     line = {
         "metric": METRIC_NAME, "value": value, "unit": "queries/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(secs)) * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int8",
-        "data": f"synthetic (paper_2110_08919_b200.synth config {args.config}, seed {c['seed']})",
+        "data": f"synthetic (synth.py config {args.config}, seed {c['seed']}; "
+                f"stand-in for the paper's dataset)",
         "config": {"workload": workload_desc(c, k), "n": c["n"], "d": c["d"], "nq": c["nq"],
-                   "k": k, "metric": ("ip", "l2", "angular")[c["metric"]],
-                   "calibration": c["calibration"], "parallelism": "host cores (forked workers)"},
+                   "batch": c["batch"], "k": k, "metric": ("ip", "l2", "angular")[c["metric"]],
+                   "calibration": c["calibration"],
+                   "parallelism": f"{cores} host processes (forked workers over query slices)",
+                   "l2": "flushed (256 MiB write) before every timed step"},
         "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": ref.cores,
-                         "kind": "reference",
-                         "sample": f"{sample} queries per step against the full {c['n']}x{c['d']} "
-                                   f"int8 db (reference quantann._core.scan_topk)"},
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "reference",
+                         "sample": f"{sample} queries per step ({done} in {args.steps} steps) "
+                                   f"against the full {c['n']}x{c['d']} int8 db "
+                                   f"(reference quantann._core.scan_topk)",
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

@@ -208,6 +208,10 @@ typedef struct {
     double select_ms;
 } qa_scan_stats;
 int qa_last_scan_stats(qa_scan_stats *out);
+/* Sums of qa_scan_stats over every scan since the last reset (a step that
+ * issues several query batches reports them together). */
+int qa_scan_totals(qa_scan_stats *out);
+int qa_reset_scan_totals(void);
 /* Enable (1) / disable (0) event timing of filter and select launches. */
 int qa_set_profiling(int on);
 

@@ -34,8 +34,7 @@ BACKEND = "cuda"
 
 def _to_dev(arr: np.ndarray, dev) -> torch.Tensor:
     """Upload a (possibly read-only) host array without writing to it."""
-    arr = np.ascontiguousarray(arr)
-    return torch.from_numpy(arr if arr.flags.writeable else arr.copy()).to(dev)
+    return _dev.host_to_device(arr, dev)
 
 
 def _check_pair(data, queries):
@@ -45,6 +44,48 @@ def _check_pair(data, queries):
         raise ValueError("dtype mismatch between data and queries")
     if data.shape[1] != queries.shape[1]:
         raise ValueError("dimension mismatch between data and queries")
+
+
+# ---- device-resident corpora ---------------------------------------------
+#
+# The reference's callers hand the same frozen corpus array to every call
+# (DenseDataset freezes its array, reference dataset.py:82; exact.py:105-117
+# passes ``corpus.data`` each time).  A read-only int8 corpus is therefore
+# uploaded once and its DeviceCodes (codes + norms) kept resident, keyed on
+# the array object (weakly) plus its address, shape, strides and a strided
+# content fingerprint; writable arrays are never cached.
+
+_RESIDENT: dict = {}
+
+
+def _fingerprint(arr: np.ndarray) -> int:
+    flat = arr.reshape(-1).view(np.uint8)
+    step = max(1, flat.shape[0] // 4096)
+    return hash(flat[::step].tobytes())
+
+
+def _resident(arr: np.ndarray, dev) -> _dev.DeviceCodes:
+    if arr.flags.writeable:
+        return _dev.DeviceCodes.from_host(arr, dev)
+    key = (arr.__array_interface__["data"][0], arr.shape, arr.strides, str(dev),
+           _fingerprint(arr))
+    ent = _RESIDENT.get(id(arr))
+    if ent is not None and ent[0]() is arr and ent[1] == key:
+        return ent[2]
+    dc = _dev.DeviceCodes.from_host(arr, dev)
+    import weakref
+
+    ident = id(arr)
+    _RESIDENT[ident] = (weakref.ref(arr, lambda _r, i=ident: _RESIDENT.pop(i, None)), key, dc)
+    return dc
+
+
+def _norms_on(norms, dc: _dev.DeviceCodes | None, dev):
+    """Caller norms as a device vector; the resident copy when they are the
+    corpus' own stored norms (bit-identical: both are the int8 norm kernel's)."""
+    if dc is not None and getattr(dc, "_host_norm", None) is norms:
+        return dc.norm
+    return torch.from_numpy(np.ascontiguousarray(norms, dtype=np.float32)).to(dev)
 
 
 def scan_topk(data, queries, k, metric, data_norms=None, query_norms=None):
@@ -63,50 +104,88 @@ def scan_topk(data, queries, k, metric, data_norms=None, query_norms=None):
     if data.dtype == np.float32:
         dn = qn = None
         if int(metric) == 2:
-            dn = torch.from_numpy(np.ascontiguousarray(data_norms, dtype=np.float32)).to(dev)
-            qn = torch.from_numpy(np.ascontiguousarray(query_norms, dtype=np.float32)).to(dev)
+            dn = _norms_on(data_norms, None, dev)
+            qn = _norms_on(query_norms, None, dev)
         scores, ids = _dev.scan_topk_f32(_to_dev(data, dev), _to_dev(queries, dev), int(k),
                                          int(metric), dn, qn)
         return scores.cpu().numpy(), ids.cpu().numpy()
     if data.dtype != np.int8:
         raise ValueError("dtype must be float32 or int8")
-    db = _dev.DeviceCodes.from_host(data, dev)
-    qs = _dev.DeviceCodes.from_host(queries, dev)
+    db = _resident(data, dev)
+    qs = _resident(queries, dev)
     dn = qn = None
     if int(metric) == 2:
-        dn = torch.from_numpy(np.ascontiguousarray(data_norms, dtype=np.float32)).to(dev)
-        qn = torch.from_numpy(np.ascontiguousarray(query_norms, dtype=np.float32)).to(dev)
+        dn = _norms_on(data_norms, db, dev)
+        qn = _norms_on(query_norms, qs, dev)
     scores, ids = _dev.scan_topk(db, qs, int(k), int(metric), dn, qn)
     return scores.cpu().numpy(), ids.cpu().numpy()
 
 
-def _pair(a, b, metric: int) -> float:
-    """One pair through the exhaustive-scan kernels (n = nq = 1, k = 1)."""
+# ---- single pairs: host arithmetic, exactly the reference's loops ---------
+
+def _pair_check(a, b):
     if a.shape[0] != b.shape[0]:
         raise ValueError("length mismatch")
     if a.dtype != b.dtype:
         raise ValueError("dtype mismatch")
-    if a.shape[0] == 0:
-        return 0.0
-    x = np.ascontiguousarray(b).reshape(1, -1)
-    q = np.ascontiguousarray(a).reshape(1, -1)
-    scores, _ = scan_topk(x, q, 1, metric)
-    return float(scores[0, 0])
+
+
+def _wrap_i32(v: int) -> int:
+    """C ``int`` accumulation (two's complement wrap), _core.pyx:49-63."""
+    return ((int(v) + (1 << 31)) % (1 << 32)) - (1 << 31)
 
 
 def dot(a, b):
-    """Inner product of two 1-D vectors of equal dtype (_core.pyx:99-115):
-    float32 -> float64 sequential sum, int8 -> exact int32 sum, as float."""
-    return -_pair(a, b, 0) + 0.0   # score = -dot; + 0.0 turns -0.0 into 0.0
+    """Inner product of two 1-D vectors of equal dtype (_core.pyx:99-115).
+    One pair is O(d) host work, so it stays on the CPU: float32 -> float64
+    products summed in order (np.cumsum is a sequential sum), int8 -> the
+    exact int sum as a C int."""
+    _pair_check(a, b)
+    if a.shape[0] == 0:
+        return 0.0
+    if a.dtype == np.float32:
+        return float(np.cumsum(a.astype(np.float64) * b.astype(np.float64))[-1])
+    if a.dtype != np.int8:
+        raise ValueError("dtype must be float32 or int8")
+    return float(_wrap_i32(int(np.dot(a.astype(np.int64), b.astype(np.int64)))))
 
 
 def l2sq(a, b):
     """Squared Euclidean distance of two 1-D vectors (_core.pyx:118-134)."""
-    return _pair(a, b, 1)
+    _pair_check(a, b)
+    if a.shape[0] == 0:
+        return 0.0
+    if a.dtype == np.float32:
+        t = a.astype(np.float64) - b.astype(np.float64)
+        return float(np.cumsum(t * t)[-1])
+    if a.dtype != np.int8:
+        raise ValueError("dtype must be float32 or int8")
+    t = a.astype(np.int64) - b.astype(np.int64)
+    return float(_wrap_i32(int(np.dot(t, t))))
+
+
+def resident_norms(mat):
+    """``norms(mat)`` as a read-only array that stays identical between
+    calls for a frozen int8 corpus: passing it back as ``data_norms`` lets
+    ``scan_topk`` use the device copy instead of uploading it (exact.py)."""
+    if mat.ndim != 2:
+        raise ValueError("expected a 2-D matrix")
+    n, d = mat.shape
+    if n == 0 or d == 0 or mat.dtype != np.int8:
+        return norms(mat)
+    dc = _resident(mat, _dev.default_device())
+    out = getattr(dc, "_host_norm", None)
+    if out is None:
+        out = dc.norm.cpu().numpy()
+        out.flags.writeable = False
+        if not mat.flags.writeable:
+            dc._host_norm = out
+    return out
 
 
 def norms(mat):
-    """float32(sqrt(int64 sum c^2)) of every int8 row."""
+    """float32(sqrt(int64 sum c^2)) of every int8 row (float32 rows: the
+    sequential float64 sum), _core.pyx:137-157.  A fresh array per call."""
     if mat.ndim != 2:
         raise ValueError("expected a 2-D matrix")
     n, d = mat.shape
@@ -116,8 +195,7 @@ def norms(mat):
         return _dev.norms_f32(_to_dev(mat, _dev.default_device())).cpu().numpy()
     if mat.dtype != np.int8:
         raise ValueError("dtype must be float32 or int8")
-    dc = _dev.DeviceCodes.from_host(mat)
-    return dc.norm.cpu().numpy()
+    return np.array(resident_norms(mat))
 
 
 def quantize(values, k, sb, se, bits):

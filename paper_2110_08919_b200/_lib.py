@@ -87,6 +87,8 @@ SIGNATURES = {
     "qa_debug_dots_i8": (c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_int, c_vp, c_vp]),
     "qa_last_scan_stats": (c_int, [ctypes.POINTER(ScanStats)]),
     "qa_set_profiling": (c_int, [c_int]),
+    "qa_scan_totals": (c_int, [ctypes.POINTER(ScanStats)]),
+    "qa_reset_scan_totals": (c_int, []),
 }
 
 
@@ -142,6 +144,17 @@ def last_scan_stats() -> dict:
     s = ScanStats()
     check(lib.qa_last_scan_stats(ctypes.byref(s)))
     return {name: getattr(s, name) for name, _ in ScanStats._fields_}
+
+
+def scan_totals() -> dict:
+    """qa_scan_stats summed over every scan since reset_scan_totals()."""
+    s = ScanStats()
+    check(lib.qa_scan_totals(ctypes.byref(s)))
+    return {name: getattr(s, name) for name, _ in ScanStats._fields_}
+
+
+def reset_scan_totals() -> None:
+    check(lib.qa_reset_scan_totals())
 
 
 def set_profiling(on: bool) -> None:

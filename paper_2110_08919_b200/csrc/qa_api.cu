@@ -35,6 +35,7 @@ namespace {
 
 thread_local std::string g_err;
 thread_local qa_scan_stats g_stats;
+thread_local qa_scan_stats g_totals;
 bool g_profiling = false;
 
 // Event pairs recorded around filter / select launches when profiling.
@@ -761,6 +762,17 @@ int qa_last_scan_stats(qa_scan_stats *out) {
     return QA_OK;
 }
 
+int qa_scan_totals(qa_scan_stats *out) {
+    if (!out) return set_err(QA_EINVAL, "null stats pointer");
+    *out = g_totals;
+    return QA_OK;
+}
+
+int qa_reset_scan_totals(void) {
+    g_totals = qa_scan_stats{};
+    return QA_OK;
+}
+
 int qa_minmax_f32(const float *x, int64_t n, int64_t d, int64_t ldx, float *out_min,
                   float *out_max, void *stream) {
     if (n < 0 || d < 1 || ldx < d) return set_err(QA_EINVAL, "bad shape");
@@ -797,8 +809,18 @@ int qa_scan_topk_i8(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const i
                     int64_t ldq,
                     const int32_t *q_sqnorm, const float *q_norm, int64_t k, int metric,
                     int64_t id_offset, double *out_scores, int32_t *out_ids, void *stream) {
-    return scan_entry(db, n, d, ldd, db_sqnorm, db_norm, row_ids, q, nq, ldq, q_sqnorm, q_norm, k, metric,
-                      id_offset, out_scores, out_ids, (cudaStream_t)stream);
+    const int rc = scan_entry(db, n, d, ldd, db_sqnorm, db_norm, row_ids, q, nq, ldq, q_sqnorm,
+                              q_norm, k, metric, id_offset, out_scores, out_ids,
+                              (cudaStream_t)stream);
+    g_totals.rounds += g_stats.rounds;
+    g_totals.candidates += g_stats.candidates;
+    g_totals.launches += g_stats.launches;
+    g_totals.retries += g_stats.retries;
+    g_totals.filter_launches += g_stats.filter_launches;
+    g_totals.filter_ops += g_stats.filter_ops;
+    g_totals.filter_ms += g_stats.filter_ms;
+    g_totals.select_ms += g_stats.select_ms;
+    return rc;
 }
 
 int qa_scan_topk_i8_host(const int8_t *data, int64_t n, int64_t d, const int8_t *queries,

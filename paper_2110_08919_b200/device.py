@@ -38,6 +38,19 @@ def default_device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+def host_to_device(arr: np.ndarray, device=None) -> torch.Tensor:
+    """Copy a C-contiguous host array to the device without an extra host
+    copy.  Read-only arrays (frozen DenseDatasets) are only ever read: the
+    tensor wrapping them is the source of one H2D copy and then dropped."""
+    import warnings
+
+    arr = np.ascontiguousarray(arr)
+    with warnings.catch_warnings():
+        warnings.filterwarnings("ignore", message=".*not writable.*")
+        src = torch.from_numpy(arr)
+    return src.to(device or default_device())
+
+
 @dataclass
 class DeviceCodes:
     """int8 code matrix resident in HBM plus its per-row norms."""
@@ -80,10 +93,14 @@ class DeviceCodes:
         n, d = arr.shape
         out = cls.empty(n, d, device)
         if n:
-            src = torch.from_numpy(arr.copy() if not arr.flags.writeable else arr)
             if out.ld != d:
                 out.codes.zero_()
             if d:
+                import warnings
+
+                with warnings.catch_warnings():
+                    warnings.filterwarnings("ignore", message=".*not writable.*")
+                    src = torch.from_numpy(arr)
                 out.codes[:, :d].copy_(src, non_blocking=False)
             elif out.ld:
                 out.codes.zero_()

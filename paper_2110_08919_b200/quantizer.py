@@ -189,7 +189,7 @@ def minmax_stats(data) -> RangeStats:
     if isinstance(data, np.ndarray):
         if data.dtype != np.float32 or data.ndim != 2:
             raise ElementKindMismatch("statistics are estimated on Float32 corpora")
-        t = torch.from_numpy(np.array(data, copy=True)).to(dev.default_device())
+        t = dev.host_to_device(data)
     else:
         t = data
     n = t.shape[0]
@@ -218,7 +218,7 @@ def estimate_stats(data) -> DimensionStats:
     if isinstance(data, np.ndarray):
         if data.dtype != np.float32 or data.ndim != 2:
             raise ElementKindMismatch("statistics are estimated on Float32 corpora")
-        t = torch.from_numpy(np.array(data, copy=True)).to(dev.default_device())
+        t = dev.host_to_device(data)
     else:
         t = data
     if t.dtype != torch.float32 or t.dim() != 2:
@@ -297,7 +297,7 @@ def quantize_array(values: np.ndarray, p: QuantizerParams) -> np.ndarray:
     if n == 0:
         return np.empty((0, d), dtype=np.int8)
     device = dev.default_device()
-    x = torch.from_numpy(np.array(values, copy=True)).to(device)
+    x = dev.host_to_device(values, device)
     k, sb, se = _params_on(p, device)
     codes = dev.encode(x, k, sb, se, p.bits)
     return codes.to_host()

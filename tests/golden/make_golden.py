@@ -296,7 +296,7 @@ def cfg_minis(qa, core):
     """BASELINE cfg0 (L2, min/max) and cfg1 (angular, symmetric) at reduced
     size through the reference pipeline: constructed stats -> fit(ABS_MAX)
     -> quantize_dataset -> compiled scan_topk."""
-    from paper_2110_08919_b200 import synth
+    import synth
     from quantann import DenseDataset
     from quantann.quantizer import DimensionStats, QuantMode, fit, quantize_dataset
 

@@ -20,7 +20,8 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU container
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_2110_08919_b200 as qa  # noqa: E402
-from paper_2110_08919_b200 import _backend, device as dev, synth  # noqa: E402
+import synth  # noqa: E402
+from paper_2110_08919_b200 import _backend, device as dev  # noqa: E402
 
 
 def _rand_codes(rng, n, d, lo=-127, hi=128, nonzero=False):

@@ -10,7 +10,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from paper_2110_08919_b200 import synth
+import synth
 
 
 def test_encode_matches_reference_golden(oracle, golden_encode):

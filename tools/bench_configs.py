@@ -64,7 +64,8 @@ def run_batched(cfg, args):
     import torch
 
     import paper_2110_08919_b200 as qa
-    from paper_2110_08919_b200 import _lib, synth
+    import synth
+    from paper_2110_08919_b200 import _lib
 
     hbm, tops, src = peaks()
     c = synth.CONFIGS[cfg]
@@ -152,7 +153,8 @@ def run_cfg3(args):
     import torch
 
     import paper_2110_08919_b200 as qa
-    from paper_2110_08919_b200 import _lib, device as dev, synth
+    import synth
+    from paper_2110_08919_b200 import _lib, device as dev
     from paper_2110_08919_b200.quantizer import RangeStats, fit_minmax
 
     hbm, tops, src = peaks()
@@ -239,7 +241,7 @@ def run_cfg4(args):
     import torch
 
     import paper_2110_08919_b200 as qa
-    from paper_2110_08919_b200 import synth
+    import synth
 
     hbm, tops, src = peaks()
     c = synth.CONFIGS[4]

@@ -5,7 +5,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 import paper_2110_08919_b200 as qa
-from paper_2110_08919_b200 import _lib, synth
+import synth
+from paper_2110_08919_b200 import _lib
 
 cfg = int(sys.argv[1]); n = int(sys.argv[2]); nq = int(sys.argv[3])
 metrics = [int(m) for m in sys.argv[4].split(",")] if len(sys.argv) > 4 else [synth.CONFIGS[cfg]["metric"]]

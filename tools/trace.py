@@ -15,7 +15,8 @@ sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 import torch  # noqa: E402
 
 import paper_2110_08919_b200 as qa  # noqa: E402
-from paper_2110_08919_b200 import _lib, synth  # noqa: E402
+import synth  # noqa: E402
+from paper_2110_08919_b200 import _lib  # noqa: E402
 
 
 def main():
