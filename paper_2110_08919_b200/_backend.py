@@ -50,12 +50,20 @@ def _check_pair(data, queries):
 #
 # The reference's callers hand the same frozen corpus array to every call
 # (DenseDataset freezes its array, reference dataset.py:82; exact.py:105-117
-# passes ``corpus.data`` each time).  A read-only int8 corpus is therefore
-# uploaded once and its DeviceCodes (codes + norms) kept resident, keyed on
-# the array object (weakly) plus its address, shape, strides and a strided
-# content fingerprint; writable arrays are never cached.
+# passes ``corpus.data`` each time).  A read-only int8 array is therefore
+# uploaded once and kept resident in the form the scan wants, keyed on the
+# array object (weakly) plus its address, shape, strides and a strided
+# content fingerprint; writable arrays are never cached.  Forms:
+#
+#   "rows"  caller order (query batches; norms)
+#   "strat" index layout: stratified sample region, norm blocks (L2, IP)
+#   "ang"   index layout with plain norm bands (angular)
+#
+# The index layouts (qa_layout.cu) are what the scan's threshold estimate and
+# per-unit bounds assume; ids still report caller rows (DeviceCodes.ids).
 
 _RESIDENT: dict = {}
+_FORM_OF_METRIC = {0: "strat", 1: "strat", 2: "ang"}
 
 
 def _fingerprint(arr: np.ndarray) -> int:
@@ -64,28 +72,41 @@ def _fingerprint(arr: np.ndarray) -> int:
     return hash(flat[::step].tobytes())
 
 
-def _resident(arr: np.ndarray, dev) -> _dev.DeviceCodes:
+def _make_form(base: _dev.DeviceCodes, form: str) -> _dev.DeviceCodes:
+    if form == "rows":
+        return base
+    return base.sorted_by_norm(stratify=form == "strat")
+
+
+def _resident(arr: np.ndarray, dev, form: str = "rows") -> _dev.DeviceCodes:
     if arr.flags.writeable:
-        return _dev.DeviceCodes.from_host(arr, dev)
+        return _make_form(_dev.DeviceCodes.from_host(arr, dev), form)
     key = (arr.__array_interface__["data"][0], arr.shape, arr.strides, str(dev),
            _fingerprint(arr))
     ent = _RESIDENT.get(id(arr))
-    if ent is not None and ent[0]() is arr and ent[1] == key:
-        return ent[2]
-    dc = _dev.DeviceCodes.from_host(arr, dev)
-    import weakref
+    if ent is None or ent[0]() is not arr or ent[1] != key:
+        import weakref
 
-    ident = id(arr)
-    _RESIDENT[ident] = (weakref.ref(arr, lambda _r, i=ident: _RESIDENT.pop(i, None)), key, dc)
+        ident = id(arr)
+        ent = (weakref.ref(arr, lambda _r, i=ident: _RESIDENT.pop(i, None)), key, {})
+        _RESIDENT[ident] = ent
+    forms = ent[2]
+    dc = forms.get(form)
+    if dc is None:
+        base = forms.get("rows") or _dev.DeviceCodes.from_host(arr, dev)
+        dc = _make_form(base, form)
+        forms[form] = dc
     return dc
 
 
-def _norms_on(norms, dc: _dev.DeviceCodes | None, dev):
-    """Caller norms as a device vector; the resident copy when they are the
-    corpus' own stored norms (bit-identical: both are the int8 norm kernel's)."""
-    if dc is not None and getattr(dc, "_host_norm", None) is norms:
+def _norms_on(norms, dc: _dev.DeviceCodes, dev):
+    """Caller norms (caller row order) as a device vector in ``dc``'s stored
+    order; the resident copy when they are the matrix' own stored norms
+    (bit-identical: both are the int8 norm kernel's)."""
+    if getattr(dc, "_host_norm", None) is norms:
         return dc.norm
-    return torch.from_numpy(np.ascontiguousarray(norms, dtype=np.float32)).to(dev)
+    t = torch.from_numpy(np.ascontiguousarray(norms, dtype=np.float32)).to(dev)
+    return t if dc.ids is None else t[dc.ids.long()]
 
 
 def scan_topk(data, queries, k, metric, data_norms=None, query_norms=None):
@@ -104,15 +125,17 @@ def scan_topk(data, queries, k, metric, data_norms=None, query_norms=None):
     if data.dtype == np.float32:
         dn = qn = None
         if int(metric) == 2:
-            dn = _norms_on(data_norms, None, dev)
-            qn = _norms_on(query_norms, None, dev)
+            dn = torch.from_numpy(np.ascontiguousarray(data_norms, dtype=np.float32)).to(dev)
+            qn = torch.from_numpy(np.ascontiguousarray(query_norms, dtype=np.float32)).to(dev)
         scores, ids = _dev.scan_topk_f32(_to_dev(data, dev), _to_dev(queries, dev), int(k),
                                          int(metric), dn, qn)
         return scores.cpu().numpy(), ids.cpu().numpy()
     if data.dtype != np.int8:
         raise ValueError("dtype must be float32 or int8")
-    db = _resident(data, dev)
-    qs = _resident(queries, dev)
+    if int(metric) not in _FORM_OF_METRIC:
+        raise ValueError(f"unknown metric {metric}")
+    db = _resident(data, dev, _FORM_OF_METRIC[int(metric)])
+    qs = _resident(queries, dev, "rows")
     dn = qn = None
     if int(metric) == 2:
         dn = _norms_on(data_norms, db, dev)
@@ -164,19 +187,26 @@ def l2sq(a, b):
     return float(_wrap_i32(int(np.dot(t, t))))
 
 
-def resident_norms(mat):
+def resident_norms(mat, corpus: bool = False):
     """``norms(mat)`` as a read-only array that stays identical between
-    calls for a frozen int8 corpus: passing it back as ``data_norms`` lets
-    ``scan_topk`` use the device copy instead of uploading it (exact.py)."""
+    calls for a frozen int8 matrix: passing it back as ``data_norms`` /
+    ``query_norms`` lets ``scan_topk`` use the device copy instead of
+    uploading it (exact.py).  ``corpus``: the matrix is an angular corpus
+    (its resident form is the angular index layout)."""
     if mat.ndim != 2:
         raise ValueError("expected a 2-D matrix")
     n, d = mat.shape
     if n == 0 or d == 0 or mat.dtype != np.int8:
         return norms(mat)
-    dc = _resident(mat, _dev.default_device())
+    dc = _resident(mat, _dev.default_device(), "ang" if corpus else "rows")
     out = getattr(dc, "_host_norm", None)
     if out is None:
-        out = dc.norm.cpu().numpy()
+        stored = dc.norm.cpu().numpy()
+        if dc.ids is None:
+            out = stored
+        else:
+            out = np.empty_like(stored)
+            out[dc.ids.cpu().numpy()] = stored
         out.flags.writeable = False
         if not mat.flags.writeable:
             dc._host_norm = out

@@ -130,10 +130,12 @@ struct Buf {
 struct Workspace {
     std::mutex mu;
     Buf state, state_cnt, thr, cand, ccount, ovf, flags, scratch, grp, est;
+    Buf sched;                       // [kSchedSlots] work-unit counters of the filter passes
     Buf f32_scores, f32_ss, f32_si, f32_sn;  // float32 exact search (qa_exact_f32.cu)
 };
 
 constexpr int kMaxDevices = 64;
+constexpr int kSchedSlots = 64;  // filter passes per query chunk with a preset counter
 Workspace g_ws[kMaxDevices];
 
 int current_device() {
@@ -312,6 +314,8 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
     QA_TRY(ws.ovf.reserve((size_t)nq * 4), "workspace");
     QA_TRY(ws.flags.reserve(64), "workspace");
     QA_TRY(ws.est.reserve((size_t)qc * 8), "workspace");
+    QA_TRY(ws.sched.reserve((size_t)kSchedSlots * 4), "workspace");
+    unsigned *sched = (unsigned *)ws.sched.ptr;
     unsigned long long *est = (unsigned long long *)ws.est.ptr;
     Entry *state = (Entry *)ws.state.ptr;
     int32_t *state_cnt = (int32_t *)ws.state_cnt.ptr;
@@ -335,8 +339,10 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
         // state, thresholds, this chunk's overflow flags and (chunk 0) the
         // search flags in one launch
         QA_TRY(launch_init_state_full(state_cnt, thr, m, metric, ovf + c0, c0 == 0 ? flags : nullptr,
-                                      ccount, (int32_t)std::min(n, pl.r0), st),
+                                      ccount, (int32_t)std::min(n, pl.r0), st, sched,
+                                      kSchedSlots),
                "init");
+        int pass = 0;  // filter passes of this chunk (work-unit counter slot)
         g_stats.launches += 1;
         if (c0 == 0 && metric == kAngular) {
             zero_norm_kernel<<<(unsigned)((n + nq + 255) / 256), 256, 0, st>>>(db_norm, n, q_norm,
@@ -349,7 +355,7 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
         bool counts_preset = true;  // init set round 0's (dense) counts
         int64_t cur_j = 0;  // estimate rank of the pass in flight (0: k-th bound)
         for (;;) {
-            FilterArgs fa;
+            FilterArgs fa{};
             fa.db = db;
             fa.ldd = ld;
             fa.q = q + c0 * ld;
@@ -379,6 +385,9 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             fa.mode = mode;
             fa.dots_out = nullptr;
             fa.ld_dots = 0;
+            if (pass >= kSchedSlots) QA_TRY(cudaMemsetAsync(sched + pass % kSchedSlots, 0, 4, st), "sched");
+            fa.sched = sched + pass % kSchedSlots;
+            ++pass;
             // ~k new candidates per doubling of the rows seen; the estimated
             // final pass admits ~est_j per prefix-sized slice
             fa.exp_cands = cur_j ? (double)cur_j * (double)(r_hi - r_lo) / (double)r_lo
@@ -713,6 +722,17 @@ int scan_entry(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_
     return QA_OK;
 }
 
+void add_totals() {
+    g_totals.rounds += g_stats.rounds;
+    g_totals.candidates += g_stats.candidates;
+    g_totals.launches += g_stats.launches;
+    g_totals.retries += g_stats.retries;
+    g_totals.filter_launches += g_stats.filter_launches;
+    g_totals.filter_ops += g_stats.filter_ops;
+    g_totals.filter_ms += g_stats.filter_ms;
+    g_totals.select_ms += g_stats.select_ms;
+}
+
 }  // namespace
 
 int num_sms() {
@@ -812,14 +832,7 @@ int qa_scan_topk_i8(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const i
     const int rc = scan_entry(db, n, d, ldd, db_sqnorm, db_norm, row_ids, q, nq, ldq, q_sqnorm,
                               q_norm, k, metric, id_offset, out_scores, out_ids,
                               (cudaStream_t)stream);
-    g_totals.rounds += g_stats.rounds;
-    g_totals.candidates += g_stats.candidates;
-    g_totals.launches += g_stats.launches;
-    g_totals.retries += g_stats.retries;
-    g_totals.filter_launches += g_stats.filter_launches;
-    g_totals.filter_ops += g_stats.filter_ops;
-    g_totals.filter_ms += g_stats.filter_ms;
-    g_totals.select_ms += g_stats.select_ms;
+    add_totals();
     return rc;
 }
 
@@ -974,8 +987,7 @@ int qa_debug_dots_i8(const int8_t *db, int64_t n, const int8_t *q, int64_t nq, i
                      int impl, int32_t *out, void *stream) {
     if (n < 1 || nq < 1 || d < 0) return set_err(QA_EINVAL, "bad shape");
     const int64_t ld = qa_code_stride(d);
-    FilterArgs fa;
-    memset(&fa, 0, sizeof(fa));
+    FilterArgs fa{};
     fa.db = db;
     fa.ldd = ld;
     fa.q = q;
@@ -992,6 +1004,9 @@ int qa_debug_dots_i8(const int8_t *db, int64_t n, const int8_t *q, int64_t nq, i
     Workspace &ws = g_ws[current_device() % kMaxDevices];
     std::lock_guard<std::mutex> lock(ws.mu);
     QA_TRY(ws.flags.reserve(64), "workspace");
+    QA_TRY(ws.sched.reserve((size_t)kSchedSlots * 4), "workspace");
+    fa.sched = (unsigned *)ws.sched.ptr;
+    QA_TRY(cudaMemsetAsync(fa.sched, 0, 4, st), "sched");
     cudaError_t e = impl == 0 ? launch_filter_tc(fa, st)
                               : launch_filter_simt(fa, st);
     QA_TRY(e, "debug dots");

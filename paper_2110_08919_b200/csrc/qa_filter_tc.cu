@@ -47,6 +47,7 @@
 
 #include "qa_common.cuh"
 #include "qa_internal.h"
+#include "qa_tc_ptx.cuh"
 
 namespace qa {
 
@@ -90,290 +91,6 @@ __host__ __device__ constexpr int nacc() { return 512 / N < 8 ? 512 / N : 8; }
 // 4 + reps (measured -20 % per tile with the bias MMAs removed).
 template <int N>
 __host__ __device__ constexpr bool direct_bounds() { return N == 64; }  // bias MMAs per tile at most (|bias| <= 4.1M)
-// try_wait suspend-time hint for the epilogue warps' waits (ns)
-constexpr int kWaitHintNs = 20000;
-
-// ------------------------------------------------------------------ PTX --
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    uint32_t addr = smem_u32(bar);
-    asm volatile(
-        "{\n\t"
-        ".reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-        "@!p bra WAIT_%=;\n\t"
-        "}" ::"r"(addr),
-        "r"(parity), "n"(kWaitHintNs)
-        : "memory");
-}
-
-__device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t"
-        ".reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t"
-        "}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-
-// Wait with nanosleep backoff, for the single-thread roles (producer, MMA,
-// bias), which would otherwise spin and steal issue slots from the epilogue
-// warps sharing their SM sub-partition.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
-    if (mbar_try(bar, parity)) return;
-    uint32_t ns = 16;
-    while (!mbar_try(bar, parity)) {
-        __nanosleep(ns);
-        ns = ns < 64 ? ns * 2 : 64;
-    }
-}
-
-template <uint32_t kMaxNs>
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t parity) {
-    uint32_t ns = 32;
-    while (!mbar_try(bar, parity)) {
-        __nanosleep(ns);
-        ns = ns < kMaxNs ? ns * 2 : kMaxNs;
-    }
-}
-
-// Pure polling wait for the latency-critical MMA issuer.
-__device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
-    while (!mbar_try(bar, parity)) {
-    }
-}
-
-// Wait accounting (diagnostics build, -DQA_WAIT_STATS): cycles each role
-// spends in each wait, summed per CTA and printed by CTAs 0..1.
-#ifdef QA_WAIT_STATS
-#define WSTAT(i, stmt)                      \
-    do {                                    \
-        const long long _t0 = clock64();    \
-        stmt;                               \
-        wst[i] += clock64() - _t0;          \
-    } while (0)
-#else
-#define WSTAT(i, stmt) stmt
-#endif
-#ifdef QA_WAIT_STATS
-constexpr int kWst = 16;
-#endif
-
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar,
-                                            int32_t c0, int32_t c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-        "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-        : "memory");
-}
-
-// L2 prefetch of one database tile (no shared memory, no barrier)
-__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *map, int32_t c0, int32_t c1) {
-    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
-                     (uint64_t)map),
-                 "r"(c0), "r"(c1)
-                 : "memory");
-}
-
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)map) : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_before() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-
-// generic-proxy smem writes -> visible to the tensor core (async proxy)
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-__device__ __forceinline__ void tc_commit(uint64_t *bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-            smem_u32(bar))
-        : "memory");
-}
-
-
-// One K chunk of a tile, issued by one elected lane of a converged warp:
-// KSTEPS MMAs of K=32 bytes (descriptor start addresses step by 32 B = 2 in
-// the >>4 encoding), then a commit to `bar`.  Inline PTX with elect.sync
-// keeps the issue free of per-lane branching.
-template <int KSTEPS>
-__device__ __forceinline__ void mma_chunk_elect(uint32_t tmem_d, uint64_t ad, uint64_t bd,
-                                                uint32_t idesc, uint32_t first, uint32_t bar) {
-    static_assert(KSTEPS == 1 || KSTEPS == 2 || KSTEPS == 4, "1, 2 or 4 K steps");
-    if constexpr (KSTEPS == 4) {
-        asm volatile(
-            "{\n\t.reg .pred e, p;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
-            "elect.sync _|e, 0xffffffff;\n\t"
-            "setp.eq.u32 p, %4, 0;\n\t"
-            "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
-            "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
-            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
-            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a1, b1, %3, 1;\n\t"
-            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a2, b2, %3, 1;\n\t"
-            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a3, b3, %3, 1;\n\t"
-            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t"
-            "}" ::"r"(tmem_d),
-            "l"(ad), "l"(bd), "r"(idesc), "r"(first), "r"(bar)
-            : "memory");
-    } else if constexpr (KSTEPS == 2) {
-        asm volatile(
-            "{\n\t.reg .pred e, p;\n\t.reg .b64 a1, b1;\n\t"
-            "elect.sync _|e, 0xffffffff;\n\t"
-            "setp.eq.u32 p, %4, 0;\n\t"
-            "add.s64 a1, %1, 2;\n\tadd.s64 b1, %2, 2;\n\t"
-            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
-            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a1, b1, %3, 1;\n\t"
-            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t"
-            "}" ::"r"(tmem_d),
-            "l"(ad), "l"(bd), "r"(idesc), "r"(first), "r"(bar)
-            : "memory");
-    } else {
-        asm volatile(
-            "{\n\t.reg .pred e, p;\n\t"
-            "elect.sync _|e, 0xffffffff;\n\t"
-            "setp.eq.u32 p, %4, 0;\n\t"
-            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
-            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t"
-            "}" ::"r"(tmem_d),
-            "l"(ad), "l"(bd), "r"(idesc), "r"(first), "r"(bar)
-            : "memory");
-    }
-}
-
-// The bias MMA of a tile (accumulate) and the commit that hands the tile to
-// the epilogue, by one elected lane of a converged warp.
-__device__ __forceinline__ void mma_bias_commit_elect(uint32_t tmem_d, uint64_t ad, uint64_t bd,
-                                                      uint32_t idesc, uint32_t do_mma,
-                                                      uint32_t bar) {
-    asm volatile(
-        "{\n\t.reg .pred e, m;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "setp.ne.and.u32 m, %4, 0, e;\n\t"
-        "@m tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 1;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t"
-        "}" ::"r"(tmem_d),
-        "l"(ad), "l"(bd), "r"(idesc), "r"(do_mma), "r"(bar)
-        : "memory");
-}
-
-// an extra bias MMA (same constant A tile and digits; no commit)
-__device__ __forceinline__ void mma_bias_elect(uint32_t tmem_d, uint64_t ad, uint64_t bd,
-                                               uint32_t idesc) {
-    asm volatile(
-        "{\n\t.reg .pred e;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 1;\n\t"
-        "}" ::"r"(tmem_d),
-        "l"(ad), "l"(bd), "r"(idesc)
-        : "memory");
-}
-
-__device__ __forceinline__ void tmem_wait() {
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-// tcgen05.ld of C (16 or 32) consecutive accumulator columns of this warp's
-// 32 TMEM lanes; the registers are valid after tmem_wait().
-template <int C>
-__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, int32_t (&v)[C]) {
-    if constexpr (C == 32) {
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32"
-            " {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15,"
-            " %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31},"
-            " [%32];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-              "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
-              "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]),
-              "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
-              "=r"(v[30]), "=r"(v[31])
-            : "r"(taddr)
-            : "memory");
-    } else if constexpr (C == 8) {
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x8.b32"
-            " {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-              "=r"(v[7])
-            : "r"(taddr)
-            : "memory");
-    } else {
-        static_assert(C == 16, "8, 16 or 32 columns");
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32"
-            " {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15},"
-            " [%16];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-              "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-            : "r"(taddr)
-            : "memory");
-    }
-}
-
-// Shared-memory atomics / stores by 32-bit shared address.  (Through a
-// generic pointer the compiler emits generic ATOM / ST, an order of
-// magnitude slower on the survivor path.)
-__device__ __forceinline__ int32_t atom_add_smem(uint32_t addr, int32_t v) {
-    int32_t old;
-    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
-    return old;
-}
-__device__ __forceinline__ void sts64(uint32_t addr, uint32_t a, uint32_t b) {
-    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
-}
-
-__device__ __forceinline__ int32_t lds32(uint32_t addr) {
-    int32_t r;
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(r) : "r"(addr));
-    return r;
-}
-
-
-// UMMA shared-memory descriptor, K-major, swizzle SW bytes (32/64/128):
-// start>>4 [0,14), LBO>>4 [16,30) (unused for swizzled K-major: 1),
-// SBO>>4 [32,46) = 8 rows * SW bytes, version 1 at bit 46, layout type
-// [61,64): 128B=2, 64B=4, 32B=6.
-template <int SW>
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
-    constexpr uint64_t layout = SW == 128 ? 2 : (SW == 64 ? 4 : 6);
-    constexpr uint64_t sbo = (8 * SW) >> 4;
-    return (uint64_t)((saddr >> 4) & 0x3fff) | ((uint64_t)1 << 16) | (sbo << 32) |
-           ((uint64_t)1 << 46) | (layout << 61);
-}
 
 // Instruction descriptor for kind::i8: D=S32 (bits 4-5 = 2), A/B signed
 // int8 (bits 7-9, 10-12 = 1), both K-major, N>>3 at 17, M>>4 at 24.
@@ -403,6 +120,7 @@ struct Staged {
     int32_t dot;
 };
 constexpr int kUnitRowsMax = 32 * kBlockM;  // rows of a work unit (<= 32 tiles)
+constexpr int kURing = 4;                   // unit-id ring (dynamic scheduling)
 
 struct Params {
     FilterArgs a;
@@ -415,15 +133,16 @@ struct Params {
     int b_slots;            // 1 or 2 query-tile buffers
     int stage_cap;          // survivor staging entries per slot
     int norm_bulk;          // norm arrays 16-byte aligned (bulk-copyable)
-    int experiment;         // diagnostics only (QA_B200_EXPERIMENT); 0 in production
-    int l2_prefetch;        // database tiles prefetched into L2 ahead of the loads
+    uint32_t idesc;         // MMA instruction descriptor (signed or unsigned bytes)
 };
 
 // Work unit u -> (query tile t, row block b).  Query tiles vary fastest, so
 // the CTAs working at the same time share row blocks (L2 reuse of the
-// streamed database tiles).  Units are assigned statically: CTA i takes
-// u = i, i + grid, i + 2 grid, ... -- every role of the CTA walks the same
-// sequence on its own, so no role waits for a scheduler.
+// streamed database tiles).  Units are handed out dynamically (a global
+// counter read by the producer, published through the unit-id ring): the
+// cost of a unit is dominated by its survivors, which concentrate in the
+// norm bands near the queries' -- a static round-robin left the slowest CTA
+// at 3.7x the fastest on cfg2.
 __device__ __forceinline__ void unit_tb(const Params &p, int64_t u, int64_t &t, int64_t &b) {
     t = u % p.n_qtiles;
     b = u / p.n_qtiles;
@@ -440,7 +159,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const FilterArgs &a = p.a;
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int64_t u_first = blockIdx.x, u_step = gridDim.x;
     constexpr int kNacc = nacc<N>();
 #ifdef QA_WAIT_STATS
     long long wst[kWst] = {};
@@ -487,9 +205,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *stage_full = bias_empty + 2;
     uint64_t *stage_free = stage_full + 2;
     uint64_t *norm_full = stage_free + 2;
-    uint32_t *tmem_base_s = (uint32_t *)(norm_full + 2);
+    uint64_t *unit_full = norm_full + 2;        // [kURing] unit id published
+    uint64_t *unit_empty = unit_full + kURing;  // [kURing] every role has read it
+    uint32_t *tmem_base_s = (uint32_t *)(unit_empty + kURing);
     int32_t *stage_n_all = (int32_t *)(tmem_base_s + 1);  // [2]
     int32_t *reps_s = stage_n_all + 2;  // [2] bias MMAs per tile of the unit
+    int32_t *uring = reps_s + 2;        // [kURing] unit ids (-1: no more work)
     constexpr int kEpiWarps = kEpiThreads / 32;
 
     if (threadIdx.x == 0) {
@@ -510,6 +231,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < kNacc; ++s) {
             mbar_init(acc_full + s, 1);
             mbar_init(acc_empty + s, kEpiWarps);
+        }
+        for (int s = 0; s < kURing; ++s) {
+            mbar_init(unit_full + s, 1);
+            mbar_init(unit_empty + s, kEpiWarps + 3);  // MMA, bias, flush, epilogue warps
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -533,40 +258,45 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_base_s;
 
+    // the it-th unit of this CTA (every consumer role walks the same
+    // sequence); the slot is handed back as soon as the id is read
+    auto unit_take = [&](int it) -> int {
+        const int s = it & (kURing - 1);
+        mbar_wait(unit_full + s, (uint32_t)(it / kURing) & 1);
+        const int u = *(volatile int *)(uring + s);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(unit_empty + s);
+        return u;
+    };
+
     if (warp == 0) {
         // =============================== TMA producer ===================
         if (lane == 0) {
             int stage = 0;
             uint32_t aph = 0;
-            int it = 0;
-            // L2 prefetch cursor, p.l2_prefetch tiles ahead of the loads in
-            // this CTA's (unit, tile) sequence: the shared-memory ring alone
-            // holds too few bytes in flight to cover the HBM latency when the
-            // MMAs are short (small query batches: one query tile, every row
-            // read once)
-            int64_t pf_u = u_first, pf_tile = 0, pf_end = 0;
-            auto pf_unit = [&](int64_t uu) {
-                int64_t tt, bb;
-                unit_tb(p, uu, tt, bb);
-                pf_tile = bb * p.tiles_per_unit;
-                pf_end = min(p.n_tiles, pf_tile + p.tiles_per_unit);
+            // unit ids are handed out by a global counter (dynamic
+            // scheduling: survivors concentrate in a few norm bands, so
+            // units differ in cost by several x) and published to the other
+            // roles through a 4-slot ring, two units ahead
+            int fetched = 0;
+            bool done = false;
+            auto fetch = [&]() {
+                if (done) return;
+                const int s = fetched & (kURing - 1);
+                WSTAT(14, mbar_wait_sleep(unit_empty + s, ((uint32_t)(fetched / kURing) & 1) ^ 1));
+                const unsigned v = atomicAdd(a.sched, 1u);
+                const int u = v < (unsigned)p.n_units ? (int)v : -1;
+                *(volatile int *)(uring + s) = u;
+                mbar_arrive(unit_full + s);
+                done = u < 0;
+                ++fetched;
             };
-            auto pf_next = [&]() {
-                if (pf_u >= p.n_units) return;
-                if (pf_tile >= pf_end) {
-                    pf_u += u_step;
-                    if (pf_u >= p.n_units) return;
-                    pf_unit(pf_u);
-                }
-                for (int c = 0; c < p.kchunks; ++c)
-                    tma_prefetch_2d(&tm_db, c * SW, (int32_t)(a.r_lo + pf_tile * kBlockM));
-                ++pf_tile;
-            };
-            if (p.l2_prefetch > 0 && pf_u < p.n_units) {
-                pf_unit(pf_u);
-                for (int i = 0; i < p.l2_prefetch; ++i) pf_next();
-            }
-            for (int64_t u = u_first; u < p.n_units; u += u_step, ++it) {
+            fetch();
+            fetch();
+            for (int it = 0;; ++it) {
+                fetch();
+                const int u = *(volatile int *)(uring + (it & (kURing - 1)));  // own write
+                if (u < 0) break;
                 int64_t t, b;
                 unit_tb(p, u, t, b);
                 // resident query tile for this unit
@@ -582,9 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int64_t tile0 = b * p.tiles_per_unit;
                 const int64_t tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
                 for (int64_t tile = tile0; tile < tile1; ++tile) {
-                    if (p.l2_prefetch > 0) pf_next();
-                    // (experiment 10: always the same, L2-hot tile)
-                    const int32_t row0 = (int32_t)(a.r_lo + (p.experiment == 10 ? 0 : tile) * kBlockM);
+                    const int32_t row0 = (int32_t)(a.r_lo + tile * kBlockM);
                     for (int c = 0; c < p.kchunks; ++c) {
                         WSTAT(1, mbar_wait_sleep(a_empty + stage, aph ^ 1));
                         mbar_arrive_expect_tx(a_full + stage, a_stage_bytes);
@@ -605,20 +333,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         // once: the start-address field is the low 14 bits (addr >> 4) and
         // smem addresses stay below 256 KiB, so stepping a descriptor is a
         // 64-bit add of (bytes >> 4).
-        constexpr uint32_t idesc = make_idesc(N);
+        const uint32_t idesc = p.idesc;
         const uint64_t adesc0 = make_desc<SW>(smem_u32(sA));
         const uint64_t bdesc0 = make_desc<SW>(smem_u32(sB));
         const uint64_t abias_desc = make_desc<32>(smem_u32(sAbias));
         const uint64_t bbias_desc0 = make_desc<32>(smem_u32(sBbias));
-        const bool no_acc_wait = p.experiment == 5 || p.experiment == 7;
-        const bool no_bias = p.experiment == 4 || p.experiment == 9;
-        const bool no_mma = p.experiment == 6 || p.experiment == 7;
         int stage = 0;
         uint32_t aph = 0;
         int acc = 0;
         uint32_t accph = 0;
-        int it = 0;
-        for (int64_t u = u_first; u < p.n_units; u += u_step, ++it) {
+        for (int it = 0;; ++it) {
+            const int u = unit_take(it);
+            if (u < 0) break;
             const int slot = it & 1;
             const uint32_t ph = (it >> 1) & 1;
             int64_t t, b;
@@ -632,54 +358,37 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t bbias_desc = bbias_desc0 + (uint64_t)((slot * N * kBiasK) >> 4);
             const int reps = reps_s[slot];  // written before bias_full
             for (int ti = 0; ti < ntl; ++ti) {
-                if (!no_acc_wait) WSTAT(4, mbar_wait_spin(acc_empty + acc, accph ^ 1));
+                WSTAT(4, mbar_wait_spin(acc_empty + acc, accph ^ 1));
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + (uint32_t)(acc * N);
                 for (int c = 0; c < p.kchunks; ++c) {
                     WSTAT(5, mbar_wait_spin(a_full + stage, aph));
                     tc_fence_after();
-                    if (no_mma) {  // diagnostics: TMA + barrier protocol only
-                        if (lane == 0) mbar_arrive(a_empty + stage);
-                        __syncwarp();
-                    } else {
-                        // "mma-with-elect": the whole warp reaches the issue,
-                        // one lane issues (no divergent branch around it)
-                        const uint64_t ad = adesc0 + (uint64_t)((stage * a_stage_bytes) >> 4);
-                        const uint64_t bd = bdesc + (uint64_t)((c * N * SW) >> 4);
-                        mma_chunk_elect<SW / 32>(tmem_d, ad, bd, idesc, c == 0 ? 1u : 0u,
-                                                 smem_u32(a_empty + stage));
-                    }
+                    // "mma-with-elect": the whole warp reaches the issue,
+                    // one lane issues (no divergent branch around it)
+                    const uint64_t ad = adesc0 + (uint64_t)((stage * a_stage_bytes) >> 4);
+                    const uint64_t bd = bdesc + (uint64_t)((c * N * SW) >> 4);
+                    mma_chunk_elect<SW / 32>(tmem_d, ad, bd, idesc, c == 0 ? 1u : 0u,
+                                             smem_u32(a_empty + stage));
                     if (++stage == p.stages) {
                         stage = 0;
                         aph ^= 1;
                     }
                 }
-                if (no_mma) {
-                    if (lane == 0 && !no_acc_wait) mbar_arrive(acc_full + acc);
-                    __syncwarp();
-                } else {
-                    // + bias_q on every row: constant A (127) x per-query digits,
-                    // issued `reps` times (bounds beyond one MMA's range)
-                    if (!no_bias)
-                        for (int r = 1; r < reps; ++r)
-                            mma_bias_elect(tmem_d, abias_desc, bbias_desc, idesc);
-                    mma_bias_commit_elect(tmem_d, abias_desc, bbias_desc, idesc,
-                                          (no_bias || reps == 0) ? 0u : 1u,
-                                          smem_u32(acc_full + acc));
-                }
+                // + bias_q on every row: constant A (127) x per-query digits,
+                // issued `reps` times (bounds beyond one MMA's range)
+                for (int r = 1; r < reps; ++r)
+                    mma_bias_elect(tmem_d, abias_desc, bbias_desc, idesc);
+                mma_bias_commit_elect(tmem_d, abias_desc, bbias_desc, idesc,
+                                      reps == 0 ? 0u : 1u, smem_u32(acc_full + acc));
                 if (++acc == kNacc) {
                     acc = 0;
                     accph ^= 1;
                 }
             }
             if (lane == 0) {
-                if (no_mma) {
-                    mbar_arrive(b_empty + bslot);
-                    mbar_arrive(bias_empty + slot);
-                } else {
-                    tc_commit(b_empty + bslot);
-                    tc_commit(bias_empty + slot);
-                }
+                tc_commit(b_empty + bslot);
+                tc_commit(bias_empty + slot);
             }
             __syncwarp();
         }
@@ -693,8 +402,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // two units ahead of the MMA.
         constexpr int kQPL = N / 32;  // query columns per lane
         const bool filtered = (a.mode == 0 || a.mode == 3);
-        int it = 0;
-        for (int64_t u = u_first; u < p.n_units; u += u_step, ++it) {
+        for (int it = 0;; ++it) {
+            const int u = unit_take(it);
+            if (u < 0) break;
             const int slot = it & 1;
             const uint32_t ph = (it >> 1) & 1;
             int64_t t, b;
@@ -789,7 +499,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) need = max(need, __shfl_xor_sync(0xffffffffu, need, o));
             constexpr bool kDirect = direct_bounds<N>();
-            const int reps = kDirect ? 0 : (filtered ? max(1, need) : 1);
+            // dense / diagnostic passes: no bias MMA at all
+            const int reps = kDirect ? 0 : (filtered ? max(1, need) : 0);
             const long long unit_a = (long long)kBiasA * (reps > 0 ? reps : 1);
             int32_t *bnd_out = bnd_all + slot * N;
 #pragma unroll
@@ -863,8 +574,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // in the query's global candidate list, then the staged survivors
         // are copied.  The epilogue never waits on global atomics.
         constexpr int kQPL = N / 32;
-        int it = 0;
-        for (int64_t u = u_first; u < p.n_units; u += u_step, ++it) {
+        for (int it = 0;; ++it) {
+            const int u = unit_take(it);
+            if (u < 0) break;
             const int slot = it & 1;
             const uint32_t ph = (it >> 1) & 1;
             int64_t t, b;
@@ -876,6 +588,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int32_t *qc = qcnt_all + slot * N;
                 Staged *sb = stage_all + slot * stage_cap;
                 const int ns = min(stage_n_all[slot], stage_cap);
+#ifdef QA_WAIT_STATS
+                if (lane == 0) wst[13] += ns;
+#endif
                 // each survivor's slot among its query's survivors of the unit
                 for (int e = lane; e < ns; e += 32) {
                     const uint32_t key = sb[e].key;
@@ -917,13 +632,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ew = warp - kEpiWarp0;           // 0..15
         const int quarter = warp & 3;
         const int col0 = (ew >> 2) * kCB;          // first column of this warp
-        const bool acc_sync = p.experiment != 5 && p.experiment != 7;
         constexpr bool lean = kFilter;
         const uint32_t tm_warp = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)col0;
         int acc = 0;
         uint32_t accph = 0;
-        int it = 0;
-        for (int64_t u = u_first; u < p.n_units; u += u_step, ++it) {
+        for (int it = 0;; ++it) {
+            const int u = unit_take(it);
+            if (u < 0) break;
             const int slot = it & 1;
             const uint32_t ph = (it >> 1) & 1;
             int64_t t, b;
@@ -1063,7 +778,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                 }
             } else {
-            if (p.experiment == 0 && (a.mode == 1 || a.mode == 3)) {
+            if (a.mode == 1 || a.mode == 3) {
                 // ---- dense (round 0) and masked-dense (early rounds) ----
                 // every element has its candidate slot; masked dense marks
                 // rows failing the bound row = -1 (no atomics at all)
@@ -1108,54 +823,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             } else {
-                // ---- diagnostics: the dot matrix / pipeline experiments ----
+                // ---- diagnostics (mode 2): the full dot matrix ----
                 for (int ti = 0; ti < ntl; ++ti, wrow0 += kBlockM) {
                     const int32_t row = wrow0 + lane;
                     const bool valid = row < r_hi;
-                    if (acc_sync) {
-                        if (p.experiment == 11)
-                            WSTAT(12, mbar_wait_backoff<256>(acc_full + acc, accph));
-                        else
-                            WSTAT(12, mbar_wait(acc_full + acc, accph));
-                    }
+                    mbar_wait(acc_full + acc, accph);
                     tc_fence_after();
                     const uint32_t tbase = tm_warp + (uint32_t)(acc * N);
 #pragma unroll 1
                     for (int ci = 0; ci < nch; ++ci) {
                         int32_t cur[kC];
-                        if (p.experiment >= 2) continue;  // no TMEM read at all
                         tmem_ld_cols<kC>(tbase + (uint32_t)(ci * kC), cur);
                         tmem_wait();
-                        if (p.experiment != 0) {          // TMEM read only
-                            if (cur[0] == 0x12345678 && cur[31 % kC] == 0x7654321) *stage_n = 0;
-                            continue;
-                        }
                         if (!valid) continue;
-                        const bool exc = (excm >> ci) & 1u;
 #pragma unroll
                         for (int j = 0; j < kC; ++j) {
                             const int c = col0 + ci * kC + j;
-                            if (c >= nqt) continue;
-                            const int64_t q = q0 + c;
-                            if (a.mode == 1) {         // dense: every dot (bias 0)
-                                a.cand[q * a.cap + (row - (int32_t)a.r_lo)] = Cand{row, cur[j]};
-                            } else if (a.mode == 2) {  // diagnostics: the dot matrix
-                                a.dots_out[q * a.ld_dots + row] = cur[j];
-                            } else {
-                                // masked dense (survivor-dense early rounds):
-                                // every element has its slot; rows failing the
-                                // bound are marked row = -1 (no atomics)
-                                const int32_t dot = (int32_t)((uint32_t)cur[j] -
-                                                              (uint32_t)lds32(bias_addr + 4u * (uint32_t)c));
-                                const bool keep = cur[j] >= 0 || exc;
-                                a.cand[q * a.cap + (row - (int32_t)a.r_lo)] =
-                                    keep ? Cand{row, dot} : Cand{-1, 0};
-                            }
+                            if (c < nqt) a.dots_out[(q0 + c) * a.ld_dots + row] = cur[j];
                         }
                     }
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0 && acc_sync) mbar_arrive(acc_empty + acc);
+                    if (lane == 0) mbar_arrive(acc_empty + acc);
                     if (++acc == kNacc) {
                         acc = 0;
                         accph ^= 1;
@@ -1177,6 +866,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < kWst; ++i)
             if (wst[i]) atomicAdd(&wst_s[i], (unsigned long long)wst[i]);
     __syncthreads();
+    if (threadIdx.x == 0)
+        printf("wstc cta=%d total=%lld surv=%d\n", (int)blockIdx.x, clock64() - t_start,
+               (int)wst_s[13]);
     if (threadIdx.x == 0 && blockIdx.x < 2)
         printf("wst cta=%d total=%lld prod[b_empty=%llu a_empty=%llu] mma[b_full=%llu bias_full=%llu "
                "acc_empty=%llu a_full=%llu] bias[bias_empty=%llu norm=%llu] flush[stage_full=%llu] "
@@ -1195,6 +887,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ------------------------------------------------------------- host side --
+
+}  // namespace
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1226,10 +920,12 @@ bool make_map(CUtensorMap *m, const int8_t *ptr, int64_t rows, int64_t cols, int
     return r == CUDA_SUCCESS;
 }
 
+namespace {
+
 // Diagnostics knobs, read once from the environment; production runs use
-// the defaults (QA_B200_EXPERIMENT=0: the real kernel).
+// the defaults.
 struct Knobs {
-    int experiment, stage_cap, max_stages, b_slots, l2_prefetch;
+    int stage_cap, max_stages, b_slots;
 };
 const Knobs &knobs() {
     static const Knobs k = [] {
@@ -1237,9 +933,8 @@ const Knobs &knobs() {
             const char *v = getenv(name);
             return (v && *v) ? atoi(v) : dflt;
         };
-        return Knobs{env_int("QA_B200_EXPERIMENT", 0), env_int("QA_B200_STAGECAP", kStageCapDefault),
-                     env_int("QA_B200_MAXSTAGES", 12), env_int("QA_B200_BSLOTS", 2),
-                     env_int("QA_B200_L2PF", 0)};  // measured: no gain (cfg4)
+        return Knobs{env_int("QA_B200_STAGECAP", kStageCapDefault),
+                     env_int("QA_B200_MAXSTAGES", 12), env_int("QA_B200_BSLOTS", 2)};
     }();
     return k;
 }
@@ -1257,17 +952,14 @@ cudaError_t launch_t(const FilterArgs &a, cudaStream_t st) {
     const int sms = num_sms();
     // tiles per unit: a power of two <= 32, so units stay inside one
     // 32-tile norm-sorted block of an index laid out by qa_order_rows_by_norm;
-    // at least ~4 units per CTA so the static assignment stays balanced
-    int64_t want = (p.n_tiles * p.n_qtiles) / ((int64_t)sms * 4);
+    // at least ~8 units per CTA so the dynamic assignment can balance
+    int64_t want = (p.n_tiles * p.n_qtiles) / ((int64_t)sms * 8);
     int64_t tpu = 1;
     while (tpu * 2 <= want && tpu < 32) tpu *= 2;
     p.tiles_per_unit = tpu;
     p.n_units = ((p.n_tiles + tpu - 1) / tpu) * p.n_qtiles;
     const Knobs &kn = knobs();
-    p.experiment = kn.experiment;
-    // one query tile: every database tile is read by one CTA once, so the
-    // stream is latency-bound on the shared-memory ring; prefetch ahead
-    p.l2_prefetch = p.n_qtiles == 1 ? kn.l2_prefetch : 0;
+    p.idesc = make_idesc(N);
     p.stage_cap = kn.stage_cap;
     {
         const void *nrm = (M == kL2) ? (const void *)a.db_sqnorm : (const void *)a.db_norm;
@@ -1288,8 +980,7 @@ cudaError_t launch_t(const FilterArgs &a, cudaStream_t st) {
     if (stages > kn.max_stages) stages = kn.max_stages;
     p.stages = stages;
     const size_t smem = fixed + (size_t)stages * (stage_bytes + 16);
-    auto kern = (a.mode == 0 && (p.experiment == 0 || p.experiment == 8)) ? filter_tc_kernel<SW, N, M, true>
-                                                   : filter_tc_kernel<SW, N, M, false>;
+    auto kern = a.mode == 0 ? filter_tc_kernel<SW, N, M, true> : filter_tc_kernel<SW, N, M, false>;
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1328,6 +1019,7 @@ cudaError_t dispatch_n(const FilterArgs &a, cudaStream_t st) {
 
 cudaError_t launch_filter_tc(const FilterArgs &a, cudaStream_t st) {
     if (a.r_hi <= a.r_lo || a.nq == 0) return cudaSuccess;
+    if (!a.sched) return cudaErrorInvalidValue;
     if (a.kdim % 32 != 0 || a.kdim > 1024) return cudaErrorNotSupported;
     if (a.ldd % 16 != 0 || a.ldq % 16 != 0) return cudaErrorNotSupported;
     if (a.r_hi > INT32_MAX) return cudaErrorNotSupported;

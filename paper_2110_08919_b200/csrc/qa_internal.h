@@ -52,7 +52,11 @@ struct FilterArgs {
     // expected candidates per query in this pass (mode 0; sizes the work
     // units so their survivors fit the on-chip staging)
     double exp_cands;
+    // zeroed work-unit counter of this launch (dynamic scheduling)
+    unsigned *sched = nullptr;
 };
+
+
 
 // Tensor-core (tcgen05 kind::i8) filter pass.  Returns cudaErrorNotSupported
 // when the shape is outside what the kernel handles.
@@ -112,9 +116,10 @@ cudaError_t launch_finalize(const Entry *state, int64_t nq, int64_t k, int64_t k
                             int32_t *any_redo = nullptr);
 // state_cnt := 0, thr := pass-all for nq queries; also zeroes ovf[nq] and
 // flags[16] when given (fused memsets)
+// (and zeroes sched[nsched], the filter passes' work-unit counters)
 cudaError_t launch_init_state_full(int32_t *state_cnt, int32_t *thr, int64_t nq, int metric,
                                    int32_t *ovf, int32_t *flags, int32_t *ccount, int32_t fill0,
-                                   cudaStream_t st);
+                                   cudaStream_t st, unsigned *sched = nullptr, int nsched = 0);
 // Norm range of every 32-row group, padded to `groups` entries (groups past
 // n never pass a filter bound).
 cudaError_t launch_group_ranges(int metric, const int32_t *sqnorm, const float *norm, int64_t n,

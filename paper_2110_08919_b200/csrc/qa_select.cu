@@ -530,8 +530,10 @@ __global__ void reset_kernel(int32_t *p, int64_t n, int32_t v) {
 
 __global__ void init_state_kernel(int32_t *state_cnt, int32_t *thr, int64_t nq,
                                   int32_t pass_all, int32_t *ovf, int32_t *flags,
-                                  int32_t *ccount = nullptr, int32_t fill0 = 0) {
+                                  int32_t *ccount = nullptr, int32_t fill0 = 0,
+                                  unsigned *sched = nullptr, int nsched = 0) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (sched && i < nsched) sched[i] = 0;
     if (i < nq) {
         state_cnt[i] = 0;
         thr[i] = pass_all;
@@ -786,12 +788,14 @@ cudaError_t launch_init_state(int32_t *state_cnt, int32_t *thr, int64_t nq, int 
 
 cudaError_t launch_init_state_full(int32_t *state_cnt, int32_t *thr, int64_t nq, int metric,
                                    int32_t *ovf, int32_t *flags, int32_t *ccount, int32_t fill0,
-                                   cudaStream_t st) {
+                                   cudaStream_t st, unsigned *sched, int nsched) {
     int32_t pass = metric == kIP ? kThrPassIP
                                  : (metric == kL2 ? kThrPassL2 : (int32_t)kThrPassAngBits);
-    const int64_t m = nq > 16 ? nq : 16;
+    int64_t m = nq > 16 ? nq : 16;
+    if (m < nsched) m = nsched;
     init_state_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(state_cnt, thr, nq, pass, ovf,
-                                                                   flags, ccount, fill0);
+                                                                   flags, ccount, fill0, sched,
+                                                                   nsched);
     return cudaGetLastError();
 }
 

@@ -159,6 +159,8 @@ def encode(x: torch.Tensor, k: torch.Tensor, sb: torch.Tensor, se: torch.Tensor,
             raise ValueError(f"{name} must be float32[{d}] on {x.device}")
     if out is None:
         out = DeviceCodes.empty(n, d, x.device)
+    elif out.n != n or out.d != d or out.device != x.device:
+        raise ValueError(f"out must hold {n} signed code rows of width {d} on {x.device}")
     check(lib.qa_encode_i8(_p(x), n, d, x.stride(0), _p(k.contiguous()), _p(sb.contiguous()),
                            _p(se.contiguous()), int(bits), _p(out.codes), out.ld,
                            _p(out.sqnorm), _p(out.norm), _stream()))
@@ -185,6 +187,11 @@ def scan_topk(db: DeviceCodes, q: DeviceCodes, k: int, metric: int, db_norm=None
         ids = torch.empty((q.n, keff), dtype=torch.int32, device=dev)
     else:
         scores, ids = out
+        for t, dt in ((scores, torch.float64), (ids, torch.int32)):
+            if (t.dtype != dt or tuple(t.shape) != (q.n, keff) or t.device != dev
+                    or not t.is_contiguous()):
+                raise ValueError(f"out tensors must be contiguous [{q.n}, {keff}] "
+                                 f"float64/int32 on {dev}")
     dn = db.norm if db_norm is None else db_norm
     qn = q.norm if q_norm is None else q_norm
     check(lib.qa_scan_topk_i8(_p(db.codes), db.n, db.d, db.ld, _p(db.sqnorm), _p(dn),

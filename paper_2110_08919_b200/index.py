@@ -41,18 +41,22 @@ class Int8Index:
     @classmethod
     def from_params(cls, x: torch.Tensor, params: QuantizerParams, metric: Metric,
                     id_offset: int = 0, sort_rows: bool = True) -> "Int8Index":
-        """Encode ``x`` with ``params``.  For L2 and angular the stored rows
-        are ordered by code norm (ids still report positions in ``x``), which
-        keeps the scan's per-warp filter bounds tight."""
+        """Encode ``x`` with ``params``.  The stored rows are ordered by code
+        norm (ids still report positions in ``x``), which keeps the scan's
+        per-unit filter bounds tight and its estimate prefix a stratified
+        sample."""
         device = x.device
         k, sb, se = (torch.from_numpy(np.array(a, dtype=np.float32)).to(device)
                      for a in (params.k, params.sb, params.se))
         codes = dev.encode(x, k, sb, se, params.bits)
-        if sort_rows and Metric(metric) != Metric.INNER_PRODUCT:
-            # L2: a stratified sample region first (qa_layout.cu); angular
-            # norms are narrow and keep plain norm bands
-            codes = codes.sorted_by_norm(stratify=Metric(metric) == Metric.L2_SQUARED)
-        return cls(params, Metric(metric), codes, k, sb, se, id_offset)
+        metric = Metric(metric)
+        if sort_rows:
+            # a stratified sample region first (qa_layout.cu) -- the threshold
+            # estimate reads the first rows as a sample of the whole index, so
+            # clustered or sorted input must not reach it in caller order;
+            # angular norms are narrow and keep plain norm bands
+            codes = codes.sorted_by_norm(stratify=metric != Metric.ANGULAR)
+        return cls(params, metric, codes, k, sb, se, id_offset)
 
     def codes_in_input_order(self) -> np.ndarray:
         """int8 codes [n, d] in the order of the encoded input rows."""

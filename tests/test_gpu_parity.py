@@ -2,8 +2,8 @@
 
 Bar: bit-exact codes, norms, int32 dots, top-k ids AND float64 scores for
 every metric -- the reference's own contract (_core.pyx:8-14).  Sizes here
-are ones the oracle finishes in seconds; full BASELINE sizes are covered by
-size-independent properties in test_gpu_scale.py.
+are ones the oracle finishes in seconds; the full BASELINE sizes are in
+test_gpu_configs.py (oracle subsets + size-independent properties).
 """
 
 from __future__ import annotations

@@ -36,7 +36,8 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int reps, long long *c
     __shared__ volatile int stop;
     __shared__ uint32_t tmem_base_s;
     for (int i = threadIdx.x; i < (128 + N) * 128 / 4; i += blockDim.x)
-        reinterpret_cast<int32_t *>(sA)[i] = 0x01010101;
+        reinterpret_cast<uint32_t *>(sA)[i] =
+            VAR == 9 ? (uint32_t)(i * 2654435761u) ^ 0x5bd1e995u : 0x01010101u;  // 9: random bytes
     if (threadIdx.x == 0) {
         stop = 0;
         for (int i = 0; i < 4; ++i)
@@ -59,6 +60,8 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int reps, long long *c
     uint32_t idesc;
     if (KIND == 0)
         idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
+    else if (KIND == 2)  // unsigned x unsigned bytes
+        idesc = (2u << 4) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
     else  // bf16 x bf16 -> f32: D fmt f32 (1 at bit 4), A/B fmt bf16 (1 at 7, 1 at 10)
         idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
     long long t0 = 0, t1 = 0;
@@ -70,7 +73,7 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int reps, long long *c
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
                 const uint64_t ad = make_desc128(a0 + kk * 32), bd = make_desc128(b0 + kk * 32);
-                if (KIND == 0)
+                if (KIND != 1)
                     asm volatile(
                         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
@@ -83,12 +86,12 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int reps, long long *c
                         "l"(ad), "l"(bd), "r"(idesc), "r"(kk)
                         : "memory");
             }
-            if (VAR >= 1)
+            if (VAR >= 1 && VAR != 9)
                 asm volatile(
                     "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                         smem_u32(&cbar[0]))
                     : "memory");
-            if (VAR >= 2) {
+            if (VAR >= 2 && VAR != 9) {
                 const uint64_t ad = (VAR == 2) ? make_desc32(a0) : make_desc128(a0);
                 const uint64_t bd = (VAR == 2) ? make_desc32(b0) : make_desc128(b0);
                 asm volatile(
@@ -167,8 +170,8 @@ void run(const char *name, int sms, const int8_t *src = nullptr, int tiles = 0) 
     double avg = 0;
     for (int i = 0; i < sms; ++i) avg += (double)h[i];
     avg /= sms;
-    const double mmas = (VAR >= 2 ? 5.0 : 4.0) * reps;
-    const double kmul = KIND == 0 ? 32 : 16;
+    const double mmas = ((VAR >= 2 && VAR != 9) ? 5.0 : 4.0) * reps;
+    const double kmul = KIND != 1 ? 32 : 16;
     const double ops = 2.0 * 128 * N * kmul * mmas * sms;
     printf("%-6s%s N=%3d  %7.1f cycles/MMA  %8.1f T(FL)OP/s over %.3f ms  (%s)\n", name,
            tiles ? "+stream" : (VAR == 1 ? "+commit" : (VAR == 2 ? "+bias32" : (VAR == 3 ? "+bias128" : "       "))), N,
@@ -185,6 +188,15 @@ int main() {
     cudaMalloc(&src, (size_t)tiles * 16384);
     cudaMemset(src, 1, (size_t)tiles * 16384);
     run<0, 256>("i8", sms);
+    run<2, 256>("u8", sms);
+    run<0, 224>("i8", sms);
+    run<2, 224>("u8", sms);
+    run<0, 192>("i8", sms);
+    run<0, 160>("i8", sms);
+    run<2, 224>("u8", sms, src, tiles);
+    run<0, 256, 9>("i8rnd", sms);
+    run<2, 224, 9>("u8rnd", sms);
+    run<0, 128, 9>("i8rnd", sms);
     run<0, 256, 1>("i8", sms);
     run<0, 256, 2>("i8", sms);
     run<0, 256, 3>("i8", sms);

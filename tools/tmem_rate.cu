@@ -47,7 +47,9 @@ __global__ void __launch_bounds__(544, 1) tmem_rate_kernel(int iters, int with_m
             const uint32_t idesc =
                 (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) | (8u << 24);
             const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+            long long m0 = clock64(), nm = 0;
             while (*(volatile int *)&done_warps < 16) {
+                nm += 256;
                 for (int r = 0; r < 64; ++r)
                     for (int kk = 0; kk < 4; ++kk)
                         asm volatile(
@@ -58,6 +60,7 @@ __global__ void __launch_bounds__(544, 1) tmem_rate_kernel(int iters, int with_m
                             "r"(idesc), "r"(kk)
                             : "memory");
             }
+            if (blockIdx.x == 0) printf("  MMA stream during loads: %.1f cycles per M128N256K32 MMA\n", (double)(clock64() - m0) / nm);
         }
     } else {
         const int quarter = warp & 3;
