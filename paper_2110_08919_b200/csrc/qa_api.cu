@@ -132,6 +132,10 @@ struct Workspace {
     Buf state, state_cnt, thr, cand, ccount, ovf, flags, scratch, grp, est;
     Buf sched;                       // [kSchedSlots] work-unit counters of the filter passes
     Buf f32_scores, f32_ss, f32_si, f32_sn;  // float32 exact search (qa_exact_f32.cu)
+    Buf f32_full;                            // any-k full sort scratch
+    Buf f32_x, f32_q, f32_xn;                // codes as float32 (large k / wide rows)
+    Buf r_idx, r_q, r_qsq, r_qn, r_s, r_ids;  // overflow retry
+    Buf merge;                                // large-k shard merge
 };
 
 constexpr int kMaxDevices = 64;
@@ -546,8 +550,24 @@ int f32_impl(Workspace &ws, const float *db, int64_t n, int64_t d, int64_t ldd,
              const float *db_norm, const float *q, int64_t nq, int64_t ldq, const float *q_norm,
              int64_t keff, int metric, int64_t id_offset, double *out_scores, int32_t *out_ids,
              cudaStream_t st) {
-    if (keff > kMaxKF32) return set_err(QA_EUNSUPPORTED, "k above this build's limit");
     if (n > INT32_MAX || d > INT32_MAX) return set_err(QA_EUNSUPPORTED, "shape above this build's limit");
+    if (keff > kMaxKF32) {
+        // any k: every score of a query chunk, stable-sorted per query
+        // (keff rows of the full (score, id) order, _core.pyx:348-365)
+        int64_t m = std::max<int64_t>(1, ((int64_t)2 << 30) / (32 * n));
+        m = std::min<int64_t>({m, nq, (int64_t)INT32_MAX / n, 65535});
+        const size_t need = f32_fullsort_bytes(m, n);
+        QA_TRY(ws.f32_full.reserve(need), "workspace");
+        for (int64_t c0 = 0; c0 < nq; c0 += m) {
+            const int64_t mm = std::min(m, nq - c0);
+            QA_TRY(launch_f32_fullsort(db, ldd, q + c0 * ldq, ldq, d, mm, n, metric, db_norm,
+                                       q_norm ? q_norm + c0 : nullptr, keff, id_offset,
+                                       out_scores + c0 * keff, out_ids + c0 * keff, ws.f32_full.ptr,
+                                       ws.f32_full.bytes, st),
+                   "f32 full sort");
+        }
+        return QA_OK;
+    }
     constexpr int64_t kF32Rows = 16384, kF32Queries = 1024;
     const int64_t R = std::min(n, kF32Rows);
     const int64_t qc = std::min(nq, kF32Queries);
@@ -608,60 +628,46 @@ int scan_entry(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_
         return set_err(QA_EINVAL, "angular metric needs data and query norms");
     if (metric == kL2 && (!db_sqnorm || !q_sqnorm))
         return set_err(QA_EINVAL, "L2 metric needs data and query squared norms");
-    if (keff > kMaxKF32)
-        return set_err(QA_EUNSUPPORTED, "k=%lld above this build's limit %lld", (long long)keff,
-                       (long long)kMaxKF32);
-    // int32 exactness: |dot| <= d*128^2 and l2 <= d*255^2 must stay < 2^31
-    // (the reference accumulates in C int as well, _core.pyx:49-63).
-    if (d > 131071 || (metric == kL2 && d > 33025))
-        return set_err(QA_EUNSUPPORTED, "d=%lld exceeds the int32-exact range for this metric",
-                       (long long)d);
     if (n > INT32_MAX) return set_err(QA_EUNSUPPORTED, "n exceeds int32 ids");
+    // Widths whose worst-case int32 sum could wrap (|dot| <= d*128^2, l2 <=
+    // d*255^2; the reference accumulates in C int, _core.pyx:49-63) take the
+    // float64-exact route below, like large k: identical to the reference
+    // whenever its int32 sums do not overflow.
+    const bool wide_d = d > 131071 || (metric == kL2 && d > 33025);
     Workspace &ws = g_ws[current_device() % kMaxDevices];
     std::lock_guard<std::mutex> lock(ws.mu);
-    if (keff > kMaxK) {
-        // large k: the float64-exact scan on the codes as float32 (bit-exact
-        // with the int8 path, see codes_to_f32_kernel), caller row order
-        float *xf = nullptr, *qf = nullptr, *xn = nullptr;
-        int rc = QA_OK;
-        cudaError_t e = cudaMalloc(&xf, (size_t)n * d * 4 + 16);
-        if (e == cudaSuccess) e = cudaMalloc(&qf, (size_t)nq * d * 4 + 16);
-        if (e == cudaSuccess) e = cudaMalloc(&xn, (size_t)n * 4 + 16);
-        if (e == cudaSuccess) {
-            codes_to_f32_kernel<<<(unsigned)n, 128, 0, st>>>(db, n, d, ld, row_ids,
-                                                             metric == kAngular ? db_norm : nullptr,
-                                                             xf, xn);
-            codes_to_f32_kernel<<<(unsigned)nq, 128, 0, st>>>(q, nq, d, ld, nullptr, nullptr, qf,
-                                                              nullptr);
-            e = cudaGetLastError();
-        }
-        if (e == cudaSuccess && metric == kAngular) {
+    if (keff > kMaxK || wide_d) {
+        // large k (or wide rows): the float64-exact scan on the codes as
+        // float32 (bit-exact with the int8 path, see codes_to_f32_kernel),
+        // caller row order
+        QA_TRY(ws.f32_x.reserve((size_t)n * d * 4 + 16), "workspace");
+        QA_TRY(ws.f32_q.reserve((size_t)nq * d * 4 + 16), "workspace");
+        QA_TRY(ws.f32_xn.reserve((size_t)n * 4 + 16), "workspace");
+        float *xf = (float *)ws.f32_x.ptr, *qf = (float *)ws.f32_q.ptr, *xn = (float *)ws.f32_xn.ptr;
+        codes_to_f32_kernel<<<(unsigned)n, 128, 0, st>>>(db, n, d, ld, row_ids,
+                                                         metric == kAngular ? db_norm : nullptr,
+                                                         xf, xn);
+        codes_to_f32_kernel<<<(unsigned)nq, 128, 0, st>>>(q, nq, d, ld, nullptr, nullptr, qf,
+                                                          nullptr);
+        QA_TRY(cudaGetLastError(), "large-k path");
+        if (metric == kAngular) {
             int32_t zf = 0;
             QA_TRY(ws.flags.reserve(64), "workspace");
             int32_t *dflag = (int32_t *)ws.flags.ptr + 2;
-            cudaMemsetAsync(dflag, 0, 4, st);
+            QA_TRY(cudaMemsetAsync(dflag, 0, 4, st), "large-k path");
             zero_norm_kernel<<<(unsigned)((n + nq + 255) / 256), 256, 0, st>>>(db_norm, n, q_norm,
                                                                                nq, dflag);
-            cudaMemcpyAsync(&zf, dflag, 4, cudaMemcpyDeviceToHost, st);
-            e = cudaStreamSynchronize(st);
-            if (e == cudaSuccess && zf) {
-                cudaFree(xf);
-                cudaFree(qf);
-                cudaFree(xn);
-                return set_err(QA_EZERONORM, "angular metric needs nonzero corpus and query vectors");
-            }
+            QA_TRY(cudaMemcpyAsync(&zf, dflag, 4, cudaMemcpyDeviceToHost, st), "large-k path");
+            QA_TRY(cudaStreamSynchronize(st), "large-k path");
+            if (zf) return set_err(QA_EZERONORM, "angular metric needs nonzero corpus and query vectors");
         }
-        if (e == cudaSuccess)
-            rc = f32_impl(ws, xf, n, d, d, metric == kAngular ? xn : nullptr, qf, nq, d,
-                          metric == kAngular ? q_norm : nullptr, keff, metric, id_offset,
-                          out_scores, out_ids, st);
-        else
-            rc = cuda_err(e, "large-k path");
-        if (rc == QA_OK && (e = cudaStreamSynchronize(st)) != cudaSuccess) rc = cuda_err(e, "large-k path");
-        cudaFree(xf);
-        cudaFree(qf);
-        cudaFree(xn);
-        return rc;
+        const int rc = f32_impl(ws, xf, n, d, d, metric == kAngular ? xn : nullptr, qf, nq, d,
+                                metric == kAngular ? q_norm : nullptr, keff, metric, id_offset,
+                                out_scores, out_ids, st);
+        if (rc != QA_OK) return rc;
+        // the workspace is reused by the next call on any stream
+        QA_TRY(cudaStreamSynchronize(st), "large-k path");
+        return QA_OK;
     }
     std::vector<int32_t> ovf;
     g_timer.reset();
@@ -675,18 +681,18 @@ int scan_entry(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_
         g_stats.retries += 1;
         cap = std::min<int64_t>(cap * 4, std::max<int64_t>(n, 2048));
         const int64_t m = (int64_t)ovf.size();
-        int32_t *idx = nullptr;
-        int8_t *qsub = nullptr;
-        int32_t *qsq = nullptr;
-        float *qn = nullptr;
-        double *s = nullptr;
-        int32_t *ids = nullptr;
-        QA_TRY(cudaMalloc(&idx, m * 4), "retry");
-        QA_TRY(cudaMalloc(&qsub, m * ld), "retry");
-        QA_TRY(cudaMalloc(&qsq, m * 4), "retry");
-        QA_TRY(cudaMalloc(&qn, m * 4), "retry");
-        QA_TRY(cudaMalloc(&s, m * keff * 8), "retry");
-        QA_TRY(cudaMalloc(&ids, m * keff * 4), "retry");
+        QA_TRY(ws.r_idx.reserve((size_t)m * 4), "workspace");
+        QA_TRY(ws.r_q.reserve((size_t)m * ld), "workspace");
+        QA_TRY(ws.r_qsq.reserve((size_t)m * 4), "workspace");
+        QA_TRY(ws.r_qn.reserve((size_t)m * 4), "workspace");
+        QA_TRY(ws.r_s.reserve((size_t)m * keff * 8), "workspace");
+        QA_TRY(ws.r_ids.reserve((size_t)m * keff * 4), "workspace");
+        int32_t *idx = (int32_t *)ws.r_idx.ptr;
+        int8_t *qsub = (int8_t *)ws.r_q.ptr;
+        int32_t *qsq = (int32_t *)ws.r_qsq.ptr;
+        float *qn = (float *)ws.r_qn.ptr;
+        double *s = (double *)ws.r_s.ptr;
+        int32_t *ids = (int32_t *)ws.r_ids.ptr;
         QA_TRY(cudaMemcpyAsync(idx, ovf.data(), m * 4, cudaMemcpyHostToDevice, st), "retry");
         gather_rows_kernel<<<(unsigned)m, 128, 0, st>>>(q, ld, idx, m, qsub);
         if (q_sqnorm)
@@ -708,12 +714,6 @@ int scan_entry(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_
         // map second-level overflow indices back to original query ids
         std::vector<int32_t> next;
         for (int32_t i : ovf2) next.push_back(ovf[i]);
-        cudaFree(idx);
-        cudaFree(qsub);
-        cudaFree(qsq);
-        cudaFree(qn);
-        cudaFree(s);
-        cudaFree(ids);
         if (rc != QA_OK) return rc;
         ovf.swap(next);
         if (cap >= n && !ovf.empty())
@@ -803,6 +803,9 @@ int qa_minmax_f32(const float *x, int64_t n, int64_t d, int64_t ldx, float *out_
     QA_TRY(ws.scratch.reserve((size_t)floats * 4), "workspace");
     QA_TRY(launch_minmax(x, n, d, ldx, out_min, out_max, (float *)ws.scratch.ptr, floats, st),
            "minmax");
+    // the shared scratch is free for the next caller (any stream) only once
+    // this call's kernels are done (build-time entry: the sync is cheap)
+    QA_TRY(cudaStreamSynchronize(st), "minmax");
     return QA_OK;
 }
 
@@ -959,6 +962,7 @@ int qa_order_rows_by_norm(const int32_t *sqnorm, int64_t n, int stratify, int32_
     QA_TRY(launch_order_by_key(sqnorm, n, stratify != 0, perm, ws.scratch.ptr, ws.scratch.bytes,
                               &need, st),
            "order");
+    QA_TRY(cudaStreamSynchronize(st), "order");  // shared scratch (see qa_minmax_f32)
     return QA_OK;
 }
 
@@ -976,10 +980,19 @@ int qa_merge_topk(const double *in_scores, const int32_t *in_ids, int64_t G, int
                   int64_t kin, int64_t k, double *out_scores, int32_t *out_ids, void *stream) {
     if (G < 1 || nq < 0 || kin < 0 || k < 0) return set_err(QA_EINVAL, "bad shape");
     if (k > G * kin) return set_err(QA_EINVAL, "k exceeds the number of merged entries");
-    if (k > kMaxK) return set_err(QA_EUNSUPPORTED, "k above this build's limit");
-    QA_TRY(launch_merge(in_scores, in_ids, G, nq, kin, k, out_scores, out_ids,
-                        (cudaStream_t)stream),
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t need = merge_scratch_bytes(G, nq, kin, k);
+    if (need == 0) {
+        QA_TRY(launch_merge(in_scores, in_ids, G, nq, kin, k, out_scores, out_ids, st), "merge");
+        return QA_OK;
+    }
+    // large k: merge-path tree through a workspace buffer
+    Workspace &ws = g_ws[current_device() % kMaxDevices];
+    std::lock_guard<std::mutex> lock(ws.mu);
+    QA_TRY(ws.merge.reserve(need), "workspace");
+    QA_TRY(launch_merge(in_scores, in_ids, G, nq, kin, k, out_scores, out_ids, st, ws.merge.ptr),
            "merge");
+    QA_TRY(cudaStreamSynchronize(st), "merge");  // the buffer is shared per device
     return QA_OK;
 }
 

@@ -23,6 +23,7 @@
 //                  and bitonic-sorts state + survivors in shared memory.
 // The orchestration (rounds of kF32Rows rows, query chunks) is in qa_api.cu.
 #include <cstdint>
+#include <cub/device/device_segmented_radix_sort.cuh>
 #include <cuda_runtime.h>
 
 #include "qa_common.cuh"
@@ -251,6 +252,37 @@ __global__ void f32_finalize_kernel(const double *__restrict__ st_s, const int32
     out_i[t] = (int32_t)(st_i[t] + id_offset);
 }
 
+// Any k (keff beyond the shared-memory select): every score of a query
+// chunk, sorted per query by (score, id) with a stable segmented radix sort.
+// Keys are order-preserving u64 maps of score + 0.0 (so -0.0 ties +0.0, the
+// reference's double compare), values the row ids in ascending order -- the
+// stable sort keeps ties in id order.
+__global__ void fullsort_keys_kernel(const double *__restrict__ scores, int64_t total, int64_t n,
+                                     unsigned long long *__restrict__ keys,
+                                     int32_t *__restrict__ vals) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= total) return;
+    keys[t] = skey_from_double(scores[t] + 0.0);
+    vals[t] = (int32_t)(t % n);
+}
+
+__global__ void fullsort_out_kernel(const double *__restrict__ scores,
+                                    const int32_t *__restrict__ vals, int64_t m, int64_t n,
+                                    int64_t keff, int64_t id_offset, double *__restrict__ out_s,
+                                    int32_t *__restrict__ out_i) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m * keff) return;
+    const int64_t q = t / keff, j = t - q * keff;
+    const int32_t id = vals[q * n + j];
+    out_s[t] = scores[q * n + id];  // the score itself (keeps -0.0)
+    out_i[t] = (int32_t)(id + id_offset);
+}
+
+__global__ void fullsort_offsets_kernel(int64_t m, int64_t n, int64_t *__restrict__ off) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t <= m) off[t] = t * n;
+}
+
 // (float)sqrt(sequential float64 sum of x^2), one thread per row
 __global__ void norms_f32_kernel(const float *__restrict__ x, int64_t n, int64_t d, int64_t ldx,
                                  float *__restrict__ out) {
@@ -322,6 +354,55 @@ cudaError_t launch_norms_f32(const float *x, int64_t n, int64_t d, int64_t ldx, 
                              cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     norms_f32_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(x, n, d, ldx, out);
+    return cudaGetLastError();
+}
+
+}  // namespace qa
+
+namespace qa {
+
+size_t f32_fullsort_bytes(int64_t m, int64_t n) {
+    // scores (8) + keys in/out (16) + values in/out (8) per (query, row),
+    // offsets, and CUB's temporary storage
+    size_t temp = 0;
+    const int64_t total = m * n;
+    cub::DeviceSegmentedRadixSort::SortPairs(nullptr, temp, (unsigned long long *)nullptr,
+                                             (unsigned long long *)nullptr, (int32_t *)nullptr,
+                                             (int32_t *)nullptr, total, (int)m,
+                                             (int64_t *)nullptr, (int64_t *)nullptr);
+    return (size_t)total * 32 + (size_t)(m + 1) * 8 + temp + 1024;
+}
+
+cudaError_t launch_f32_fullsort(const float *db, int64_t ldd, const float *q, int64_t ldq,
+                                int64_t d, int64_t m, int64_t n, int metric, const float *db_norm,
+                                const float *q_norm, int64_t keff, int64_t id_offset,
+                                double *out_s, int32_t *out_i, void *scratch, size_t bytes,
+                                cudaStream_t st) {
+    if (m == 0 || n == 0 || keff == 0) return cudaSuccess;
+    if (bytes < f32_fullsort_bytes(m, n)) return cudaErrorInvalidValue;
+    const int64_t total = m * n;
+    char *p = (char *)scratch;
+    auto take = [&](size_t b) {
+        char *r = p;
+        p += (b + 255) / 256 * 256;
+        return r;
+    };
+    double *sc = (double *)take((size_t)total * 8);
+    unsigned long long *k_in = (unsigned long long *)take((size_t)total * 8);
+    unsigned long long *k_out = (unsigned long long *)take((size_t)total * 8);
+    int32_t *v_in = (int32_t *)take((size_t)total * 4);
+    int32_t *v_out = (int32_t *)take((size_t)total * 4);
+    int64_t *off = (int64_t *)take((size_t)(m + 1) * 8);
+    size_t temp = (size_t)((char *)scratch + bytes - p);
+    cudaError_t e = launch_f32_scores(db, ldd, q, ldq, d, m, 0, n, metric, db_norm, q_norm, sc, n, st);
+    if (e != cudaSuccess) return e;
+    fullsort_keys_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(sc, total, n, k_in, v_in);
+    fullsort_offsets_kernel<<<(unsigned)((m + 256) / 256), 256, 0, st>>>(m, n, off);
+    e = cub::DeviceSegmentedRadixSort::SortPairs(p, temp, k_in, k_out, v_in, v_out, total, (int)m,
+                                                 off, off + 1, 0, 64, st);
+    if (e != cudaSuccess) return e;
+    fullsort_out_kernel<<<(unsigned)((m * keff + 255) / 256), 256, 0, st>>>(sc, v_out, m, n, keff,
+                                                                          id_offset, out_s, out_i);
     return cudaGetLastError();
 }
 

@@ -131,9 +131,11 @@ cudaError_t launch_order_by_key(const int32_t *key, int64_t n, bool stratify, in
 cudaError_t launch_permute_rows(const int8_t *src, const int32_t *sq_in, const float *n_in,
                                 int64_t n, int64_t ld, const int32_t *perm, int8_t *dst,
                                 int32_t *sq_out, float *n_out, cudaStream_t st);
+// scratch bytes launch_merge needs (0: the shared-memory merge serves k)
+size_t merge_scratch_bytes(int64_t G, int64_t nq, int64_t kin, int64_t k);
 cudaError_t launch_merge(const double *in_scores, const int32_t *in_ids, int64_t G, int64_t nq,
                          int64_t kin, int64_t k, double *out_scores, int32_t *out_ids,
-                         cudaStream_t st);
+                         cudaStream_t st, void *scratch = nullptr);
 
 // float32 exhaustive search (qa_exact_f32.cu), bit-exact with _scan_f32.
 cudaError_t launch_f32_scores(const float *db, int64_t ldd, const float *q, int64_t ldq, int64_t d,
@@ -148,6 +150,14 @@ cudaError_t launch_f32_finalize(const double *st_s, const int32_t *st_i, int64_t
 cudaError_t launch_norms_f32(const float *x, int64_t n, int64_t d, int64_t ldx, float *out,
                              cudaStream_t st);
 size_t f32_select_smem(int64_t k);
+// any k: all n scores of m queries sorted per query (CUB segmented radix sort);
+// scratch of f32_fullsort_bytes(m, n) bytes
+size_t f32_fullsort_bytes(int64_t m, int64_t n);
+cudaError_t launch_f32_fullsort(const float *db, int64_t ldd, const float *q, int64_t ldq,
+                                int64_t d, int64_t m, int64_t n, int metric, const float *db_norm,
+                                const float *q_norm, int64_t keff, int64_t id_offset,
+                                double *out_s, int32_t *out_i, void *scratch, size_t bytes,
+                                cudaStream_t st);
 
 // estimate_stats (qa_stats.cu): x on the device, every output on the HOST;
 // synchronous on st.  qlo/qhi: the trimming quantiles per dimension.

@@ -16,6 +16,7 @@
 // a binary-search count in the other list).
 #include <cfloat>
 #include <cstdlib>
+#include <vector>
 
 #include "qa_common.cuh"
 #include "qa_internal.h"
@@ -628,6 +629,54 @@ __global__ void __launch_bounds__(256) merge_kernel(const double *__restrict__ i
     }
 }
 
+// Large k: merge two per-query sorted lists A [nq, la] and B [nq, lb] (score,
+// id order) into the first k of their union, by merge path: an element's
+// output rank is its own index plus the count of the other list's elements
+// before it (A first on equal keys, so padding duplicates never collide).
+__device__ __forceinline__ bool mkey_less(double sa, int32_t ia, double sb, int32_t ib) {
+    const unsigned long long ka = skey_from_double(sa + 0.0), kb = skey_from_double(sb + 0.0);
+    return ka < kb || (ka == kb && ia < ib);
+}
+
+__global__ void merge_pair_kernel(const double *__restrict__ as, const int32_t *__restrict__ ai,
+                                  int64_t la, int64_t lda, const double *__restrict__ bs,
+                                  const int32_t *__restrict__ bi, int64_t lb, int64_t ldb,
+                                  int64_t k, double *__restrict__ os, int32_t *__restrict__ oi,
+                                  int64_t ldo) {
+    const int64_t q = blockIdx.y;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= la + lb) return;
+    const double *A = as + q * lda, *B = bs + q * ldb;
+    const int32_t *Ai = ai + q * lda, *Bi = bi + q * ldb;
+    double x;
+    int32_t xi;
+    int64_t r;
+    if (t < la) {
+        x = A[t];
+        xi = Ai[t];
+        int64_t lo = 0, hi = lb;  // #{B < x}
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (mkey_less(B[mid], Bi[mid], x, xi)) lo = mid + 1; else hi = mid;
+        }
+        r = t + lo;
+    } else {
+        const int64_t j = t - la;
+        x = B[j];
+        xi = Bi[j];
+        int64_t lo = 0, hi = la;  // #{A <= x}
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (!mkey_less(x, xi, A[mid], Ai[mid])) lo = mid + 1; else hi = mid;
+        }
+        r = j + lo;
+    }
+    if (r < k) {
+        os[q * ldo + r] = x;
+        oi[q * ldo + r] = xi;
+    }
+}
+
 int pow2_at_least(int64_t v, int64_t cap) {
     int64_t p = 32;
     while (p < v && p < cap) p <<= 1;
@@ -823,10 +872,59 @@ cudaError_t launch_finalize(const Entry *state, int64_t nq, int64_t k, int64_t k
     return cudaGetLastError();
 }
 
+size_t merge_scratch_bytes(int64_t G, int64_t nq, int64_t kin, int64_t k) {
+    if (k <= kMaxK && k + kin <= kSortMax) return 0;
+    const int64_t len = std::min<int64_t>(k, 2 * kin);
+    return (size_t)2 * ((G + 1) / 2) * nq * len * 12 + 256;
+}
+
 cudaError_t launch_merge(const double *in_scores, const int32_t *in_ids, int64_t G, int64_t nq,
                          int64_t kin, int64_t k, double *out_scores, int32_t *out_ids,
-                         cudaStream_t st) {
+                         cudaStream_t st, void *scratch) {
     if (nq == 0 || k == 0) return cudaSuccess;
+    if (k > kMaxK || k + kin > kSortMax) {
+        // pairwise merge-path tree; level buffers [lists, nq, len] x 2 in scratch
+        if (!scratch) return cudaErrorInvalidValue;
+        const int64_t cap = std::min<int64_t>(k, 2 * kin);
+        const int64_t half = (G + 1) / 2;
+        double *bs[2] = {(double *)scratch, (double *)scratch + half * nq * cap};
+        int32_t *bi[2] = {(int32_t *)(bs[1] + half * nq * cap),
+                          (int32_t *)(bs[1] + half * nq * cap) + half * nq * cap};
+        const double *cs = in_scores;
+        const int32_t *ci = in_ids;
+        std::vector<int64_t> lens((size_t)G, kin);  // valid entries per list
+        int64_t ld = kin;
+        int buf = 0;
+        while (true) {
+            const int64_t lists = (int64_t)lens.size();
+            const bool last = lists <= 2;
+            const int64_t nlen = last ? k : cap;
+            double *os = last ? out_scores : bs[buf];
+            int32_t *oi = last ? out_ids : bi[buf];
+            const int64_t ldo = nlen;
+            std::vector<int64_t> nl;
+            for (int64_t p = 0; 2 * p < lists; ++p) {
+                const int64_t a0 = 2 * p, b0 = 2 * p + 1;
+                const int64_t la = lens[a0], lb = b0 < lists ? lens[b0] : 0;
+                const int64_t outn = std::min<int64_t>(nlen, la + lb);
+                dim3 grid((unsigned)((la + lb + 255) / 256), (unsigned)nq);
+                merge_pair_kernel<<<grid, 256, 0, st>>>(
+                    cs + a0 * nq * ld, ci + a0 * nq * ld, la, ld,
+                    cs + (b0 < lists ? b0 : a0) * nq * ld, ci + (b0 < lists ? b0 : a0) * nq * ld,
+                    lb, ld, outn, os + p * nq * ldo, oi + p * nq * ldo, ldo);
+                nl.push_back(outn);
+            }
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+            if (last) break;
+            cs = os;
+            ci = oi;
+            lens.swap(nl);
+            ld = ldo;
+            buf ^= 1;
+        }
+        return cudaSuccess;
+    }
     const int sz = pow2_at_least(k + kin, kSortMax);
     const size_t smem = (size_t)sz * sizeof(MEntry);
     cudaError_t e = cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

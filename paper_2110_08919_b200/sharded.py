@@ -10,7 +10,8 @@ and every rank reports exactly min(k, shard rows) entries in that order,
 the merge equals the single-GPU result bit for bit.
 
 The exchange is the only collective on the data path: k candidates per
-query per rank (nq * k * 12 bytes), independent of n.
+query per rank (nq * k * 12 bytes, scores and ids packed into ONE byte
+buffer so a batch costs one all-gather), independent of n.
 """
 
 from __future__ import annotations
@@ -29,16 +30,22 @@ def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def gather_topk(scores: torch.Tensor, ids: torch.Tensor, group=None):
-    """All-gather per-rank [nq, kin] lists into [world, nq, kin] tensors.
+    """All-gather per-rank [nq, kin] lists into [world, nq, kin] tensors with
+    one collective: float64 scores and int32 ids travel as one packed
+    [nq, kin * 12] byte row per query.
 
     Every rank must pass the same kin (ranks whose shard has fewer rows pad
     with +inf scores / INT32_MAX ids, which sort last)."""
     world = dist.get_world_size(group)
-    s_all = [torch.empty_like(scores) for _ in range(world)]
-    i_all = [torch.empty_like(ids) for _ in range(world)]
-    dist.all_gather(s_all, scores.contiguous(), group=group)
-    dist.all_gather(i_all, ids.contiguous(), group=group)
-    return torch.stack(s_all), torch.stack(i_all)
+    nq, kin = scores.shape
+    packed = torch.cat([scores.contiguous().view(torch.uint8).reshape(nq, kin * 8),
+                        ids.contiguous().view(torch.uint8).reshape(nq, kin * 4)], dim=1)
+    parts = [torch.empty_like(packed) for _ in range(world)]
+    dist.all_gather(parts, packed, group=group)
+    allp = torch.stack(parts)  # [world, nq, kin * 12]
+    s_all = allp[:, :, : kin * 8].contiguous().view(torch.float64).reshape(world, nq, kin)
+    i_all = allp[:, :, kin * 8:].contiguous().view(torch.int32).reshape(world, nq, kin)
+    return s_all, i_all
 
 
 def pad_topk(scores: torch.Tensor, ids: torch.Tensor, kin: int):

@@ -321,26 +321,27 @@ def test_ground_truth_and_recall_cfg_minis(golden_cfg, cfg):
 
 # ------------------------------------------------------------ sharding --
 
-@pytest.mark.parametrize("G", [2, 3, 8])
-def test_virtual_shards_merge_equals_full(oracle, G):
+@pytest.mark.parametrize("G,k", [(2, 100), (3, 100), (8, 100), (3, 3000), (5, 2500)])
+def test_virtual_shards_merge_equals_full(oracle, G, k):
+    # k > 2048: the merge-path tree (shared-memory merge beyond its limit)
     from paper_2110_08919_b200.sharded import pad_topk, shard_bounds
 
-    rng = np.random.default_rng(G)
+    rng = np.random.default_rng(G + k)
     X = _rand_codes(rng, 10_007, 32, -6, 7, nonzero=True)   # many ties across shards
-    Q = _rand_codes(rng, 40, 32, -6, 7, nonzero=True)
+    Q = _rand_codes(rng, 40 if k <= 100 else 6, 32, -6, 7, nonzero=True)
     for metric in (0, 1, 2):
         db = dev.DeviceCodes.from_host(X)
         qs = dev.DeviceCodes.from_host(Q)
-        kin = min(100, -(-X.shape[0] // G))
+        kin = min(k, -(-X.shape[0] // G))
         parts_s, parts_i = [], []
         for r in range(G):
             lo, hi = shard_bounds(X.shape[0], G, r)
-            s, i = dev.scan_topk(db.slice_rows(lo, hi), qs, 100, metric, id_offset=lo)
+            s, i = dev.scan_topk(db.slice_rows(lo, hi), qs, k, metric, id_offset=lo)
             s, i = pad_topk(s, i, kin)
             parts_s.append(s)
             parts_i.append(i)
-        ms, mi = dev.merge_topk(torch.stack(parts_s), torch.stack(parts_i), 100)
-        osc, oids = _scan_oracle(oracle, X, Q, 100, metric)
+        ms, mi = dev.merge_topk(torch.stack(parts_s), torch.stack(parts_i), k)
+        osc, oids = _scan_oracle(oracle, X, Q, k, metric)
         np.testing.assert_array_equal(mi.cpu().numpy(), oids)
         np.testing.assert_array_equal(ms.cpu().numpy(), osc)
 
@@ -463,9 +464,44 @@ def test_large_k_beyond_int8_select(oracle, metric):
         osc, oids = _scan_oracle(oracle, X, Q, k, metric)
         np.testing.assert_array_equal(ids.cpu().numpy(), oids + 3)
         np.testing.assert_array_equal(sc.cpu().numpy(), osc)
-    with pytest.raises(NotImplementedError):
-        big = dev.DeviceCodes.from_host(_rand_codes(rng, 20_000, 8))
-        dev.scan_topk(big, dev.DeviceCodes.from_host(_rand_codes(rng, 1, 8)), 16_000, metric)
+    # any k (reference: keff = min(k, n) for every k, _core.pyx:348-365):
+    # beyond the shared-memory select, every score is sorted per query
+    Xb = _rand_codes(rng, 20_000, 8, nonzero=True)
+    Qb = _rand_codes(rng, 3, 8, nonzero=True)
+    big = dev.DeviceCodes.from_host(Xb).sorted_by_norm()
+    for k in (16_000, 20_000, 25_000):
+        sc, ids = dev.scan_topk(big, dev.DeviceCodes.from_host(Qb), k, metric)
+        osc, oids = _scan_oracle(oracle, Xb, Qb, k, metric)
+        np.testing.assert_array_equal(ids.cpu().numpy(), oids)
+        np.testing.assert_array_equal(sc.cpu().numpy(), osc)
+
+
+@pytest.mark.parametrize("metric", [0, 1, 2])
+def test_any_k_float32_path(oracle, metric):
+    rng = np.random.default_rng(950 + metric)
+    X = rng.standard_normal((18_000, 9)).astype(np.float32)
+    X[::7] = X[3]  # ties
+    Q = rng.standard_normal((2, 9)).astype(np.float32)
+    xn, qn = oracle.norms_f32(X), oracle.norms_f32(Q)
+    sc, ids = _backend.scan_topk(X, Q, 17_000, metric, xn, qn)
+    osc, oids = oracle.scan_topk_f32(X, Q, 17_000, metric, xn, qn)
+    np.testing.assert_array_equal(ids, oids)
+    np.testing.assert_array_equal(sc, osc)
+
+
+@pytest.mark.parametrize("metric", [0, 1, 2])
+def test_rows_wider_than_int32_safe_bound(oracle, metric):
+    # d beyond the int32-exact worst case (L2: 33025, others: 131071) takes
+    # the float64-exact route; equal to the reference whenever its int32 sums
+    # do not wrap (small codes here)
+    rng = np.random.default_rng(990 + metric)
+    d = 33_100 if metric == 1 else 131_100
+    X = _rand_codes(rng, 300, d, -3, 4, nonzero=True)
+    Q = _rand_codes(rng, 2, d, -3, 4, nonzero=True)
+    sc, ids = _scan_gpu(X, Q, 20, metric, oracle.norms_i8(X), oracle.norms_i8(Q))
+    osc, oids = _scan_oracle(oracle, X, Q, 20, metric)
+    np.testing.assert_array_equal(ids, oids)
+    np.testing.assert_array_equal(sc, osc)
 
 
 def test_pair_distances_backend_and_module():

@@ -59,9 +59,9 @@ def test_invalid_arguments_map_to_reference_errors():
         _lib.check(L.qa_encode_i8(None, 1, 1, 1, None, None, None, 9, None, 32, None, None, None))
     with pytest.raises(ValueError, match="k exceeds"):
         _lib.check(L.qa_merge_topk(None, None, 2, 1, 3, 7, None, None, None))
-    with pytest.raises(NotImplementedError):
-        _lib.check(L.qa_scan_topk_i8(None, 30_000, 8, 32, None, None, None, None, 1, 32, None, None,
-                                     20_000, 0, 0, None, None, None))
+    with pytest.raises(NotImplementedError, match="int32 ids"):  # any k is served; n is not
+        _lib.check(L.qa_scan_topk_i8(None, 2**31 + 1, 8, 32, None, None, None, None, 1, 32, None,
+                                     None, 10, 0, 0, None, None, None))
     # empty problems are valid no-ops (_core.pyx:352-353)
     _lib.check(L.qa_scan_topk_i8(None, 0, 4, 32, None, None, None, None, 3, 32, None, None, 5, 0, 0,
                                  None, None, None))

@@ -78,19 +78,21 @@ def _worker(rank, world, port, X, Q, k, metric, out):
 
 
 @pytest.mark.parametrize("metric", [0, 1, 2])
-def test_two_rank_gloo_merge_equals_full_scan(oracle, metric):
-    rng = np.random.default_rng(40 + metric)
-    X = rng.integers(-4, 5, size=(1001, 12)).astype(np.int8)   # many ties
+@pytest.mark.parametrize("world,n,k", [(2, 1001, 50), (3, 1001, 50), (3, 100, 50)])
+def test_gloo_merge_equals_full_scan(oracle, metric, world, n, k):
+    # world 3: uneven shards (334/334/333); n=100, k=50: every shard holds
+    # fewer than k rows, so its list is padded before the exchange
+    rng = np.random.default_rng(40 + metric + world)
+    X = rng.integers(-4, 5, size=(n, 12)).astype(np.int8)   # many ties
     X[~X.any(axis=1), 0] = 1
     Q = rng.integers(-4, 5, size=(7, 12)).astype(np.int8)
     Q[~Q.any(axis=1), 0] = 1
-    k = 50
     manager = mp.Manager()
     out = manager.dict()
-    mp.start_processes(_worker, args=(2, _free_port(), X, Q, k, metric, out), nprocs=2,
+    mp.start_processes(_worker, args=(world, _free_port(), X, Q, k, metric, out), nprocs=world,
                        join=True, start_method="fork")
     want_s, want_i = oracle.scan_topk_i8(X, Q, k, metric, oracle.norms_i8(X), oracle.norms_i8(Q))
-    for rank in range(2):
+    for rank in range(world):
         s, i = out[rank]
         np.testing.assert_array_equal(i, want_i)
         np.testing.assert_array_equal(s, want_s)
