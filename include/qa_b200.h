@@ -117,6 +117,22 @@ int qa_scan_topk_i8(const int8_t *db, int64_t n, int64_t d, int64_t ldd,
                     int64_t k, int metric, int64_t id_offset,
                     double *out_scores, int32_t *out_ids, void *stream);
 
+/* Asynchronous form of qa_scan_topk_i8 (same arguments and results): returns
+ * once the search is enqueued on `stream`, with no host synchronisation.
+ * Queries whose candidate list overflowed or whose threshold estimate failed
+ * are recomputed on the device (a full exact scan, still in stream order), so
+ * the outputs are final when the stream reaches them.  Differences: a zero
+ * angular norm is not reported (callers check norms, as exact.py does), and
+ * the per-call candidate statistics are not collected.  Calls sharing a
+ * device's workspace must use one stream. */
+int qa_scan_topk_i8_async(const int8_t *db, int64_t n, int64_t d, int64_t ldd,
+                          const int32_t *db_sqnorm, const float *db_norm,
+                          const int32_t *row_ids,
+                          const int8_t *q, int64_t nq, int64_t ldq,
+                          const int32_t *q_sqnorm, const float *q_norm,
+                          int64_t k, int metric, int64_t id_offset,
+                          double *out_scores, int32_t *out_ids, void *stream);
+
 /* Host-buffer form of the reference call scan_topk(data, queries, k, metric,
  * data_norms, query_norms) for int8 inputs: data[n, d] and queries[nq, d]
  * C-contiguous int8 in HOST memory; data_norms/query_norms host float32,

@@ -65,6 +65,11 @@ SIGNATURES = {
         [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp,
          c_i64, c_int, c_i64, c_vp, c_vp, c_vp],
     ),
+    "qa_scan_topk_i8_async": (
+        c_int,
+        [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp,
+         c_i64, c_int, c_i64, c_vp, c_vp, c_vp],
+    ),
     "qa_order_rows_by_norm": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp]),
     "qa_permute_rows_i8": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "qa_scan_topk_i8_host": (

@@ -64,8 +64,9 @@ struct EventTimer {
         if (!g_profiling) return;
         cudaEventRecord(next(), st);
     }
-    // call after the stream is synchronised
+    // sums the recorded spans into s (waits for the last event) and resets
     void accumulate(qa_scan_stats &s) {
+        if (used > 0) cudaEventSynchronize(pool[used - 1]);
         for (auto &sp : spans) {
             float ms = 0.f;
             cudaEventElapsedTime(&ms, pool[sp.second], pool[sp.second + 1]);
@@ -136,6 +137,7 @@ struct Workspace {
     Buf f32_x, f32_q, f32_xn;                // codes as float32 (large k / wide rows)
     Buf r_idx, r_q, r_qsq, r_qn, r_s, r_ids;  // overflow retry
     Buf merge;                                // large-k shard merge
+    Buf repair;                               // device-side recompute (async scans)
 };
 
 constexpr int kMaxDevices = 64;
@@ -307,7 +309,7 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
               const int32_t *q_sqnorm,
               const float *q_norm, int64_t keff, int metric, int64_t id_offset,
               double *out_scores, int32_t *out_ids, int64_t cap_min, bool allow_estimate,
-              cudaStream_t st, std::vector<int32_t> *overflowed) {
+              cudaStream_t st, std::vector<int32_t> *overflowed, bool async_ = false) {
     ScanPlan pl = plan_scan(n, nq, keff, cap_min, allow_estimate);
     const int64_t qc = pl.qchunk;
     QA_TRY(ws.state.reserve((size_t)qc * keff * sizeof(Entry)), "workspace");
@@ -348,7 +350,7 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
                "init");
         int pass = 0;  // filter passes of this chunk (work-unit counter slot)
         g_stats.launches += 1;
-        if (c0 == 0 && metric == kAngular) {
+        if (c0 == 0 && metric == kAngular && !async_) {
             zero_norm_kernel<<<(unsigned)((n + nq + 255) / 256), 256, 0, st>>>(db_norm, n, q_norm,
                                                                                nq, flags + 2);
             QA_TRY(cudaGetLastError(), "norm check");
@@ -524,6 +526,17 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
                "finalize");
         g_stats.launches += 1;
     }
+    overflowed->clear();
+    if (async_) {
+        // no host round trip: the flagged queries (overflow, failed estimate
+        // check) are recomputed on the device, in stream order
+        QA_TRY(ws.repair.reserve(repair_scratch_bytes(n, nq, keff)), "workspace");
+        RepairArgs rp{db, n, ld, db_sqnorm, db_norm, row_ids, q, nq, q_sqnorm, q_norm, keff,
+                      metric, id_offset, ovf, out_scores, out_ids, ws.repair.ptr};
+        QA_TRY(launch_repair(rp, st), "repair");
+        g_stats.launches += 2;
+        return QA_OK;
+    }
     int32_t hflags[6] = {0, 0, 0, 0, 0, 0};
     QA_TRY(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, st),
            "overflow check");
@@ -535,7 +548,6 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
     std::memcpy(&cands, hflags + 4, sizeof(cands));
     g_stats.candidates += (int64_t)cands;
     g_timer.accumulate(g_stats);
-    overflowed->clear();
     if (any) {
         std::vector<int32_t> h(nq);
         QA_TRY(cudaMemcpy(h.data(), ovf, (size_t)nq * 4, cudaMemcpyDeviceToHost), "overflow list");
@@ -613,7 +625,8 @@ __global__ void codes_to_f32_kernel(const int8_t *__restrict__ codes, int64_t n,
 int scan_entry(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_t *db_sqnorm,
                const float *db_norm, const int32_t *row_ids, const int8_t *q, int64_t nq, int64_t ldq,
                const int32_t *q_sqnorm, const float *q_norm, int64_t k, int metric,
-               int64_t id_offset, double *out_scores, int32_t *out_ids, cudaStream_t st) {
+               int64_t id_offset, double *out_scores, int32_t *out_ids, cudaStream_t st,
+               bool async_ = false) {
     g_stats = qa_scan_stats{};
     if (metric < 0 || metric > 2) return set_err(QA_EINVAL, "unknown metric %d", metric);
     if (k < 0) return set_err(QA_EINVAL, "k must be >= 0");
@@ -670,9 +683,9 @@ int scan_entry(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_
         return QA_OK;
     }
     std::vector<int32_t> ovf;
-    g_timer.reset();
+    if (!async_) g_timer.reset();
     int rc = scan_impl(ws, db, n, d, ld, db_sqnorm, db_norm, row_ids, q, nq, q_sqnorm, q_norm, keff, metric,
-                       id_offset, out_scores, out_ids, 0, true, st, &ovf);
+                       id_offset, out_scores, out_ids, 0, true, st, &ovf, async_);
     if (rc != QA_OK) return rc;
     int64_t cap = plan_scan(n, nq, keff, 0, true).cap;
     while (!ovf.empty()) {
@@ -784,11 +797,13 @@ int qa_last_scan_stats(qa_scan_stats *out) {
 
 int qa_scan_totals(qa_scan_stats *out) {
     if (!out) return set_err(QA_EINVAL, "null stats pointer");
+    g_timer.accumulate(g_totals);  // timing spans of asynchronous scans
     *out = g_totals;
     return QA_OK;
 }
 
 int qa_reset_scan_totals(void) {
+    g_timer.reset();
     g_totals = qa_scan_stats{};
     return QA_OK;
 }
@@ -835,6 +850,18 @@ int qa_scan_topk_i8(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const i
     const int rc = scan_entry(db, n, d, ldd, db_sqnorm, db_norm, row_ids, q, nq, ldq, q_sqnorm,
                               q_norm, k, metric, id_offset, out_scores, out_ids,
                               (cudaStream_t)stream);
+    add_totals();
+    return rc;
+}
+
+int qa_scan_topk_i8_async(const int8_t *db, int64_t n, int64_t d, int64_t ldd,
+                          const int32_t *db_sqnorm, const float *db_norm, const int32_t *row_ids,
+                          const int8_t *q, int64_t nq, int64_t ldq, const int32_t *q_sqnorm,
+                          const float *q_norm, int64_t k, int metric, int64_t id_offset,
+                          double *out_scores, int32_t *out_ids, void *stream) {
+    const int rc = scan_entry(db, n, d, ldd, db_sqnorm, db_norm, row_ids, q, nq, ldq, q_sqnorm,
+                              q_norm, k, metric, id_offset, out_scores, out_ids,
+                              (cudaStream_t)stream, true);
     add_totals();
     return rc;
 }

@@ -95,6 +95,31 @@ struct SelectArgs {
 };
 
 cudaError_t launch_select(const SelectArgs &a, cudaStream_t st);
+
+// Device-side exact recompute of the flagged queries (flag[q] != 0) of a
+// search: a full scan per flagged query, results into out_* (qa_select.cu).
+struct RepairArgs {
+    const int8_t *db;
+    int64_t n, ld;
+    const int32_t *db_sqnorm;
+    const float *db_norm;
+    const int32_t *row_ids;
+    const int8_t *q;
+    int64_t nq;
+    const int32_t *q_sqnorm;
+    const float *q_norm;
+    int64_t keff;
+    int metric;
+    int64_t id_offset;
+    const int32_t *flag;
+    double *out_scores;
+    int32_t *out_ids;
+    // workspace (repair_scratch_bytes): compacted flag list, counters, the
+    // per-part partial lists
+    void *scratch;
+};
+size_t repair_scratch_bytes(int64_t n, int64_t nq, int64_t keff);
+cudaError_t launch_repair(const RepairArgs &r, cudaStream_t st);
 cudaError_t launch_init_state(int32_t *state_cnt, int32_t *thr, int64_t nq, int metric,
                               cudaStream_t st);
 cudaError_t launch_fill(int32_t *p, int64_t n, int32_t v, cudaStream_t st);

@@ -677,6 +677,269 @@ __global__ void merge_pair_kernel(const double *__restrict__ as, const int32_t *
     }
 }
 
+
+// ------------------------------------------------------------ repair --
+//
+// Device-side recompute of the queries a search flagged (candidate list
+// overflow or a failed threshold-estimate check; flag[q] != 0), so that an
+// asynchronous search needs no host round trip.  Two launches, both cheap
+// when nothing is flagged:
+//   compact   flagged query list + count (one CTA);
+//   partial   work items (flagged query f < min(count, kRepMaxQ), row part p
+//             of P): every row of the part is scored exactly (dp4a int32
+//             dots, the float64 scores of make_entry) and a sorted top-keff
+//             kept in shared memory; the partial list goes to scratch, and
+//             the LAST part to finish for f merges the P lists (merge-path
+//             levels, in scratch) into the query's output row.  Flagged
+//             queries beyond kRepMaxQ are scanned whole by one CTA each
+//             (pathological inputs only: slow, still exact).
+// Exact by construction: every row of a flagged query is scored.
+constexpr int kRepChunk = 1024;
+constexpr int kRepThreads = 256;
+constexpr int kRepMaxQ = 64;       // flagged queries repaired part-parallel
+constexpr int kRepMaxParts = 128;
+
+__device__ __forceinline__ int32_t rep_dot(const int8_t *__restrict__ x, const int8_t *__restrict__ q,
+                                           int64_t ld) {
+    const int4 *x4 = reinterpret_cast<const int4 *>(x);
+    const int4 *q4 = reinterpret_cast<const int4 *>(q);
+    int32_t acc = 0;
+    for (int64_t w = 0; w < (ld >> 4); ++w) {
+        const int4 a = __ldg(x4 + w), b = __ldg(q4 + w);
+        acc = __dp4a(a.x, b.x, acc);
+        acc = __dp4a(a.y, b.y, acc);
+        acc = __dp4a(a.z, b.z, acc);
+        acc = __dp4a(a.w, b.w, acc);
+    }
+    return acc;
+}
+
+int rep_parts(int64_t n) {
+    int64_t P = n / 8192;
+    if (P < 1) P = 1;
+    if (P > kRepMaxParts) P = kRepMaxParts;
+    return (int)P;
+}
+
+struct RepLayout {
+    int32_t *flist, *count, *done;
+    double *ps;      // [kRepMaxQ][P][keff] partial scores, then merge levels
+    int32_t *pi;
+    double *ms;      // [kRepMaxQ][P/2 + 1][keff] merge ping-pong
+    int32_t *mi;
+};
+
+__host__ __device__ inline RepLayout rep_layout(void *scratch, int64_t nq, int64_t keff, int P) {
+    RepLayout L;
+    char *c = (char *)scratch;
+    auto take = [&](size_t b) {
+        char *r = c;
+        c += (b + 255) / 256 * 256;
+        return r;
+    };
+    L.flist = (int32_t *)take((size_t)nq * 4);
+    L.count = (int32_t *)take(8);
+    L.done = (int32_t *)take((size_t)kRepMaxQ * 4);
+    const size_t lists = (size_t)kRepMaxQ * P * keff, half = (size_t)kRepMaxQ * (P / 2 + 1) * keff;
+    L.ps = (double *)take(lists * 8);
+    L.pi = (int32_t *)take(lists * 4);
+    L.ms = (double *)take(half * 8);
+    L.mi = (int32_t *)take(half * 4);
+    return L;
+}
+
+__global__ void __launch_bounds__(1024) repair_compact_kernel(const int32_t *__restrict__ flag,
+                                                              int64_t nq, RepLayout L) {
+    __shared__ int base_s;
+    __shared__ int warp_cnt[32];
+    if (threadIdx.x == 0) base_s = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t c0 = 0; c0 < nq; c0 += 1024) {
+        const int64_t i = c0 + threadIdx.x;
+        const bool f = i < nq && flag[i] != 0;
+        const unsigned b = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) warp_cnt[warp] = __popc(b);
+        __syncthreads();
+        int before = 0;
+        for (int w = 0; w < warp; ++w) before += warp_cnt[w];
+        if (f) L.flist[base_s + before + __popc(b & ((1u << lane) - 1))] = (int32_t)i;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int w = 0; w < 32; ++w) tot += warp_cnt[w];
+            base_s += tot;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *L.count = base_s;
+    for (int i = threadIdx.x; i < kRepMaxQ; i += blockDim.x) L.done[i] = 0;
+}
+
+// top-keff of query q over rows [lo, hi) into state (shared memory); returns
+// the number kept.  Block-wide (all threads).
+template <int M>
+__device__ int rep_scan_rows(const RepairArgs &r, int64_t q, int64_t lo, int64_t hi, Entry *state,
+                             Entry *buf, Entry *tmp, int *buf_n) {
+    const int keff = (int)r.keff;
+    const int8_t *qrow = r.q + q * r.ld;
+    const int32_t qq = (M == kL2) ? r.q_sqnorm[q] : 0;
+    const float qn = (M == kAngular) ? r.q_norm[q] : 1.0f;
+    int cnt = 0;
+    for (int64_t c0 = lo; c0 < hi; c0 += kRepChunk) {
+        if (threadIdx.x == 0) *buf_n = 0;
+        __syncthreads();
+        const bool full = cnt == keff;
+        const Entry kth = full ? state[keff - 1] : Entry{~0ull, INT32_MAX, -1};
+        for (int i = threadIdx.x; i < kRepChunk && c0 + i < hi; i += blockDim.x) {
+            const int32_t row = (int32_t)(c0 + i);
+            const int32_t dot = rep_dot(r.db + (int64_t)row * r.ld, qrow, r.ld);
+            Entry e;
+            e.row = row;
+            e.id = r.row_ids ? __ldg(r.row_ids + row) : row;
+            if constexpr (M == kIP) {
+                e.skey = skey_from_int((int32_t)(0u - (uint32_t)dot));
+            } else if constexpr (M == kL2) {
+                e.skey = skey_from_int(
+                    (int32_t)((uint32_t)qq + (uint32_t)__ldg(r.db_sqnorm + row) - 2u * (uint32_t)dot));
+            } else {
+                e.skey = skey_from_double(angular_score(dot, qn, __ldg(r.db_norm + row)));
+            }
+            if (!full || entry_less(e, kth)) buf[atomicAdd(buf_n, 1)] = e;
+        }
+        __syncthreads();
+        const int ns = *buf_n;
+        if (ns == 0) continue;
+        int P = 2;
+        while (P < ns) P <<= 1;
+        for (int i = ns + threadIdx.x; i < P; i += blockDim.x) buf[i] = Entry{~0ull, INT32_MAX, -1};
+        __syncthreads();
+        block_bitonic_sort(buf, P, EntryLess());
+        const int newcnt = min(keff, cnt + ns);  // merge state + buf (ids unique)
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const int rk = i + count_less(buf, ns, state[i]);
+            if (rk < newcnt) tmp[rk] = state[i];
+        }
+        for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+            const int rk = i + count_less(state, cnt, buf[i]);
+            if (rk < newcnt) tmp[rk] = buf[i];
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < newcnt; i += blockDim.x) state[i] = tmp[i];
+        cnt = newcnt;
+        __syncthreads();
+    }
+    return cnt;
+}
+
+template <int M>
+__device__ __forceinline__ double rep_score(unsigned long long k) {
+    if constexpr (M == kIP) {
+        const int32_t v = int_from_skey(k);
+        return v == 0 ? -0.0 : (double)v;  // -(double)0 is -0.0 in _core.pyx:95
+    } else if constexpr (M == kL2) {
+        return (double)int_from_skey(k);
+    } else {
+        return double_from_skey(k);
+    }
+}
+
+template <int M>
+__global__ void __launch_bounds__(kRepThreads) repair_kernel(RepairArgs r, RepLayout L, int P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int keff = (int)r.keff;
+    Entry *state = reinterpret_cast<Entry *>(smem_raw);   // [keff]
+    Entry *buf = state + keff;                             // [kRepChunk]
+    Entry *tmp = buf + kRepChunk;                          // [keff]
+    __shared__ int buf_n, last_s;
+    const int count = *L.count;
+    const int fast = min(count, kRepMaxQ);
+    const int64_t items = (int64_t)fast * P + (count - fast);
+    for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+        if (w < (int64_t)fast * P) {
+            // part p of flagged query f
+            const int f = (int)(w / P), p = (int)(w % P);
+            const int64_t q = L.flist[f];
+            const int64_t lo = r.n * p / P, hi = r.n * (p + 1) / P;
+            const int cnt = rep_scan_rows<M>(r, q, lo, hi, state, buf, tmp, &buf_n);
+            double *os = L.ps + ((int64_t)f * P + p) * keff;
+            int32_t *oi = L.pi + ((int64_t)f * P + p) * keff;
+            for (int j = threadIdx.x; j < keff; j += blockDim.x) {
+                os[j] = j < cnt ? rep_score<M>(state[j].skey) : INFINITY;
+                oi[j] = j < cnt ? state[j].id : INT32_MAX;
+            }
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) last_s = atomicAdd(L.done + f, 1) == P - 1;
+            __syncthreads();
+            if (!last_s) continue;
+            __threadfence();
+            // the last part merges the P sorted lists of f, pairwise levels
+            const double *cs = L.ps + (int64_t)f * P * keff;
+            const int32_t *ci = L.pi + (int64_t)f * P * keff;
+            double *bs[2] = {L.ms + (int64_t)f * (P / 2 + 1) * keff, L.ps + (int64_t)f * P * keff};
+            int32_t *bi[2] = {L.mi + (int64_t)f * (P / 2 + 1) * keff, L.pi + (int64_t)f * P * keff};
+            int lists = P, pp = 0;
+            while (lists > 1) {
+                const int pairs = lists / 2, outl = pairs + (lists & 1);
+                double *ts = bs[pp];
+                int32_t *ti = bi[pp];
+                if (cs == ts) {  // never write over the level being read
+                    ts = bs[pp ^ 1];
+                    ti = bi[pp ^ 1];
+                }
+                for (int64_t t = threadIdx.x; t < (int64_t)lists * keff; t += blockDim.x) {
+                    const int li = (int)(t / keff), e = (int)(t % keff);
+                    const int pr = li >> 1, other = li ^ 1;
+                    const double x = cs[(int64_t)li * keff + e];
+                    const int32_t xi = ci[(int64_t)li * keff + e];
+                    int64_t rk = e;
+                    if (other < lists) {
+                        const double *O = cs + (int64_t)other * keff;
+                        const int32_t *Oi = ci + (int64_t)other * keff;
+                        int lo2 = 0, hi2 = keff;
+                        if (li & 1) {  // B side: #{A <= x}
+                            while (lo2 < hi2) {
+                                const int mid = (lo2 + hi2) >> 1;
+                                if (!mkey_less(x, xi, O[mid], Oi[mid])) lo2 = mid + 1; else hi2 = mid;
+                            }
+                        } else {       // A side: #{B < x}
+                            while (lo2 < hi2) {
+                                const int mid = (lo2 + hi2) >> 1;
+                                if (mkey_less(O[mid], Oi[mid], x, xi)) lo2 = mid + 1; else hi2 = mid;
+                            }
+                        }
+                        rk += lo2;
+                    }
+                    if (rk < keff) {
+                        ts[(int64_t)pr * keff + rk] = x;
+                        ti[(int64_t)pr * keff + rk] = xi;
+                    }
+                }
+                __syncthreads();
+                cs = ts;
+                ci = ti;
+                lists = outl;
+                pp ^= 1;
+            }
+            for (int j = threadIdx.x; j < keff; j += blockDim.x) {
+                r.out_scores[q * keff + j] = cs[j];
+                r.out_ids[q * keff + j] = (int32_t)(ci[j] + r.id_offset);
+            }
+            __syncthreads();
+        } else {
+            // flagged queries beyond kRepMaxQ: one CTA scans all rows
+            const int64_t q = L.flist[kRepMaxQ + (w - (int64_t)fast * P)];
+            const int cnt = rep_scan_rows<M>(r, q, 0, r.n, state, buf, tmp, &buf_n);
+            for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+                r.out_scores[q * keff + j] = rep_score<M>(state[j].skey);
+                r.out_ids[q * keff + j] = (int32_t)(state[j].id + r.id_offset);
+            }
+            __syncthreads();
+        }
+    }
+}
+
 int pow2_at_least(int64_t v, int64_t cap) {
     int64_t p = 32;
     while (p < v && p < cap) p <<= 1;
@@ -740,6 +1003,31 @@ cudaError_t launch_select(const SelectArgs &a_in, cudaStream_t st) {
         case kL2: return launch_select_t<kL2>(a, st);
         default: return launch_select_t<kAngular>(a, st);
     }
+}
+
+size_t repair_scratch_bytes(int64_t n, int64_t nq, int64_t keff) {
+    const int P = rep_parts(n);
+    const size_t lists = (size_t)kRepMaxQ * P * keff, half = (size_t)kRepMaxQ * (P / 2 + 1) * keff;
+    return (size_t)nq * 4 + 8 + kRepMaxQ * 4 + lists * 12 + half * 12 + 8 * 256;
+}
+
+cudaError_t launch_repair(const RepairArgs &r, cudaStream_t st) {
+    if (r.nq == 0 || r.keff == 0 || r.n == 0) return cudaSuccess;
+    if (r.keff > kMaxK || r.ld % 16 != 0 || !r.scratch) return cudaErrorNotSupported;
+    const int P = rep_parts(r.n);
+    const RepLayout L = rep_layout(r.scratch, r.nq, r.keff, P);
+    repair_compact_kernel<<<1, 1024, 0, st>>>(r.flag, r.nq, L);
+    const size_t smem = (size_t)(2 * r.keff + kRepChunk) * sizeof(Entry);
+    auto go = [&](auto kern) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        kern<<<(unsigned)(num_sms() * 2), kRepThreads, smem, st>>>(r, L, P);
+        return cudaGetLastError();
+    };
+    if (r.metric == kIP) return go(repair_kernel<kIP>);
+    if (r.metric == kL2) return go(repair_kernel<kL2>);
+    return go(repair_kernel<kAngular>);
 }
 
 cudaError_t launch_fill(int32_t *p, int64_t n, int32_t v, cudaStream_t st) {

@@ -168,13 +168,17 @@ def encode(x: torch.Tensor, k: torch.Tensor, sb: torch.Tensor, se: torch.Tensor,
 
 
 def scan_topk(db: DeviceCodes, q: DeviceCodes, k: int, metric: int, db_norm=None, q_norm=None,
-              id_offset: int = 0, out=None):
+              id_offset: int = 0, out=None, sync: bool = True):
     """Exhaustive top-k of every query over the database (_core.pyx:333-365).
 
     Returns (scores float64 [nq, keff], ids int32 [nq, keff]) on the device,
     rows ascending by (score, id), keff = min(k, n).  For the angular metric
     ``db_norm``/``q_norm`` (float32 device vectors) override the stored code
     norms, as the reference takes them from the caller.
+
+    ``sync=False``: qa_scan_topk_i8_async -- no host round trip; flagged
+    queries are recomputed on the device; a zero angular norm is not
+    reported (the caller's check).
     """
     if db.d != q.d:
         raise ValueError("dimension mismatch between data and queries")
@@ -194,9 +198,10 @@ def scan_topk(db: DeviceCodes, q: DeviceCodes, k: int, metric: int, db_norm=None
                                  f"float64/int32 on {dev}")
     dn = db.norm if db_norm is None else db_norm
     qn = q.norm if q_norm is None else q_norm
-    check(lib.qa_scan_topk_i8(_p(db.codes), db.n, db.d, db.ld, _p(db.sqnorm), _p(dn),
-                              _p(db.ids), _p(q.codes), q.n, q.ld, _p(q.sqnorm), _p(qn), int(k), int(metric),
-                              int(id_offset), _p(scores), _p(ids), _stream()))
+    fn = lib.qa_scan_topk_i8 if sync else lib.qa_scan_topk_i8_async
+    check(fn(_p(db.codes), db.n, db.d, db.ld, _p(db.sqnorm), _p(dn), _p(db.ids), _p(q.codes), q.n,
+             q.ld, _p(q.sqnorm), _p(qn), int(k), int(metric), int(id_offset), _p(scores), _p(ids),
+             _stream()))
     return scores, ids
 
 

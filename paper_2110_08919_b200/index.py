@@ -78,11 +78,19 @@ class Int8Index:
     def encode_queries(self, q: torch.Tensor, out: dev.DeviceCodes | None = None):
         return dev.encode(q, self.k_dev, self.sb_dev, self.se_dev, self.params.bits, out=out)
 
-    def search_codes(self, qc: dev.DeviceCodes, k: int, out=None):
-        """Angular with a zero code norm raises ZeroNorm (checked on the device
-        inside the scan, reference exact.py:67-69)."""
+    def search_codes(self, qc: dev.DeviceCodes, k: int, out=None, sync: bool | None = None):
+        """Top-k of the query codes, (scores f64, ids i32) on the device.
+
+        ``sync=False`` (the default for L2 and inner product) is the stream-
+        ordered search: no host round trip, queries that need a recompute are
+        redone on the device (qa_scan_topk_i8_async).  ``sync=True`` (the
+        default for angular) also reports a zero code norm as ZeroNorm
+        (checked on the device inside the scan, reference exact.py:67-69);
+        callers that guarantee nonzero vectors may pass ``sync=False``."""
+        if sync is None:
+            sync = self.metric == Metric.ANGULAR
         return dev.scan_topk(self.codes, qc, k, int(self.metric), id_offset=self.id_offset,
-                             out=out)
+                             out=out, sync=sync)
 
     def search(self, q: torch.Tensor, k: int):
         """fp32 query batch on the device -> (scores f64, ids i32) on the device."""

@@ -594,3 +594,58 @@ def test_acceptance_gate4_pipeline_matches_reference():
     np.testing.assert_array_equal(approx.ids, g["approx"])
     rec = qa.recall_at_k(gt, approx, 100).mean
     assert rec == float(g["recall"]) and rec >= 0.95
+
+
+# ------------------------------------------------- asynchronous search --
+
+@pytest.mark.parametrize("metric", [0, 1, 2])
+def test_async_search_repairs_overflow_on_device(oracle, metric):
+    # heavy ties overflow the candidate lists; the asynchronous entry has no
+    # host retry -- the flagged queries are recomputed by the device-side
+    # repair pass, in stream order
+    rng = np.random.default_rng(1300 + metric)
+    X = _rand_codes(rng, 60_000, 8, -2, 3, nonzero=True)
+    X[:20_000] = X[0]
+    Q = _rand_codes(rng, 300, 8, -2, 3, nonzero=True)
+    Q[:100] = X[0]
+    db = dev.DeviceCodes.from_host(X).sorted_by_norm()
+    qs = dev.DeviceCodes.from_host(Q)
+    for k in (10, 100, 700):
+        sc, ids = dev.scan_topk(db, qs, k, metric, id_offset=2, sync=False)
+        osc, oids = _scan_oracle(oracle, X, Q, k, metric)
+        np.testing.assert_array_equal(ids.cpu().numpy(), oids + 2)
+        np.testing.assert_array_equal(sc.cpu().numpy(), osc)
+
+
+@pytest.mark.parametrize("metric", [0, 1, 2])
+def test_async_search_repairs_failed_estimates(oracle, monkeypatch, metric):
+    # j = 1 makes the threshold estimate fail for many queries
+    monkeypatch.setenv("QA_B200_EST_ROWS", "2048")
+    monkeypatch.setenv("QA_B200_EST_J", "1")
+    rng = np.random.default_rng(1400 + metric)
+    X = _rand_codes(rng, 40_000, 64, -30, 31, nonzero=True)
+    Q = _rand_codes(rng, 300, 64, -30, 31, nonzero=True)
+    db = dev.DeviceCodes.from_host(X).sorted_by_norm()
+    qs = dev.DeviceCodes.from_host(Q)
+    sc, ids = dev.scan_topk(db, qs, 20, metric, sync=False)
+    osc, oids = _scan_oracle(oracle, X, Q, 20, metric)
+    np.testing.assert_array_equal(ids.cpu().numpy(), oids)
+    np.testing.assert_array_equal(sc.cpu().numpy(), osc)
+
+
+def test_async_index_batches_back_to_back(oracle):
+    # many stream-ordered searches without a host synchronisation between
+    # them, outputs into preallocated buffers (the serving loop)
+    X, Q = synth.generate(2, n=200_000, nq=3 * 300)
+    index = qa.Int8Index.build(torch.from_numpy(X).cuda(), qa.Metric.L2_SQUARED, "minmax")
+    qc = index.encode_queries(torch.from_numpy(Q).cuda())
+    outs = [(torch.empty((300, 100), dtype=torch.float64, device="cuda"),
+             torch.empty((300, 100), dtype=torch.int32, device="cuda")) for _ in range(3)]
+    for i in range(3):
+        index.search_codes(qc.slice_rows(300 * i, 300 * (i + 1)), 100, out=outs[i])
+    Xc = index.codes_in_input_order()
+    Qc = qc.to_host()
+    for i in range(3):
+        osc, oids = _scan_oracle(oracle, Xc, Qc[300 * i: 300 * i + 8], 100, 1)
+        np.testing.assert_array_equal(outs[i][1][:8].cpu().numpy(), oids)
+        np.testing.assert_array_equal(outs[i][0][:8].cpu().numpy(), osc)
