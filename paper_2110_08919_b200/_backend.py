@@ -56,14 +56,15 @@ def _check_pair(data, queries):
 # content fingerprint; writable arrays are never cached.  Forms:
 #
 #   "rows"  caller order (query batches; norms)
-#   "strat" index layout: stratified sample region, norm blocks (L2, IP)
-#   "ang"   index layout with plain norm bands (angular)
+#   "l2"    index layout: stratified sample region, norm blocks
+#   "ip"    index layout: a fixed pseudo-random row order
+#   "ang"   index layout with plain norm bands
 #
 # The index layouts (qa_layout.cu) are what the scan's threshold estimate and
 # per-unit bounds assume; ids still report caller rows (DeviceCodes.ids).
 
 _RESIDENT: dict = {}
-_FORM_OF_METRIC = {0: "strat", 1: "strat", 2: "ang"}
+_FORM_OF_METRIC = {0: "ip", 1: "l2", 2: "ang"}
 
 
 def _fingerprint(arr: np.ndarray) -> int:
@@ -75,7 +76,9 @@ def _fingerprint(arr: np.ndarray) -> int:
 def _make_form(base: _dev.DeviceCodes, form: str) -> _dev.DeviceCodes:
     if form == "rows":
         return base
-    return base.sorted_by_norm(stratify=form == "strat")
+    if form == "ip":
+        return base.shuffled()
+    return base.sorted_by_norm(stratify=form == "l2")
 
 
 def _resident(arr: np.ndarray, dev, form: str = "rows") -> _dev.DeviceCodes:

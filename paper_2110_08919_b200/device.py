@@ -114,6 +114,23 @@ class DeviceCodes:
         ids = None if self.ids is None else self.ids[lo:hi]
         return DeviceCodes(self.codes[lo:hi], self.d, self.sqnorm[lo:hi], self.norm[lo:hi], ids)
 
+    def shuffled(self, seed: int = 0) -> "DeviceCodes":
+        """Copy with rows in a fixed pseudo-random order (``ids`` map back):
+        any prefix is a uniform sample of the rows, which the scan's threshold
+        estimate assumes, whatever order the caller's rows come in."""
+        g = torch.Generator(device=self.device)
+        g.manual_seed(seed)
+        perm = torch.randperm(self.n, generator=g, device=self.device, dtype=torch.int64).to(torch.int32)
+        return self._permuted(perm)
+
+    def _permuted(self, perm: torch.Tensor) -> "DeviceCodes":
+        out = DeviceCodes.empty(self.n, self.d, self.device)
+        check(lib.qa_permute_rows_i8(_p(self.codes), _p(self.sqnorm), _p(self.norm), self.n,
+                                     self.ld, _p(perm), _p(out.codes), _p(out.sqnorm),
+                                     _p(out.norm), _stream()))
+        out.ids = perm if self.ids is None else self.ids[perm.long()]
+        return out
+
     def sorted_by_norm(self, stratify: bool = True) -> "DeviceCodes":
         """Copy with rows in ascending-norm order (stable) and ``ids`` mapping
         each stored row back to its position in this matrix.  The scan's
@@ -121,12 +138,7 @@ class DeviceCodes:
         perm = torch.empty((self.n,), dtype=torch.int32, device=self.device)
         check(lib.qa_order_rows_by_norm(_p(self.sqnorm), self.n, 1 if stratify else 0, _p(perm),
                                         _stream()))
-        out = DeviceCodes.empty(self.n, self.d, self.device)
-        check(lib.qa_permute_rows_i8(_p(self.codes), _p(self.sqnorm), _p(self.norm), self.n,
-                                     self.ld, _p(perm), _p(out.codes), _p(out.sqnorm),
-                                     _p(out.norm), _stream()))
-        out.ids = perm if self.ids is None else self.ids[perm.long()]
-        return out
+        return self._permuted(perm)
 
 
 def norms_(dc: DeviceCodes) -> None:

@@ -51,11 +51,18 @@ class Int8Index:
         codes = dev.encode(x, k, sb, se, params.bits)
         metric = Metric(metric)
         if sort_rows:
-            # a stratified sample region first (qa_layout.cu) -- the threshold
-            # estimate reads the first rows as a sample of the whole index, so
-            # clustered or sorted input must not reach it in caller order;
-            # angular norms are narrow and keep plain norm bands
-            codes = codes.sorted_by_norm(stratify=metric != Metric.ANGULAR)
+            # The threshold estimate reads the first rows as a sample of the
+            # whole index, so clustered or sorted input must not reach it in
+            # caller order.  L2: norm bands after a stratified sample region
+            # (qa_layout.cu; tight per-unit bounds); angular: plain norm bands
+            # (narrow norms); inner product: a fixed pseudo-random order -- its
+            # bound does not use norms, and norm strata starve the prefix of
+            # the high-norm rows where the best dots live (2.5x the
+            # candidates and failed estimates on cfg4 in norm order).
+            if metric == Metric.INNER_PRODUCT:
+                codes = codes.shuffled()
+            else:
+                codes = codes.sorted_by_norm(stratify=metric == Metric.L2_SQUARED)
         return cls(params, metric, codes, k, sb, se, id_offset)
 
     def codes_in_input_order(self) -> np.ndarray:

@@ -649,3 +649,21 @@ def test_async_index_batches_back_to_back(oracle):
         osc, oids = _scan_oracle(oracle, Xc, Qc[300 * i: 300 * i + 8], 100, 1)
         np.testing.assert_array_equal(outs[i][1][:8].cpu().numpy(), oids)
         np.testing.assert_array_equal(outs[i][0][:8].cpu().numpy(), osc)
+
+
+def test_ip_index_on_sorted_caller_rows_keeps_estimate(oracle):
+    # a caller corpus sorted by norm (clustered input) must not reach the
+    # threshold estimate in caller order: the IP index stores a fixed
+    # pseudo-random order, so no query needs the recompute
+    from paper_2110_08919_b200 import _lib
+
+    X, Q = synth.sift_like(300_000, 64, 128, 7)
+    X = X[np.argsort((X.astype(np.float64) ** 2).sum(1))[::-1]].copy()
+    index = qa.Int8Index.build(torch.from_numpy(X).cuda(), qa.Metric.INNER_PRODUCT, "minmax")
+    qc = index.encode_queries(torch.from_numpy(Q).cuda())
+    sc, ids = index.search_codes(qc, 10, sync=True)
+    assert _lib.last_scan_stats()["retries"] == 0
+    Xc = index.codes_in_input_order()
+    osc, oids = _scan_oracle(oracle, Xc, qc.to_host()[:6], 10, 0)
+    np.testing.assert_array_equal(ids[:6].cpu().numpy(), oids)
+    np.testing.assert_array_equal(sc[:6].cpu().numpy(), osc)

@@ -72,7 +72,9 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int reps, long long *c
             const uint32_t d = tmem + (uint32_t)((r & 1) * N);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
-                const uint64_t ad = make_desc128(a0 + kk * 32), bd = make_desc128(b0 + kk * 32);
+                // VAR 10: a different A tile every rep (4 tiles of the ring)
+                const uint32_t abase = VAR == 10 ? smem_u32(sS) + (uint32_t)((r & 3) * 16384) : a0;
+                const uint64_t ad = make_desc128(abase + kk * 32), bd = make_desc128(b0 + kk * 32);
                 if (KIND != 1)
                     asm volatile(
                         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -86,12 +88,12 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int reps, long long *c
                         "l"(ad), "l"(bd), "r"(idesc), "r"(kk)
                         : "memory");
             }
-            if (VAR >= 1 && VAR != 9)
+            if (VAR >= 1 && VAR < 9)
                 asm volatile(
                     "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                         smem_u32(&cbar[0]))
                     : "memory");
-            if (VAR >= 2 && VAR != 9) {
+            if (VAR >= 2 && VAR < 9) {
                 const uint64_t ad = (VAR == 2) ? make_desc32(a0) : make_desc128(a0);
                 const uint64_t bd = (VAR == 2) ? make_desc32(b0) : make_desc128(b0);
                 asm volatile(
@@ -170,7 +172,7 @@ void run(const char *name, int sms, const int8_t *src = nullptr, int tiles = 0) 
     double avg = 0;
     for (int i = 0; i < sms; ++i) avg += (double)h[i];
     avg /= sms;
-    const double mmas = ((VAR >= 2 && VAR != 9) ? 5.0 : 4.0) * reps;
+    const double mmas = ((VAR >= 2 && VAR < 9) ? 5.0 : 4.0) * reps;
     const double kmul = KIND != 1 ? 32 : 16;
     const double ops = 2.0 * 128 * N * kmul * mmas * sms;
     printf("%-6s%s N=%3d  %7.1f cycles/MMA  %8.1f T(FL)OP/s over %.3f ms  (%s)\n", name,
@@ -195,6 +197,9 @@ int main() {
     run<0, 160>("i8", sms);
     run<2, 224>("u8", sms, src, tiles);
     run<0, 256, 9>("i8rnd", sms);
+    run<0, 256, 10>("i8 A-rot", sms);
+    run<2, 224, 10>("u8 A-rot", sms);
+    run<0, 128, 10>("i8 A-rot", sms);
     run<2, 224, 9>("u8rnd", sms);
     run<0, 128, 9>("i8rnd", sms);
     run<0, 256, 1>("i8", sms);
