@@ -73,6 +73,8 @@ def parse_args():
     ap.add_argument("--k", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time eager launches instead of a CUDA-graph replay of the step")
     return ap.parse_args()
 
 
@@ -305,17 +307,16 @@ def run_gpu(args):
         for i, (a, b) in enumerate(spans):
             search_batch(i, q_dev[a:b])
 
-    launches_per_step = [0]
-
-    def timed(fn, steps):
-        times, launches = [], 0
+    def run_timed(fn, steps):
+        """CUDA-event time of `steps` calls of fn on the launching stream,
+        L2 flushed (256 MiB write) before each, max over ranks."""
+        times = []
         for _ in range(steps):
             flush.zero_()
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            _lib.reset_scan_totals()
             ev0.record(stream)
             fn()
             ev1.record(stream)
@@ -326,23 +327,51 @@ def run_gpu(args):
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 ms = float(t.item())
             times.append(ms)
-            tot = _lib.scan_totals()
-            # encode launches + the scan's own launches (+ merge per batch when sharded)
-            launches += len(spans) + tot["launches"] + (len(spans) if world > 1 else 0)
-        launches_per_step[0] = launches // max(1, steps)
-        return times, launches
+        return times
+
+    def as_graph(fn):
+        """The step captured once as a CUDA graph (the search is stream-ordered:
+        no host round trip inside), or None when capture is unavailable."""
+        if args.no_graph or world > 1:
+            return None
+        try:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                fn()
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            torch.cuda.synchronize()
+            return g
+        except Exception as exc:  # pragma: no cover - capture failure: eager timing
+            print(f"[bench] graph capture unavailable ({exc}); timing eager launches",
+                  file=sys.stderr)
+            torch.cuda.synchronize()
+            return None
 
     # warm-up
     for _ in range(max(3, args.warmup)):
         device_step()
     torch.cuda.synchronize()
+    # one profiled eager step: the kernel-level event timings (filter / select
+    # launches on their stream), launch and round counts
+    _lib.reset_scan_totals()
+    _lib.set_profiling(True)
+    device_step()
+    torch.cuda.synchronize()
+    tot = _lib.scan_totals()
+    _lib.set_profiling(False)
+    # encode launches + the scan's own launches (+ merge per batch when sharded)
+    launches_per_step = len(spans) + tot["launches"] + (len(spans) if world > 1 else 0)
+    graph = as_graph(device_step)
 
     clocks = ClockSampler(local)
     clocks.start()
-    _lib.set_profiling(True)
-    step_ms, launches = timed(device_step, args.steps)
-    tot = _lib.scan_totals()  # last step's kernel-level event timings (all batches)
-    _lib.set_profiling(False)
+    step_ms = run_timed(graph.replay if graph is not None else device_step, args.steps)
+    launches = launches_per_step * args.steps
     clk = clocks.stop()
 
     e2e = e2e_api = None
@@ -350,22 +379,27 @@ def run_gpu(args):
         host_out = [(torch.empty((b - a, keff), dtype=torch.float64).pin_memory(),
                      torch.empty((b - a, keff), dtype=torch.int32).pin_memory()) for a, b in spans]
 
+        q_in = [torch.empty((b - a, d), dtype=torch.float32, device="cuda") for a, b in spans]
+
         def e2e_step():
             for i, (a, b) in enumerate(spans):
-                qd = q_host[a:b].to("cuda", non_blocking=True)
-                s, ids = search_batch(i, qd)
+                q_in[i].copy_(q_host[a:b], non_blocking=True)
+                s, ids = search_batch(i, q_in[i])
                 host_out[i][0].copy_(s, non_blocking=True)
                 host_out[i][1].copy_(ids, non_blocking=True)
 
         for _ in range(2):
             e2e_step()
-        e2e_ms, _ = timed(e2e_step, args.steps)
+        torch.cuda.synchronize()
+        e2e_graph = as_graph(e2e_step)
+        e2e_ms = run_timed(e2e_graph.replay if e2e_graph is not None else e2e_step, args.steps)
         e2e = {"value": nq / (float(np.mean(e2e_ms)) / 1e3), "unit": "queries/s",
                "h2d_bytes_per_step": int(nq * d * 4),
                "d2h_bytes_per_step": int(nq * keff * (8 + 4)),
                "ms_per_step": float(np.mean(e2e_ms)),
                "path": "Int8Index.encode_queries + search_codes per batch, pinned host fp32 "
-                       "queries in, pinned host scores + ids out"}
+                       "queries in, pinned host scores + ids out"
+                       + (" (the step replayed as one CUDA graph)" if e2e_graph is not None else "")}
         if world == 1:
             # the reference-facing API: host int8 DenseDatasets in, GroundTruth
             # out (exact.py:105-117); the corpus is the frozen host code array
@@ -453,7 +487,9 @@ def run_gpu(args):
         "e2e": e2e,
         "e2e_reference_api": e2e_api,
         "gpu_launches": launches,
-        "gpu_launches_per_step": launches_per_step[0],
+        "gpu_launches_per_step": launches_per_step,
+        "timing": ("CUDA graph of the whole step (stream-ordered searches, no host round trip), "
+                   "replayed per step" if graph is not None else "eager launches"),
         "clocks": clk,
         "parity_spot_check": parity,
         "impl": "b200",
