@@ -723,6 +723,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     int32_t gall = g8s[0];
 #pragma unroll
                     for (int g = 1; g < kCB / 8; ++g) gall &= g8s[g];
+#ifdef QA_DROP_SURVIVORS
+                    if (gall != 0x12345678) continue;  // diagnostics: no slow path at all
+#endif
+#ifdef QA_SKIP_SLOW_RT
+                    if (p.stage_cap != 12345) continue;  // diagnostics: slow path compiled, never run
+#endif
                     if ((gall < 0 && !excg) || row >= r_hi) continue;
                     uint32_t hit = excg;
 #pragma unroll
@@ -954,8 +960,12 @@ cudaError_t launch_t(const FilterArgs &a, cudaStream_t st) {
     // 32-tile norm-sorted block of an index laid out by qa_order_rows_by_norm;
     // at least ~8 units per CTA so the dynamic assignment can balance
     int64_t want = (p.n_tiles * p.n_qtiles) / ((int64_t)sms * 8);
+    static const int64_t tpu_max = [] {
+        const char *v = getenv("QA_B200_TPU");  // diagnostics: largest tiles per unit
+        return v ? (int64_t)atoi(v) : (int64_t)32;
+    }();
     int64_t tpu = 1;
-    while (tpu * 2 <= want && tpu < 32) tpu *= 2;
+    while (tpu * 2 <= want && tpu < tpu_max) tpu *= 2;
     p.tiles_per_unit = tpu;
     p.n_units = ((p.n_tiles + tpu - 1) / tpu) * p.n_qtiles;
     const Knobs &kn = knobs();
@@ -1009,7 +1019,13 @@ cudaError_t dispatch_n(const FilterArgs &a, cudaStream_t st) {
     }();
     if (force_n == 128 && nmax >= 128) return dispatch_metric<SW, 128>(a, st);
     if (force_n == 64 && nmax >= 64) return dispatch_metric<SW, 64>(a, st);
-    if (a.nq > 128 && nmax >= 256) return dispatch_metric<SW, 256>(a, st);
+    // 256-query tiles only when K is long enough for the MMA time per tile to
+    // cover the epilogue (cfg3, d = 256: 420 vs 542 us per final pass); with
+    // K <= 128 the 128-query tiles and their 4 TMEM accumulators absorb the
+    // epilogue's survivor work better (cfg2: 1.76M -> 1.90M q/s; cfg1 and
+    // the dense round 0 likewise)
+    if (a.nq > 128 && nmax >= 256 && a.kdim > 128 && a.mode == 0)
+        return dispatch_metric<SW, 256>(a, st);
     if (a.nq > 64 && nmax >= 128) return dispatch_metric<SW, 128>(a, st);
     if (nmax >= 64) return dispatch_metric<SW, 64>(a, st);
     return cudaErrorNotSupported;
