@@ -16,6 +16,7 @@
 // a binary-search count in the other list).
 #include <cfloat>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "qa_common.cuh"
@@ -524,6 +525,255 @@ __global__ void __launch_bounds__(256, QA_SEL_MINB) select_reg_kernel(SelectArgs
     }
 }
 
+
+// ------------------------------------------------- radix select (k<=128) --
+//
+// Large batches, integer scores (IP / L2): one warp per query.  The retained
+// list and the round's surviving candidates are gathered as 64-bit keys
+// (score key << 32 | id: the (score, id) order) into a shared-memory buffer
+// U; whenever U fills, and once at the end, the k smallest keys are found by
+// an MSB-first radix select (8-bit digits, a 256-bin warp histogram per pass,
+// early exit once the boundary digit holds exactly the remaining rank) and
+// compacted -- no sorting until the end, when the k winners are sorted once
+// with the 32*R-wide register network.  The merge-per-chunk select above
+// sorts every 128 candidates; with 1024 dense candidates per query (round
+// 0) that was ~13k instructions per warp, this is ~3k.
+constexpr int kRadixWarps = 4;
+constexpr int kRadixCap = 1280;  // keys per warp buffer (k + chunks of candidates)
+
+// the k smallest of U[0, nu) (unique keys) moved to U[0, k); returns the
+// largest kept key (the k-th smallest)
+__device__ unsigned long long radix_keep_k(unsigned long long *U, int nu, int k, int *hist) {
+    const int lane = threadIdx.x & 31;
+    // bits above the highest one where the keys differ are common to all:
+    // the radix starts at that byte (scores of one query share their top bits)
+    unsigned long long kmin = ~0ull, kmax0 = 0;
+    for (int i = lane; i < nu; i += 32) {
+        const unsigned long long key = U[i];
+        kmin = key < kmin ? key : kmin;
+        kmax0 = key > kmax0 ? key : kmax0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a0 = __shfl_xor_sync(0xffffffffu, kmin, o);
+        const unsigned long long b0 = __shfl_xor_sync(0xffffffffu, kmax0, o);
+        kmin = a0 < kmin ? a0 : kmin;
+        kmax0 = b0 > kmax0 ? b0 : kmax0;
+    }
+    const int hi = 63 - __clzll((long long)(kmin ^ kmax0) | 1ll);  // highest differing bit
+    int shift0 = (hi / 8) * 8;
+    unsigned long long mask = shift0 == 56 ? 0ull : ~0ull << (shift0 + 8);
+    unsigned long long prefix = kmin & mask;
+    int want = k;  // rank still to place among keys matching prefix
+    for (int shift = shift0; shift >= 0; shift -= 8) {
+#pragma unroll
+        for (int b = 0; b < 8; ++b) hist[lane * 8 + b] = 0;
+        __syncwarp();
+        for (int base = 0; base < nu; base += 32) {
+            const int i = base + lane;
+            const unsigned long long key = i < nu ? U[i] : 0ull;
+            const bool in = i < nu && (key & mask) == prefix;
+            const unsigned act = __ballot_sync(0xffffffffu, in);
+            if (in) {
+                const int dg = (int)((key >> shift) & 255);
+#if defined(QA_RADIX_MATCH) && QA_RADIX_MATCH
+                // one shared atomic per distinct digit of the warp
+                const unsigned peers = __match_any_sync(act, dg);
+                if (lane == __ffs(peers) - 1) atomicAdd(hist + dg, __popc(peers));
+#else
+                (void)act;
+                atomicAdd(hist + dg, 1);
+#endif
+            }
+        }
+        __syncwarp();
+        int h[8], sum = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            h[b] = hist[lane * 8 + b];
+            sum += h[b];
+        }
+        int incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int excl = incl - sum;
+        // the lane whose bins hold rank `want`
+        const unsigned own = __ballot_sync(0xffffffffu, excl < want && incl >= want);
+        const int src = __ffs(own) - 1;
+        int d = 0, below = 0, eq = 0;
+        if (lane == src) {
+            int c = excl;
+            bool found = false;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                if (!found && c + h[b] >= want) {
+                    found = true;
+                    d = lane * 8 + b;
+                    below = c;
+                    eq = h[b];
+                }
+                c += h[b];
+            }
+        }
+        d = __shfl_sync(0xffffffffu, d, src);
+        below = __shfl_sync(0xffffffffu, below, src);
+        eq = __shfl_sync(0xffffffffu, eq, src);
+        want -= below;
+        prefix |= (unsigned long long)d << shift;
+        mask |= 255ull << shift;
+        if (eq == want) break;  // every key with this prefix is kept
+    }
+    const unsigned long long T = prefix | ~mask;  // keep keys <= T: exactly k of them
+    // in-place ballot compaction (writes never pass reads); the largest kept
+    // key is the k-th smallest
+    int w = 0;
+    unsigned long long kmax = 0;
+    for (int base = 0; base < nu; base += 32) {
+        const int i = base + lane;
+        const unsigned long long key = i < nu ? U[i] : ~0ull;
+        const bool keep = i < nu && key <= T;
+        const unsigned bb = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();
+        if (keep) {
+            U[w + __popc(bb & ((1u << lane) - 1))] = key;
+            kmax = key > kmax ? key : kmax;
+        }
+        w += __popc(bb);
+        __syncwarp();
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long v = __shfl_xor_sync(0xffffffffu, kmax, o);
+        kmax = v > kmax ? v : kmax;
+    }
+    return kmax;
+}
+
+template <int M, int R>
+__global__ void __launch_bounds__(kRadixWarps * 32) select_radix_kernel(SelectArgs a) {
+    static_assert(M == kIP || M == kL2, "integer scores");
+    __shared__ unsigned long long U_all[kRadixWarps][kRadixCap];
+    __shared__ int hist_all[kRadixWarps][256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t q = (int64_t)blockIdx.x * kRadixWarps + warp;
+    if (q >= a.nq) return;  // warp-level work only: no block barriers below
+    unsigned long long *U = U_all[warp];
+    int *hist = hist_all[warp];
+    const int k = (int)a.k;
+    const int32_t total = a.ccount[q];
+    Entry *st = a.state + q * a.k;
+    const int scur = a.state_cnt[q];
+    const int32_t qq = (M == kL2) ? a.q_sqnorm[q] : 0;
+    int nu = 0, cur = scur;
+    if (total > 0) {
+        const int m = (int)min((int64_t)total, a.cap);
+        if (total > a.cap && lane == 0) {
+            a.overflow[q] = 1;
+            atomicExch(a.any_overflow, 1);
+        }
+        for (int i = lane; i < scur; i += 32) {
+            RKey64 r;
+            to_key<M>(st[i], r);
+            U[i] = r.k;
+        }
+        nu = scur;
+        unsigned long long kth = scur == k ? U[k - 1] : ~0ull;  // the state is sorted
+        __syncwarp();
+        const Cand *cd = a.cand + q * a.cap;
+        int nvalid = 0;
+        // kIlp candidates per lane per step: their dependent gathers (norm,
+        // id of the row) are all in flight before any is used -- the loop is
+        // bound by memory latency, not instructions
+#ifndef QA_RADIX_ILP
+#define QA_RADIX_ILP 4
+#endif
+        constexpr int kIlp = QA_RADIX_ILP;
+        for (int pos = 0; pos < m; pos += 32 * kIlp) {
+            Cand c[kIlp];
+#pragma unroll
+            for (int u = 0; u < kIlp; ++u) {
+                const int i = pos + u * 32 + lane;
+                c[u] = i < m ? cd[i] : Cand{-1, 0};
+            }
+            int32_t xx[kIlp], id[kIlp];
+#pragma unroll
+            for (int u = 0; u < kIlp; ++u) {
+                const int32_t row = c[u].row >= 0 ? c[u].row : 0;
+                xx[u] = (M == kL2) ? __ldg(a.db_sqnorm + row) : 0;
+                id[u] = a.row_ids ? __ldg(a.row_ids + row) : row;
+            }
+#pragma unroll
+            for (int u = 0; u < kIlp; ++u) {
+                const bool valid = c[u].row >= 0;
+                unsigned long long key = 0;
+                if (valid) {
+                    int32_t sc;
+                    if constexpr (M == kIP)
+                        sc = (int32_t)(0u - (uint32_t)c[u].dot);
+                    else
+                        sc = (int32_t)((uint32_t)qq + (uint32_t)xx[u] - 2u * (uint32_t)c[u].dot);
+                    key = (skey_from_int(sc) << 32) | (uint32_t)id[u];
+                }
+                const bool keep = valid && key < kth;
+                nvalid += __popc(__ballot_sync(0xffffffffu, valid));
+                const unsigned bb = __ballot_sync(0xffffffffu, keep);
+                if (keep) U[nu + __popc(bb & ((1u << lane) - 1))] = key;
+                nu += __popc(bb);
+            }
+            __syncwarp();
+            if (nu + 32 * kIlp > kRadixCap && nu > k) {
+                kth = radix_keep_k(U, nu, k, hist);
+                nu = k;
+            }
+        }
+        if (nu > k) {
+            radix_keep_k(U, nu, k, hist);
+            nu = k;
+        }
+        cur = nu;
+        if (lane == 0 && a.cand_count) atomicAdd(a.cand_count, (unsigned long long)nvalid);
+    }
+    if (a.next_fill >= 0 && lane == 0) a.ccount_reset[q] = a.next_fill;
+    RKey64 t[R];
+    if (total > 0) {
+        // the kept keys, sorted once
+#pragma unroll
+        for (int e = 0; e < R; ++e) {
+            const int i = e * 32 + lane;
+            t[e].k = i < cur ? U[i] : ~0ull;
+        }
+        rsort(t);
+#pragma unroll
+        for (int e = 0; e < R; ++e) {
+            const int i = e * 32 + lane;
+            if (i < cur) st[i] = from_key(t[e]);
+        }
+        if (cur == k) {
+            const RKey64 v = rget(t, k - 1);
+            if (lane == 0) a.thr[q] = threshold_of<M>(from_key(v), qq, 1.0f);
+        }
+        if (lane == 0) a.state_cnt[q] = cur;
+    }
+    if (a.est_j > 0) {
+        // fused threshold estimate (see select_reg_kernel)
+        const int j = (int)a.est_j;
+        const int cnt = total > 0 ? cur : scur;
+        if (cnt < j) {
+            if (lane == 0 && !a.est_combine) a.est[q] = ~0ull;
+            return;
+        }
+        const Entry e = total > 0 ? from_key(rget(t, j - 1)) : a.state[q * a.k + j - 1];
+        if (lane == 0) {
+            a.thr[q] = threshold_of<M>(e, qq, 1.0f);
+            const unsigned long long prev = a.est[q];
+            a.est[q] = (a.est_combine && prev != ~0ull && prev < e.skey) ? prev : e.skey;
+        }
+    }
+}
+
 __global__ void reset_kernel(int32_t *p, int64_t n, int32_t v) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -948,6 +1198,23 @@ int pow2_at_least(int64_t v, int64_t cap) {
 
 template <int M>
 cudaError_t launch_select_t(const SelectArgs &a, cudaStream_t st) {
+    static const bool radix_on = [] {
+        const char *v = getenv("QA_B200_SEL_RADIX");  // diagnostics: 0 = merge-per-chunk select
+        return !(v && strcmp(v, "0") == 0);
+    }();
+    if constexpr (M != kAngular) {
+        // large batches, integer scores: one warp per query, radix select
+        if (radix_on && a.k <= 128 && a.nq >= 256) {
+            const unsigned grid = (unsigned)((a.nq + kRadixWarps - 1) / kRadixWarps);
+            if (a.k <= 32)
+                select_radix_kernel<M, 1><<<grid, kRadixWarps * 32, 0, st>>>(a);
+            else if (a.k <= 64)
+                select_radix_kernel<M, 2><<<grid, kRadixWarps * 32, 0, st>>>(a);
+            else
+                select_radix_kernel<M, 4><<<grid, kRadixWarps * 32, 0, st>>>(a);
+            return cudaGetLastError();
+        }
+    }
     if (a.k <= 128) {
         // warps per query: enough warps in flight to cover ~5 blocks of 8
         // per SM (the candidate stream is latency-bound per warp)
