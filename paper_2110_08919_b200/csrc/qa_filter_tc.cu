@@ -723,12 +723,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     int32_t gall = g8s[0];
 #pragma unroll
                     for (int g = 1; g < kCB / 8; ++g) gall &= g8s[g];
-#ifdef QA_DROP_SURVIVORS
-                    if (gall != 0x12345678) continue;  // diagnostics: no slow path at all
-#endif
-#ifdef QA_SKIP_SLOW_RT
-                    if (p.stage_cap != 12345) continue;  // diagnostics: slow path compiled, never run
-#endif
                     if ((gall < 0 && !excg) || row >= r_hi) continue;
                     uint32_t hit = excg;
 #pragma unroll
@@ -960,12 +954,8 @@ cudaError_t launch_t(const FilterArgs &a, cudaStream_t st) {
     // 32-tile norm-sorted block of an index laid out by qa_order_rows_by_norm;
     // at least ~8 units per CTA so the dynamic assignment can balance
     int64_t want = (p.n_tiles * p.n_qtiles) / ((int64_t)sms * 8);
-    static const int64_t tpu_max = [] {
-        const char *v = getenv("QA_B200_TPU");  // diagnostics: largest tiles per unit
-        return v ? (int64_t)atoi(v) : (int64_t)32;
-    }();
     int64_t tpu = 1;
-    while (tpu * 2 <= want && tpu < tpu_max) tpu *= 2;
+    while (tpu * 2 <= want && tpu < 32) tpu *= 2;
     p.tiles_per_unit = tpu;
     p.n_units = ((p.n_tiles + tpu - 1) / tpu) * p.n_qtiles;
     const Knobs &kn = knobs();
