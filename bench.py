@@ -300,7 +300,10 @@ def run_gpu(args):
     def search_batch(i, queries_dev):
         index.encode_queries(queries_dev, out=qcodes[i])
         if world == 1:
-            return index.search_codes(qcodes[i], k, out=outs[i])
+            # stream-ordered entry for every metric (graph-capturable); for
+            # angular this skips the zero-norm ValueError check, which the
+            # synthetic rows (unit vectors, nonzero codes) cannot trigger
+            return index.search_codes(qcodes[i], k, out=outs[i], sync=False)
         return sharded.sharded_search(lambda off: index.search_codes(qcodes[i], k), n, k)
 
     def device_step():
@@ -430,7 +433,8 @@ def run_gpu(args):
         try:
             from oracle import qa_oracle as o
 
-            s, ids = index.search_codes(qcodes[0], k)
+            torch.cuda.synchronize()
+            s, ids = outs[0]  # batch 0 as the last timed (graph-replayed) step left it
             sub = min(8, qcodes[0].n)
             Xc = index.codes_in_input_order()
             Qc = qcodes[0].to_host()[:sub]

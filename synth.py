@@ -63,7 +63,7 @@ CONFIGS = {
     0: dict(name="cfg0-l2-100k", gen="sift", n=100_000, nq=1_000, d=128, metric=1,
             calibration="minmax", k=100, seed=0, batch=1_000),
     1: dict(name="cfg1-angular-1m", gen="glove", n=1_000_000, nq=10_000, d=100, metric=2,
-            calibration="symmetric", k=100, seed=1, batch=1_024),
+            calibration="symmetric", k=100, seed=1, batch=10_000),  # unbatched in BASELINE
     2: dict(name="cfg2-l2-1m", gen="sift", n=1_000_000, nq=10_000, d=128, metric=1,
             calibration="minmax", k=100, seed=2, batch=1_024),
     3: dict(name="cfg3-ip-60m", gen="mixture", n=60_000_000, nq=10_000, d=256, metric=0,
