@@ -56,15 +56,14 @@ def _check_pair(data, queries):
 # content fingerprint; writable arrays are never cached.  Forms:
 #
 #   "rows"  caller order (query batches; norms)
-#   "l2"    index layout: stratified sample region, norm blocks
-#   "ip"    index layout: a fixed pseudo-random row order
-#   "ang"   index layout with plain norm bands
+#   "bands" index layout of L2 / angular: interleaved norm blocks
+#   "ip"    index layout of inner product: a fixed pseudo-random row order
 #
 # The index layouts (qa_layout.cu) are what the scan's threshold estimate and
 # per-unit bounds assume; ids still report caller rows (DeviceCodes.ids).
 
 _RESIDENT: dict = {}
-_FORM_OF_METRIC = {0: "ip", 1: "l2", 2: "ang"}
+_FORM_OF_METRIC = {0: "ip", 1: "bands", 2: "bands"}
 
 
 def _fingerprint(arr: np.ndarray) -> int:
@@ -78,7 +77,7 @@ def _make_form(base: _dev.DeviceCodes, form: str) -> _dev.DeviceCodes:
         return base
     if form == "ip":
         return base.shuffled()
-    return base.sorted_by_norm(stratify=form == "l2")
+    return base.sorted_by_norm(stratify=False)
 
 
 def _resident(arr: np.ndarray, dev, form: str = "rows") -> _dev.DeviceCodes:
@@ -201,7 +200,7 @@ def resident_norms(mat, corpus: bool = False):
     n, d = mat.shape
     if n == 0 or d == 0 or mat.dtype != np.int8:
         return norms(mat)
-    dc = _resident(mat, _dev.default_device(), "ang" if corpus else "rows")
+    dc = _resident(mat, _dev.default_device(), "bands" if corpus else "rows")
     out = getattr(dc, "_host_norm", None)
     if out is None:
         stored = dc.norm.cpu().numpy()

@@ -67,9 +67,11 @@ struct EventTimer {
     // sums the recorded spans into s (waits for the last event) and resets
     void accumulate(qa_scan_stats &s) {
         if (used > 0) cudaEventSynchronize(pool[used - 1]);
+        static const bool print = getenv("QA_B200_TIMES") != nullptr;  // diagnostics
         for (auto &sp : spans) {
             float ms = 0.f;
             cudaEventElapsedTime(&ms, pool[sp.second], pool[sp.second + 1]);
+            if (print) std::fprintf(stderr, "qa_time %s %.1f us\n", sp.first == 0 ? "filter" : "select", ms * 1e3f);
             if (sp.first == 0)
                 s.filter_ms += ms;
             else
@@ -131,6 +133,8 @@ struct Buf {
 struct Workspace {
     std::mutex mu;
     Buf state, state_cnt, thr, cand, ccount, ovf, flags, scratch, grp, est;
+    Buf ekeys;                       // bucket keys of the sampled estimate pass
+    Buf units;                       // work-unit table of the final pass (+ count)
     Buf sched;                       // [kSchedSlots] work-unit counters of the filter passes
     Buf f32_scores, f32_ss, f32_si, f32_sn;  // float32 exact search (qa_exact_f32.cu)
     Buf f32_full;                            // any-k full sort scratch
@@ -172,13 +176,10 @@ int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
 struct ScanPlan {
     int64_t r0, ratio, cap, qchunk;
-    // threshold estimate: once the prefix reaches est_rows, the rest of the
-    // rows are scanned in ONE pass with the est_j-th best prefix score as the
-    // bound (0 = off)
-    int64_t est_rows, est_j;
-    // two-level estimate: after round 0 the prefix [r0, est_rows) is also
-    // scanned in one pass, bounded by the est1_j-th best of round 0 (0 = off)
-    int64_t est1_j;
+    // Threshold estimate (0 = off): the sample is every est_stride-th 128-row
+    // tile of the index (est_tiles tiles, est_rows rows); the est_j-th best
+    // sample score bounds ONE pass over every row.
+    int64_t est_rows, est_j, est_stride, est_tiles;
 };
 
 // Smallest j with P(Poisson(lambda) >= j) <= tail.
@@ -210,50 +211,44 @@ ScanPlan plan_scan(int64_t n, int64_t nq, int64_t keff, int64_t cap_min, bool al
     p.ratio = nq >= 256 ? 2 : 32;
     if (const char *v = getenv("QA_B200_RATIO")) p.ratio = std::max(2, atoi(v));
     p.cap = std::max<int64_t>({2048, p.r0, 2 * keff * p.ratio, cap_min});
-    // Threshold estimate.  In a prefix of P rows (the index interleaves its
-    // norm blocks, so a prefix is a spread sample) about k*P/n rows beat the
-    // final k-th score; taking the j-th prefix score with j a high quantile
-    // of that count makes ">= k rows pass" near-certain, and the check after
-    // the pass proves it per query (the rare misses are recomputed without
-    // the estimate).  The final pass then admits ~j*n/P candidates per query
-    // instead of ~k per doubling round.
+    // Threshold estimate.  In a sample of P rows (every stride-th tile: the
+    // index interleaves narrow norm blocks, so the sample spans every band)
+    // about k*P/n rows beat the final k-th score; taking the j-th sample
+    // score with j a high quantile of that count makes ">= k rows pass"
+    // near-certain, and the check after the pass proves it per query (the
+    // rare misses are recomputed without the estimate).  The pass then admits
+    // ~j*n/P candidates per query instead of ~k per doubling round.
     p.est_rows = 0;
     p.est_j = 0;
-    p.est1_j = 0;
+    p.est_stride = 0;
+    p.est_tiles = 0;
     if (allow_estimate) {
         int64_t P = 32768;
-        if (const char *v = getenv("QA_B200_EST_ROWS")) P = atoll(v);
+        if (const char *v = getenv("QA_B200_EST_ROWS")) P = std::max<int64_t>(128, atoll(v));
         while (P < 64 * keff) P *= 2;
-        // small indexes (e.g. one GPU's row shard): a smaller prefix rather
+        // small indexes (e.g. one GPU's row shard): a smaller sample rather
         // than no estimate at all (which costs a doubling round per 2x rows)
         if (!getenv("QA_B200_EST_ROWS"))
-            while (P > 0 && 4 * P > n && P / 2 >= std::max<int64_t>(64 * keff, 4 * p.r0)) P /= 2;
-        if (P > 0 && 4 * P <= n) {
-            const double lambda = (double)keff * (double)P / (double)n;
+            while (4 * P > n && P / 2 >= std::max<int64_t>(64 * keff, 4096)) P /= 2;
+        if (4 * P <= n) {
+            const int64_t T = (n + 127) / 128;
+            const int64_t stride = std::max<int64_t>(1, T / (P / 128));
+            const int64_t S = (T + stride - 1) / stride;
+            // rows sampled (the last index tile may be partial and sampled)
+            int64_t rows = S * 128;
+            if ((S - 1) * stride == T - 1) rows -= T * 128 - n;
+            const double lambda = (double)keff * (double)rows / (double)n;
             double tail = 1e-4;
             if (const char *v = getenv("QA_B200_EST_TAIL")) tail = atof(v);
             int64_t j = std::max<int64_t>(8, poisson_quantile(lambda, tail));
             // diagnostics/tests: force j (small j makes the estimate fail often)
             if (const char *v = getenv("QA_B200_EST_J")) j = std::max<int64_t>(1, atoll(v));
             if (j < keff) {
-                p.est_rows = P;
+                p.est_rows = rows;
                 p.est_j = j;
-                p.cap = std::max<int64_t>(p.cap, 4 * j * (n / P));
-                // the same estimate one level down: round 0's j1-th best
-                // bounds the rest of the prefix (replaces the doubling rounds)
-                static const bool two_level = [] {
-                    const char *v = getenv("QA_B200_EST2");
-                    return !(v && strcmp(v, "0") == 0);
-                }();
-                if (two_level && p.r0 < P) {
-                    const double l1 = (double)keff * (double)p.r0 / (double)P;
-                    int64_t j1 = std::max<int64_t>(8, poisson_quantile(l1, tail));
-                    if (const char *v = getenv("QA_B200_EST1_J")) j1 = std::max<int64_t>(1, atoll(v));
-                    if (j1 < keff) {
-                        p.est1_j = j1;
-                        p.cap = std::max<int64_t>(p.cap, 4 * j1 * (P / p.r0));
-                    }
-                }
+                p.est_stride = stride;
+                p.est_tiles = S;
+                p.cap = std::max<int64_t>(p.cap, 4 * j * (n / rows));
             }
         }
     }
@@ -300,6 +295,122 @@ __global__ void zero_norm_kernel(const float *__restrict__ a, int64_t na,
     if (!(v > 0.0f)) *flag = 1;
 }
 
+// One query chunk with the sampled estimate: the bucket-best pass over the
+// sample tiles, the per-query est_j-th best bucket as the bound, then ONE
+// filter pass over every row and one select.  The check in finalize flags the
+// queries whose k-th score the bound did not cover.
+cudaError_t sampled_chunk(const ScanPlan &pl, int64_t n, int64_t d_alg, int64_t ld,
+                          const int8_t *db, const int32_t *db_sqnorm, const float *db_norm,
+                          const int32_t *row_ids, const int8_t *q, int64_t m,
+                          const int32_t *q_sqnorm, const float *q_norm, int64_t keff, int metric,
+                          const int32_t *grp_lo, const int32_t *grp_hi, int32_t *thr, Cand *cand,
+                          int32_t *ccount, Entry *state, int32_t *state_cnt,
+                          unsigned long long *est, int32_t *ekeys, int32_t *units,
+                          unsigned *sched, int32_t *ovf, int32_t *flags, cudaStream_t st) {
+    FilterArgs fa{};
+    fa.db = db;
+    fa.ldd = ld;
+    fa.q = q;
+    fa.ldq = ld;
+    fa.kdim = ld;
+    fa.nq = m;
+    fa.db_sqnorm = db_sqnorm;
+    fa.db_norm = db_norm;
+    fa.grp_lo = grp_lo;
+    fa.grp_hi = grp_hi;
+    fa.thr = thr;
+    fa.cand = cand;
+    fa.ccount = ccount;
+    fa.cap = pl.cap;
+    fa.metric = metric;
+    // the bucket-best pass over the sample tiles
+    int tpu = 0;
+    int64_t nb = 0;
+    filter_est_layout(pl.est_tiles, m, ld, 8 * pl.est_j, &tpu, &nb);
+    fa.mode = 4;
+    fa.r_lo = 0;
+    fa.r_hi = n;
+    fa.sample_stride = pl.est_stride;
+    fa.max_tpu = tpu;
+    fa.est_keys = ekeys;
+    fa.est_ld = nb;
+    fa.sched = sched + 0;
+    g_timer.begin(0, st);
+    cudaError_t e = launch_filter_tc(fa, st);
+    g_timer.end(st);
+    if (e != cudaSuccess) return e;
+    g_stats.filter_launches += 1;
+    g_stats.filter_ops += 2.0 * (double)m * (double)pl.est_rows * (double)d_alg;
+    e = launch_est_select(ekeys, nb, nb, m, pl.est_j, metric, q_sqnorm, q_norm, thr, est, st);
+    if (e != cudaSuccess) return e;
+    // the pass over every row, bounded by the estimate
+    fa.mode = 0;
+    fa.sample_stride = 0;
+    fa.max_tpu = 0;
+    if (const char *v = getenv("QA_B200_FINAL_TPU")) fa.max_tpu = atoi(v);  // diagnostics
+    // L2: the norm tails of the index are sparse, so their runs of tiles span
+    // wide norm ranges (cfg2: the lowest 4096-row block spans 180x the median
+    // block), their bound admits nearly every element to the exact test, and
+    // one such unit outlasted the rest of the pass (538 -> 291 us per cfg2
+    // batch as single-tile units).  Angular tests survivors in the select,
+    // not the epilogue: there the extra units cost more (cfg1 +16 %); so do
+    // they for a handful of queries, whose exact tests are few (cfg4 batch
+    // 1 / 8: +25 us, batch 64: -15 us).
+    static const bool tables = [] {
+        const char *v = getenv("QA_B200_UNIT_TABLE");  // diagnostics: 0 = off
+        return !(v && strcmp(v, "0") == 0);
+    }();
+    if (tables && metric == kL2 && m > 16 && fa.max_tpu == 0) {
+        const int tpu = filter_tiles_per_unit(n, m, ld);
+        if (tpu > 1) {
+            const int64_t nt = (n + 127) / 128;
+            e = launch_unit_table(metric, grp_lo, grp_hi, 0, nt, tpu, units, units + 2 * nt,
+                                  sched + kSchedSlots - 1, (double *)(units + 2 * nt + 2), st);
+            if (e != cudaSuccess) return e;
+            fa.unit_table = units;
+            fa.unit_count = units + 2 * nt;
+            g_stats.launches += 1;
+        }
+    }
+    fa.est_keys = nullptr;
+    fa.est_ld = 0;
+    fa.sched = sched + 1;
+    fa.exp_cands = (double)pl.est_j * (double)n / (double)pl.est_rows;
+    g_timer.begin(0, st);
+    e = launch_filter_tc(fa, st);
+    g_timer.end(st);
+    if (e != cudaSuccess) return e;
+    g_stats.filter_launches += 1;
+    g_stats.filter_ops += 2.0 * (double)m * (double)n * (double)d_alg;
+    SelectArgs sa;
+    sa.state = state;
+    sa.state_cnt = state_cnt;
+    sa.cand = cand;
+    sa.ccount = ccount;
+    sa.cap = pl.cap;
+    sa.nq = m;
+    sa.k = keff;
+    sa.metric = metric;
+    sa.db_sqnorm = db_sqnorm;
+    sa.db_norm = db_norm;
+    sa.q_sqnorm = q_sqnorm;
+    sa.q_norm = q_norm;
+    sa.row_ids = row_ids;
+    sa.thr = thr;
+    sa.overflow = ovf;
+    sa.any_overflow = flags;
+    sa.cand_count = reinterpret_cast<unsigned long long *>(flags + 4);
+    sa.next_fill = -1;
+    sa.ccount_reset = ccount;
+    g_timer.begin(1, st);
+    e = launch_select(sa, st);
+    g_timer.end(st);
+    if (e != cudaSuccess) return e;
+    g_stats.launches += 5;  // estimate pass, est_select, filter, select
+    g_stats.rounds += 2;
+    return cudaSuccess;
+}
+
 // One complete search with a given minimum candidate capacity.  Returns
 // QA_OK; *overflowed receives the list of queries whose lists overflowed
 // (their output rows are invalid and must be recomputed).
@@ -312,6 +423,23 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
               cudaStream_t st, std::vector<int32_t> *overflowed, bool async_ = false) {
     ScanPlan pl = plan_scan(n, nq, keff, cap_min, allow_estimate);
     const int64_t qc = pl.qchunk;
+    const bool simt = use_simt_filter(ld);
+    // the estimate needs the tensor-core pass (filter mode 4); the CUDA-core
+    // bring-up path scans in doubling rounds
+    if (simt) pl.est_rows = 0;
+    if (pl.est_rows > 0) {
+        int64_t nb_max = 0;
+        for (int64_t mm : {std::min(qc, nq), nq - (nq - 1) / qc * qc}) {
+            int tpu = 0;
+            int64_t nb = 0;
+            filter_est_layout(pl.est_tiles, mm, ld, 8 * pl.est_j, &tpu, &nb);
+            nb_max = std::max(nb_max, nb);
+        }
+        QA_TRY(ws.ekeys.reserve((size_t)qc * nb_max * 4), "workspace");
+        // table [2 * tiles] + count + pad, then the per-run ranges (2 doubles per run)
+        QA_TRY(ws.units.reserve(((size_t)(n + 127) / 128 * 2 + 2) * 4 + (size_t)(n + 127) / 128 * 16),
+               "workspace");
+    }
     QA_TRY(ws.state.reserve((size_t)qc * keff * sizeof(Entry)), "workspace");
     QA_TRY(ws.state_cnt.reserve((size_t)qc * 4), "workspace");
     QA_TRY(ws.thr.reserve((size_t)qc * 4), "workspace");
@@ -330,7 +458,6 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
     int32_t *ccount = (int32_t *)ws.ccount.ptr;
     int32_t *ovf = (int32_t *)ws.ovf.ptr;
     int32_t *flags = (int32_t *)ws.flags.ptr;  // [0] any overflow, [4:6) candidate counter
-    const bool simt = use_simt_filter(ld);
     // norm range of every 128-row tile (per-unit filter bounds)
     const int64_t groups = (n + 127) / 128;
     QA_TRY(ws.grp.reserve((size_t)groups * 8), "workspace");
@@ -345,8 +472,8 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
         // state, thresholds, this chunk's overflow flags and (chunk 0) the
         // search flags in one launch
         QA_TRY(launch_init_state_full(state_cnt, thr, m, metric, ovf + c0, c0 == 0 ? flags : nullptr,
-                                      ccount, (int32_t)std::min(n, pl.r0), st, sched,
-                                      kSchedSlots),
+                                      ccount, pl.est_rows > 0 ? 0 : (int32_t)std::min(n, pl.r0), st,
+                                      sched, kSchedSlots),
                "init");
         int pass = 0;  // filter passes of this chunk (work-unit counter slot)
         g_stats.launches += 1;
@@ -356,10 +483,22 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             QA_TRY(cudaGetLastError(), "norm check");
             g_stats.launches += 1;
         }
+        if (pl.est_rows > 0) {
+            QA_TRY(sampled_chunk(pl, n, d_alg, ld, db, db_sqnorm, db_norm, row_ids, q + c0 * ld, m,
+                                 q_sqnorm ? q_sqnorm + c0 : nullptr, q_norm ? q_norm + c0 : nullptr,
+                                 keff, metric, grp_lo, grp_hi, thr, cand, ccount, state, state_cnt,
+                                 est, (int32_t *)ws.ekeys.ptr, (int32_t *)ws.units.ptr, sched,
+                                 ovf + c0, flags, st),
+                   "sampled scan");
+            QA_TRY(launch_finalize(state, m, keff, keff, metric, id_offset, out_scores + c0 * keff,
+                                   out_ids + c0 * keff, st, state_cnt, est, ovf + c0, flags),
+                   "finalize");
+            g_stats.launches += 1;
+            continue;
+        }
         int64_t r_lo = 0, r_hi = pl.r0;
-        bool first = true, estimated = false;
+        bool first = true;
         bool counts_preset = true;  // init set round 0's (dense) counts
-        int64_t cur_j = 0;  // estimate rank of the pass in flight (0: k-th bound)
         for (;;) {
             FilterArgs fa{};
             fa.db = db;
@@ -394,10 +533,8 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             if (pass >= kSchedSlots) QA_TRY(cudaMemsetAsync(sched + pass % kSchedSlots, 0, 4, st), "sched");
             fa.sched = sched + pass % kSchedSlots;
             ++pass;
-            // ~k new candidates per doubling of the rows seen; the estimated
-            // final pass admits ~est_j per prefix-sized slice
-            fa.exp_cands = cur_j ? (double)cur_j * (double)(r_hi - r_lo) / (double)r_lo
-                                     : (double)keff * (double)(r_hi - r_lo) / (double)std::max<int64_t>(r_lo, 1);
+            // ~k new candidates per doubling of the rows seen
+            fa.exp_cands = (double)keff * (double)(r_hi - r_lo) / (double)std::max<int64_t>(r_lo, 1);
             // candidate counts of this round: preset by init (round 0) or by
             // the previous round's register select; otherwise here
             if (!counts_preset) {
@@ -430,36 +567,9 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             sa.overflow = ovf + c0;
             sa.any_overflow = flags;
             sa.cand_count = reinterpret_cast<unsigned long long *>(flags + 4);
-            // the estimate that follows this round (if any) runs inside the
-            // select when the register select serves k
-            int64_t est_now = 0;
-            int est_comb = 0;
-            if (r_hi < n) {
-                if (pl.est1_j > 0 && first && r_hi < pl.est_rows) {
-                    est_now = pl.est1_j;
-                } else if (pl.est_rows > 0 && r_hi >= pl.est_rows) {
-                    est_now = pl.est_j;
-                    est_comb = estimated ? 1 : 0;
-                }
-            }
-            const bool est_fused = est_now > 0 && keff <= 128;
-            sa.est_j = est_fused ? est_now : 0;
-            sa.est = est;
-            sa.est_combine = est_comb;
             // the next round's rows (and so its candidate-count preset, which
             // the register select writes when it is done with this round's)
-            int64_t next_hi = n;
-            if (r_hi < n) {
-                if (pl.est1_j > 0 && first && r_hi < pl.est_rows) {
-                    next_hi = pl.est_rows;
-                } else if (pl.est_rows > 0 && r_hi >= pl.est_rows) {
-                    next_hi = n;
-                } else {
-                    next_hi = std::min(n, round_up(r_hi * pl.ratio, 128));
-                    if (pl.est_rows > 0 && r_hi < pl.est_rows)
-                        next_hi = std::min(next_hi, pl.est_rows);
-                }
-            }
+            const int64_t next_hi = std::min(n, round_up(r_hi * pl.ratio, 128));
             const bool next_masked = (next_hi - r_hi) <= std::min<int64_t>(pl.cap, masked_max);
             const int32_t next_fill = next_masked ? (int32_t)(next_hi - r_hi) : 0;
             const bool fill_fused = keff <= 128 && r_hi < n;
@@ -482,47 +592,11 @@ int scan_impl(Workspace &ws, const int8_t *db, int64_t n, int64_t d_alg, int64_t
             }
             if (r_hi >= n) break;
             r_lo = r_hi;
-            if (pl.est1_j > 0 && first && r_hi < pl.est_rows) {
-                // one pass over the rest of the prefix with round 0's
-                // est1_j-th best as the bound
-                if (!est_fused) {
-                    QA_TRY(launch_estimate(state, state_cnt, thr, est, m, keff, pl.est1_j, metric,
-                                           q_sqnorm ? q_sqnorm + c0 : nullptr,
-                                           q_norm ? q_norm + c0 : nullptr, false, st),
-                           "estimate");
-                    g_stats.launches += 1;
-                }
-                estimated = true;
-                cur_j = pl.est1_j;
-                first = false;
-                r_hi = pl.est_rows;
-                continue;
-            }
             first = false;
-            if (pl.est_rows > 0 && r_hi >= pl.est_rows) {
-                // one pass over the rest with the estimated bound
-                cur_j = pl.est_j;
-                if (!est_fused) {
-                    QA_TRY(launch_estimate(state, state_cnt, thr, est, m, keff, pl.est_j, metric,
-                                           q_sqnorm ? q_sqnorm + c0 : nullptr,
-                                           q_norm ? q_norm + c0 : nullptr, estimated, st),
-                           "estimate");
-                    g_stats.launches += 1;
-                }
-                estimated = true;
-                r_hi = n;
-            } else {
-                r_hi = std::min(n, round_up(r_hi * pl.ratio, 128));
-                // rounds stop at the estimate prefix (the index's stratified
-                // sample region, qa_layout.cu)
-                if (pl.est_rows > 0 && r_lo < pl.est_rows) r_hi = std::min(r_hi, pl.est_rows);
-            }
+            r_hi = next_hi;
         }
-        // results, and (estimated plans) the check that queries whose k-th
-        // score fell short of an estimate are redone
         QA_TRY(launch_finalize(state, m, keff, keff, metric, id_offset, out_scores + c0 * keff,
-                               out_ids + c0 * keff, st, state_cnt, estimated ? est : nullptr,
-                               ovf + c0, flags),
+                               out_ids + c0 * keff, st, state_cnt, nullptr, ovf + c0, flags),
                "finalize");
         g_stats.launches += 1;
     }

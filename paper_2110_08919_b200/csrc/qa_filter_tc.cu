@@ -44,6 +44,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "qa_common.cuh"
 #include "qa_internal.h"
@@ -148,10 +149,25 @@ __device__ __forceinline__ void unit_tb(const Params &p, int64_t u, int64_t &t, 
     b = u / p.n_qtiles;
 }
 
-// kFilter: the filter pass proper (mode 0); otherwise the dense, masked-dense
-// and diagnostic passes.  Separate instances keep the hot loop's register
-// allocation free of the other paths.
-template <int SW, int N, int M, bool kFilter>
+// Tiles [tile0, tile1) of row unit b (relative to r_lo): fixed-size units, or
+// the pass's unit table (launch_unit_table: wide-norm blocks split into
+// single tiles, listed first).
+__device__ __forceinline__ void unit_tiles(const Params &p, int64_t b, int64_t &tile0,
+                                           int64_t &tile1) {
+    if (p.a.unit_table) {
+        const int2 e = __ldg(reinterpret_cast<const int2 *>(p.a.unit_table) + b);
+        tile0 = e.x;
+        tile1 = (int64_t)e.x + e.y;
+    } else {
+        tile0 = b * p.tiles_per_unit;
+        tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
+    }
+}
+
+// kKind 0: the filter pass proper (mode 0); 1: the dense, masked-dense and
+// diagnostic passes (modes 1-3); 2: the sampled estimate (mode 4).  Separate
+// instances keep each hot loop's register allocation free of the other paths.
+template <int SW, int N, int M, int kKind>
 __global__ void __launch_bounds__(kThreads, 1)
     filter_tc_kernel(const __grid_constant__ CUtensorMap tm_db,
                      const __grid_constant__ CUtensorMap tm_q, const Params p) {
@@ -280,12 +296,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             // roles through a 4-slot ring, two units ahead
             int fetched = 0;
             bool done = false;
+            const int64_t n_units =
+                a.unit_table ? (int64_t)__ldg(a.unit_count) * p.n_qtiles : p.n_units;
             auto fetch = [&]() {
                 if (done) return;
                 const int s = fetched & (kURing - 1);
                 WSTAT(14, mbar_wait_sleep(unit_empty + s, ((uint32_t)(fetched / kURing) & 1) ^ 1));
                 const unsigned v = atomicAdd(a.sched, 1u);
-                const int u = v < (unsigned)p.n_units ? (int)v : -1;
+                const int u = v < (unsigned)n_units ? (int)v : -1;
                 *(volatile int *)(uring + s) = u;
                 mbar_arrive(unit_full + s);
                 done = u < 0;
@@ -309,10 +327,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tma_load_2d(dstB + (size_t)c * N * SW, &tm_q, b_full + bslot, c * SW,
                                 (int32_t)(t * N));
                 // streamed database tiles
-                const int64_t tile0 = b * p.tiles_per_unit;
-                const int64_t tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
+                int64_t tile0, tile1;
+                unit_tiles(p, b, tile0, tile1);
+                const int64_t tstep = a.mode == 4 ? a.sample_stride : 1;  // sampled tiles
                 for (int64_t tile = tile0; tile < tile1; ++tile) {
-                    const int32_t row0 = (int32_t)(a.r_lo + tile * kBlockM);
+                    const int32_t row0 = (int32_t)(a.r_lo + tile * tstep * kBlockM);
                     for (int c = 0; c < p.kchunks; ++c) {
                         WSTAT(1, mbar_wait_sleep(a_empty + stage, aph ^ 1));
                         mbar_arrive_expect_tx(a_full + stage, a_stage_bytes);
@@ -349,8 +368,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t ph = (it >> 1) & 1;
             int64_t t, b;
             unit_tb(p, u, t, b);
-            const int64_t tile0 = b * p.tiles_per_unit;
-            const int ntl = (int)(min(p.n_tiles, tile0 + p.tiles_per_unit) - tile0);
+            int64_t tile0, tile1;
+            unit_tiles(p, b, tile0, tile1);
+            const int ntl = (int)(tile1 - tile0);
             const int bslot = it % bslots;
             WSTAT(2, mbar_wait_spin(b_full + bslot, (uint32_t)(it / bslots) & 1));
             WSTAT(3, mbar_wait_spin(bias_full + slot, ph));
@@ -407,8 +427,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (u < 0) break;
             const int slot = it & 1;
             const uint32_t ph = (it >> 1) & 1;
-            int64_t t, b;
+            int64_t t, b, tile0, tile1;
             unit_tb(p, u, t, b);
+            unit_tiles(p, b, tile0, tile1);
             const int64_t q0 = t * N;
             const int nqt = (int)min((int64_t)N, a.nq - q0);
             // all global reads of the unit issued together: thresholds of
@@ -422,8 +443,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             float nlo = INFINITY, nhi = -INFINITY;
             int32_t xlo = INT32_MAX;
             if (filtered && M != kIP) {
-                const int64_t gt0 = (a.r_lo >> 7) + b * p.tiles_per_unit;
-                const int64_t gt1 = (a.r_lo >> 7) + min(p.n_tiles, (b + 1) * p.tiles_per_unit);
+                const int64_t gt0 = (a.r_lo >> 7) + tile0;
+                const int64_t gt1 = (a.r_lo >> 7) + tile1;
                 for (int64_t g = gt0 + lane; g < gt1; g += 32) {
                     if constexpr (M == kL2) {
                         xlo = min(xlo, __ldg(a.grp_lo + g));
@@ -444,9 +465,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             // unaligned arrays by plain loads)
             const bool stage_norms = kExactInEpilogue && (M != kIP) && a.mode == 0;
             if (stage_norms) {
-                const int32_t row0 = (int32_t)(a.r_lo + b * p.tiles_per_unit * kBlockM);
-                const int32_t nrows = (int32_t)min((int64_t)p.tiles_per_unit * kBlockM,
-                                                   a.r_hi - (int64_t)row0);
+                const int32_t row0 = (int32_t)(a.r_lo + tile0 * kBlockM);
+                const int32_t nrows = (int32_t)min((tile1 - tile0) * kBlockM, a.r_hi - (int64_t)row0);
                 const int32_t *src = (M == kL2) ? a.db_sqnorm + row0
                                                 : reinterpret_cast<const int32_t *>(a.db_norm) + row0;
                 int32_t *dst = norm_all + slot * kUnitRowsMax;
@@ -554,9 +574,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 WSTAT(7, mbar_wait_sleep(norm_full + slot, ph));
                 if constexpr (M == kAngular) {
                     // the exact test multiplies by 1/xn: stage the reciprocal
-                    const int32_t row0 = (int32_t)(a.r_lo + b * p.tiles_per_unit * kBlockM);
-                    const int32_t nrows = (int32_t)min((int64_t)p.tiles_per_unit * kBlockM,
-                                                       a.r_hi - (int64_t)row0);
+                    const int32_t row0 = (int32_t)(a.r_lo + tile0 * kBlockM);
+                    const int32_t nrows =
+                        (int32_t)min((tile1 - tile0) * kBlockM, a.r_hi - (int64_t)row0);
                     int32_t *dst = norm_all + slot * kUnitRowsMax;
                     for (int32_t i = lane; i < nrows; i += 32)
                         dst[i] = __float_as_int(__frcp_rn(__int_as_float(dst[i])));
@@ -579,10 +599,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (u < 0) break;
             const int slot = it & 1;
             const uint32_t ph = (it >> 1) & 1;
-            int64_t t, b;
+            int64_t t, b, tile0, tile1;
             unit_tb(p, u, t, b);
+            unit_tiles(p, b, tile0, tile1);
             const int64_t q0 = t * N;
-            const int32_t unit_row0 = (int32_t)(a.r_lo + b * p.tiles_per_unit * kBlockM);
+            const int32_t unit_row0 = (int32_t)(a.r_lo + tile0 * kBlockM);
             WSTAT(8, mbar_wait_sleep(stage_full + slot, ph));
             if (a.mode == 0 && stage_n_all[slot] > 0) {
                 int32_t *qc = qcnt_all + slot * N;
@@ -632,7 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ew = warp - kEpiWarp0;           // 0..15
         const int quarter = warp & 3;
         const int col0 = (ew >> 2) * kCB;          // first column of this warp
-        constexpr bool lean = kFilter;
+        constexpr bool lean = kKind == 0;
         const uint32_t tm_warp = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)col0;
         int acc = 0;
         uint32_t accph = 0;
@@ -652,8 +673,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             int32_t *stage_n = stage_n_all + slot;
             const uint32_t stage_n_addr = smem_u32(stage_n);
             const uint32_t stage_addr = smem_u32(stage_all + slot * stage_cap);
-            const int64_t tile0 = b * p.tiles_per_unit;
-            const int64_t tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
+            int64_t tile0, tile1;
+            unit_tiles(p, b, tile0, tile1);
             const uint32_t thr_addr = smem_u32(thr_all + slot * N);
             const uint32_t bias_addr = smem_u32(bias_s + slot * N);
             const int nch = max(0, min(kCB / kC, (nqt - col0 + kC - 1) / kC));
@@ -777,6 +798,99 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                 }
+            } else if constexpr (kKind == 2) {
+            if constexpr (N <= 128) {
+                // ---- sampled estimate: best goodness per (query, bucket) ----
+                // A bucket is 8 lanes of one warp (lane & 3 fixed) over the
+                // unit's tiles.  The j-th best bucket bounds the j-th best row
+                // from below (every bucket best is a distinct row), and with
+                // hundreds of buckets per query the two rarely differ.
+                // goodness: IP dot, L2 2*dot - xx (int32), angular float(dot)/xn
+                // (tracked as float, mapped to an ordered int32 at the end)
+                using G = typename std::conditional<M == kAngular, float, int32_t>::type;
+                G gbest[kCB];
+#pragma unroll
+                for (int c = 0; c < kCB; ++c) gbest[c] = M == kAngular ? (G)(-INFINITY) : (G)INT32_MIN;
+                const int32_t rstep = (int32_t)(a.sample_stride * kBlockM);
+                wrow0 = (int32_t)(a.r_lo + tile0 * a.sample_stride * kBlockM) + quarter * 32;
+                // the row norm two tiles ahead (its global load would stall
+                // the tile: the accumulator is usually ready)
+                auto norm_of = [&](int32_t row) -> int32_t {
+                    if constexpr (M == kIP) return 0;
+                    if (row >= r_hi) return 0;
+                    return M == kL2 ? __ldg(a.db_sqnorm + row)
+                                    : __ldg(reinterpret_cast<const int32_t *>(a.db_norm) + row);
+                };
+                int32_t nrm0 = ntl > 0 ? norm_of(wrow0 + lane) : 0;
+                int32_t nrm1 = ntl > 1 ? norm_of(wrow0 + rstep + lane) : 0;
+                for (int ti = 0; ti < ntl; ++ti, wrow0 += rstep) {
+                    const int32_t row = wrow0 + lane;
+                    const bool valid = row < r_hi;
+                    const int32_t nrm = nrm0;
+                    nrm0 = nrm1;
+                    nrm1 = ti + 2 < ntl ? norm_of(row + 2 * rstep) : 0;
+                    mbar_wait(acc_full + acc, accph);
+                    tc_fence_after();
+                    const uint32_t ta = tm_warp + (uint32_t)(acc * N);
+                    int32_t v[kCB / kC][kC];
+#pragma unroll
+                    for (int ci = 0; ci < kCB / kC; ++ci)
+                        tmem_ld_cols<kC>(ta + (uint32_t)(ci * kC), v[ci]);
+                    tmem_wait();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(acc_empty + acc);
+                    if (++acc == kNacc) {
+                        acc = 0;
+                        accph ^= 1;
+                    }
+                    if (!valid) continue;
+                    const float inv_xn = M == kAngular ? __frcp_rn(__int_as_float(nrm)) : 0.f;
+#pragma unroll
+                    for (int ci = 0; ci < kCB / kC; ++ci)
+#pragma unroll
+                        for (int j = 0; j < kC; ++j) {
+                            if constexpr (M == kIP) {
+                                gbest[ci * kC + j] = max(gbest[ci * kC + j], v[ci][j]);
+                            } else if constexpr (M == kL2) {  // |.| < 2^26 for kdim <= 1024
+                                gbest[ci * kC + j] = max(gbest[ci * kC + j], 2 * v[ci][j] - nrm);
+                            } else {
+                                gbest[ci * kC + j] =
+                                    fmaxf(gbest[ci * kC + j], __int2float_rn(v[ci][j]) * inv_xn);
+                            }
+                        }
+                }
+                int32_t best[kCB];
+#pragma unroll
+                for (int c = 0; c < kCB; ++c) {
+                    if constexpr (M == kAngular) {
+                        const int32_t g = __float_as_int(gbest[c]);
+                        best[c] = g < 0 ? (g ^ 0x7fffffff) : g;  // float order as int
+                    } else {
+                        best[c] = (int32_t)gbest[c];
+                    }
+                }
+                // fold lanes differing in bits 4, 3, 2: each lane ends with
+                // kCB / 8 columns of its bucket (lane & 3)
+                int colb = 0;
+#pragma unroll
+                for (int o = 16, C = kCB; o >= 4; o >>= 1, C >>= 1) {
+                    const bool up = (lane & o) != 0;
+#pragma unroll
+                    for (int h = 0; h < C / 2; ++h) {
+                        const int32_t keep = up ? best[h + C / 2] : best[h];
+                        const int32_t send = up ? best[h] : best[h + C / 2];
+                        best[h] = max(keep, __shfl_xor_sync(0xffffffffu, send, o));
+                    }
+                    if (up) colb += C / 2;
+                }
+                const int64_t bucket = b * 16 + quarter * 4 + (lane & 3);
+#pragma unroll
+                for (int h = 0; h < kCB / 8; ++h) {
+                    const int c = col0 + colb + h;
+                    if (c < nqt) a.est_keys[(q0 + c) * a.est_ld + bucket] = best[h];
+                }
+            }
             } else {
             if (a.mode == 1 || a.mode == 3) {
                 // ---- dense (round 0) and masked-dense (early rounds) ----
@@ -939,25 +1053,72 @@ const Knobs &knobs() {
     return k;
 }
 
+// Tiles per work unit: a power of two <= 32, so units stay inside one
+// 32-tile norm-sorted block of an index laid out by qa_order_rows_by_norm;
+// at least ~8 units per CTA so the dynamic assignment can balance.  The
+// sampled-estimate pass (mode 4) takes ~2 units per CTA instead: its units
+// are uniform in cost, and fewer units mean fewer buckets for the select.
+int64_t tiles_per_unit(int64_t n_tiles, int64_t n_qtiles, int mode, int sms) {
+    int64_t tpu = 1;
+    if (mode == 4) {
+        const int64_t want = (n_tiles * n_qtiles + 2 * sms - 1) / (2 * (int64_t)sms);
+        while (tpu < want && tpu < 32) tpu *= 2;
+        return tpu;
+    }
+    const int64_t want = (n_tiles * n_qtiles) / ((int64_t)sms * 8);
+    while (tpu * 2 <= want && tpu < 32) tpu *= 2;
+    return tpu;
+}
+
+// Query-tile width N of a pass: the largest whose B buffer fits 64 KiB, no
+// larger than the query chunk needs (0: unsupported).
+int pick_tile_n(int64_t nq, int64_t kdim, int mode) {
+    const int nmax = (int)(65536 / kdim);
+    static const int force_n = [] {  // diagnostics: QA_B200_TILE_N=128 / 64
+        const char *v = getenv("QA_B200_TILE_N");
+        return v ? atoi(v) : 0;
+    }();
+    if (force_n == 128 && nmax >= 128) return 128;
+    if (force_n == 64 && nmax >= 64) return 64;
+    // 256-query tiles only when K is long enough for the MMA time per tile to
+    // cover the epilogue (cfg3, d = 256: 420 vs 542 us per final pass); with
+    // K <= 128 the 128-query tiles and their 4 TMEM accumulators absorb the
+    // epilogue's survivor work better (cfg2: 1.76M -> 1.90M q/s; cfg1 and
+    // the dense round 0 likewise)
+    if (nq > 128 && nmax >= 256 && kdim > 128 && mode == 0) return 256;
+    if (nq > 64 && nmax >= 128) return 128;
+    if (nmax >= 64) return 64;
+    return 0;
+}
+
 template <int SW, int N, int M>
 cudaError_t launch_t(const FilterArgs &a, cudaStream_t st) {
+    if (a.mode == 4 && (!a.est_keys || a.sample_stride < 1 || a.max_tpu < 1))
+        return cudaErrorInvalidValue;
     CUtensorMap tm_db, tm_q;
     if (!make_map(&tm_db, a.db, a.r_hi, a.kdim, a.ldd, kBlockM, SW)) return cudaErrorNotSupported;
     if (!make_map(&tm_q, a.q, a.nq, a.kdim, a.ldq, N, SW)) return cudaErrorNotSupported;
     Params p;
     p.a = a;
     p.n_tiles = (a.r_hi - a.r_lo + kBlockM - 1) / kBlockM;
+    if (a.mode == 4) p.n_tiles = (p.n_tiles + a.sample_stride - 1) / a.sample_stride;
     p.n_qtiles = (a.nq + N - 1) / N;
     p.kchunks = (int)(a.kdim / SW);
     const int sms = num_sms();
-    // tiles per unit: a power of two <= 32, so units stay inside one
-    // 32-tile norm-sorted block of an index laid out by qa_order_rows_by_norm;
-    // at least ~8 units per CTA so the dynamic assignment can balance
-    int64_t want = (p.n_tiles * p.n_qtiles) / ((int64_t)sms * 8);
-    int64_t tpu = 1;
-    while (tpu * 2 <= want && tpu < 32) tpu *= 2;
+    int64_t tpu = tiles_per_unit(p.n_tiles, p.n_qtiles, a.mode, sms);
+    if (a.mode == 4) {
+        tpu = a.max_tpu;  // the caller sized its bucket array with it
+        if ((p.n_tiles + tpu - 1) / tpu * 16 > a.est_ld) return cudaErrorInvalidValue;
+    } else if (a.max_tpu > 0) {
+        tpu = std::min<int64_t>(tpu, a.max_tpu);
+    }
     p.tiles_per_unit = tpu;
     p.n_units = ((p.n_tiles + tpu - 1) / tpu) * p.n_qtiles;
+    if (a.unit_table) {
+        // a unit table (mode 0 only) lists at most one unit per tile
+        if (a.mode != 0 || !a.unit_count) return cudaErrorInvalidValue;
+        p.n_units = p.n_tiles * p.n_qtiles;  // upper bound: the grid size
+    }
     const Knobs &kn = knobs();
     p.idesc = make_idesc(N);
     p.stage_cap = kn.stage_cap;
@@ -980,7 +1141,8 @@ cudaError_t launch_t(const FilterArgs &a, cudaStream_t st) {
     if (stages > kn.max_stages) stages = kn.max_stages;
     p.stages = stages;
     const size_t smem = fixed + (size_t)stages * (stage_bytes + 16);
-    auto kern = a.mode == 0 ? filter_tc_kernel<SW, N, M, true> : filter_tc_kernel<SW, N, M, false>;
+    auto kern = a.mode == 0 ? filter_tc_kernel<SW, N, M, 0>
+                            : (a.mode == 4 ? filter_tc_kernel<SW, N, M, 2> : filter_tc_kernel<SW, N, M, 1>);
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1000,28 +1162,34 @@ cudaError_t dispatch_metric(const FilterArgs &a, cudaStream_t st) {
 
 template <int SW>
 cudaError_t dispatch_n(const FilterArgs &a, cudaStream_t st) {
-    // Largest query tile whose B buffer fits 64 KiB, no larger than the query
-    // chunk needs.
-    int nmax = (int)(65536 / a.kdim);
-    static const int force_n = [] {  // diagnostics: QA_B200_TILE_N=128 / 64
-        const char *v = getenv("QA_B200_TILE_N");
-        return v ? atoi(v) : 0;
-    }();
-    if (force_n == 128 && nmax >= 128) return dispatch_metric<SW, 128>(a, st);
-    if (force_n == 64 && nmax >= 64) return dispatch_metric<SW, 64>(a, st);
-    // 256-query tiles only when K is long enough for the MMA time per tile to
-    // cover the epilogue (cfg3, d = 256: 420 vs 542 us per final pass); with
-    // K <= 128 the 128-query tiles and their 4 TMEM accumulators absorb the
-    // epilogue's survivor work better (cfg2: 1.76M -> 1.90M q/s; cfg1 and
-    // the dense round 0 likewise)
-    if (a.nq > 128 && nmax >= 256 && a.kdim > 128 && a.mode == 0)
-        return dispatch_metric<SW, 256>(a, st);
-    if (a.nq > 64 && nmax >= 128) return dispatch_metric<SW, 128>(a, st);
-    if (nmax >= 64) return dispatch_metric<SW, 64>(a, st);
-    return cudaErrorNotSupported;
+    switch (pick_tile_n(a.nq, a.kdim, a.mode)) {
+        case 256: return dispatch_metric<SW, 256>(a, st);
+        case 128: return dispatch_metric<SW, 128>(a, st);
+        case 64: return dispatch_metric<SW, 64>(a, st);
+        default: return cudaErrorNotSupported;
+    }
 }
 
 }  // namespace
+
+int filter_tiles_per_unit(int64_t rows, int64_t nq, int64_t kdim) {
+    const int n = pick_tile_n(nq, kdim, 0);
+    if (n == 0 || rows <= 0) return 0;
+    const int64_t n_tiles = (rows + kBlockM - 1) / kBlockM;
+    return (int)tiles_per_unit(n_tiles, (nq + n - 1) / n, 0, num_sms());
+}
+
+void filter_est_layout(int64_t tiles, int64_t nq, int64_t kdim, int64_t min_buckets, int *tpu,
+                       int64_t *buckets) {
+    *tpu = 0;
+    *buckets = 0;
+    const int n = pick_tile_n(nq, kdim, 4);
+    if (n == 0 || tiles <= 0) return;
+    int64_t t = tiles_per_unit(tiles, (nq + n - 1) / n, 4, num_sms());
+    while (t > 1 && (tiles + t - 1) / t * 16 < min_buckets) t /= 2;
+    *tpu = (int)t;
+    *buckets = (tiles + t - 1) / t * 16;  // 16 buckets per row unit (epilogue)
+}
 
 cudaError_t launch_filter_tc(const FilterArgs &a, cudaStream_t st) {
     if (a.r_hi <= a.r_lo || a.nq == 0) return cudaSuccess;

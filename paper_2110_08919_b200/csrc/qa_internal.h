@@ -45,7 +45,8 @@ struct FilterArgs {
     int metric;
     // 0 = filter (threshold test + append), 1 = dense (every row is a
     // candidate: cand[q, row - r_lo]; the round-0 pass), 2 = diagnostics
-    // (every dot to dots_out[q, row]).
+    // (every dot to dots_out[q, row]), 3 = masked dense, 4 = sampled
+    // estimate (per-bucket best goodness to est_keys; no candidates).
     int mode;
     int32_t *dots_out;
     int64_t ld_dots;
@@ -54,7 +55,46 @@ struct FilterArgs {
     double exp_cands;
     // zeroed work-unit counter of this launch (dynamic scheduling)
     unsigned *sched = nullptr;
+    // mode 4 (sampled threshold estimate): per query, the best "goodness" of
+    // every row bucket, est_keys[q * est_ld + bucket] (see
+    // filter_est_buckets); goodness is an order-preserving int32, larger is
+    // better: IP dot, L2 2*dot - xx, angular the float dot/xn mapped to int
+    int32_t *est_keys = nullptr;
+    int64_t est_ld = 0;
+    // mode 4: the pass reads every sample_stride-th 128-row tile of
+    // [r_lo, r_hi), max_tpu sample tiles per work unit (filter_est_layout)
+    int64_t sample_stride = 0;
+    // cap on the tiles per work unit (0 = the launcher's choice)
+    int max_tpu = 0;
+    // mode 0: work units from a table (launch_unit_table) instead of fixed
+    // runs of tiles: unit_table[2*i] = first tile (relative to r_lo),
+    // [2*i+1] = tile count (<= 32); *unit_count units
+    const int32_t *unit_table = nullptr;
+    const int32_t *unit_count = nullptr;
 };
+
+// The work-unit table of a mode-0 pass over tiles [tile_lo, tile_lo + n_tiles)
+// (global 128-row tile indices): aligned runs of `tpu` tiles, except runs
+// whose norm range is wide (the index's sparse norm tails), which are split
+// into single tiles so each gets its own bound; the split units come first so
+// their extra cost starts early.  table needs 2 * n_tiles ints, scratch
+// 2 * ceil(n_tiles / tpu) doubles; *ticket must be 0 (the kernel leaves it 0).
+cudaError_t launch_unit_table(int metric, const int32_t *grp_lo, const int32_t *grp_hi,
+                              int64_t tile_lo, int64_t n_tiles, int tpu, int32_t *table,
+                              int32_t *count, unsigned *ticket, double *scratch, cudaStream_t st);
+// tiles per unit the launcher picks for a mode-0 pass
+int filter_tiles_per_unit(int64_t rows, int64_t nq, int64_t kdim);
+
+// Work-unit size (sample tiles) and buckets per query of a mode-4 pass over
+// `tiles` sample tiles: ~2 units per CTA, halved until there are at least
+// `min_buckets` buckets per query (*tpu = 0: no tensor-core pass for the shape).
+void filter_est_layout(int64_t tiles, int64_t nq, int64_t kdim, int64_t min_buckets, int *tpu,
+                       int64_t *buckets);
+// thr[q] / est[q] from the est_j-th best bucket of a mode-4 pass (qa_select.cu);
+// est[q] = ~0 when fewer than j buckets hold a row
+cudaError_t launch_est_select(const int32_t *keys, int64_t ld, int64_t nb, int64_t nq, int64_t j,
+                              int metric, const int32_t *q_sqnorm, const float *q_norm,
+                              int32_t *thr, unsigned long long *est, cudaStream_t st);
 
 
 

@@ -7,6 +7,8 @@
 // test.  The order starts from a stable radix sort on the int32 squared norm
 // (CUB, part of the CUDA toolkit); reported ids stay the caller's row
 // positions through the row_ids map passed to the scan.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 
 #include "qa_internal.h"
@@ -120,13 +122,22 @@ __global__ void group_ranges_kernel(int metric, const int32_t *__restrict__ sqno
     const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (g >= groups) return;
     if (metric == 1) {
-        int32_t v = INT32_MAX;
+        int32_t v = INT32_MAX, w = INT32_MIN;
         for (int i = 0; i < 4; ++i) {
             const int64_t r = g * 128 + i * 32 + lane;
-            if (r < n) v = min(v, sqnorm[r]);
+            if (r < n) {
+                v = min(v, sqnorm[r]);
+                w = max(w, sqnorm[r]);
+            }
         }
-        for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
-        if (lane == 0) lo[g] = v;
+        for (int o = 16; o; o >>= 1) {
+            v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+            w = max(w, __shfl_xor_sync(0xffffffffu, w, o));
+        }
+        if (lane == 0) {
+            lo[g] = v;
+            hi[g] = w;
+        }
     } else {
         float vmin = INFINITY, vmax = -INFINITY;
         for (int i = 0; i < 4; ++i) {
@@ -147,7 +158,126 @@ __global__ void group_ranges_kernel(int metric, const int32_t *__restrict__ sqno
     }
 }
 
+// The work-unit table of a mode-0 filter pass (launch_unit_table): one warp
+// per run of tpu tiles writes the run's norm range; the last CTA to finish
+// (ticket counter) turns the ranges into the table.
+constexpr int kUnitThreads = 1024;
+
+__device__ __forceinline__ double tile_lo_of(int metric, const int32_t *lo, int64_t g) {
+    return metric == 1 ? (double)lo[g] : (double)__int_as_float(lo[g]);
+}
+__device__ __forceinline__ double tile_hi_of(int metric, const int32_t *hi, int64_t g) {
+    return metric == 1 ? (double)hi[g] : (double)__int_as_float(hi[g]);
+}
+
+__global__ void __launch_bounds__(kUnitThreads) unit_table_kernel(
+    int metric, const int32_t *__restrict__ lo, const int32_t *__restrict__ hi, int64_t tile_lo,
+    int64_t n_tiles, int tpu, int32_t *__restrict__ table, int32_t *__restrict__ count,
+    unsigned *__restrict__ ticket, double *__restrict__ rmin, double *__restrict__ rmax) {
+    using Reduce = cub::BlockReduce<double, kUnitThreads>;
+    using Scan = cub::BlockScan<int, kUnitThreads>;
+    __shared__ union {
+        typename Reduce::TempStorage r;
+        typename Scan::TempStorage s;
+    } tmp;
+    __shared__ double s_min, s_max;
+    __shared__ int s_wide;
+    __shared__ bool s_last;
+    const int64_t B = (n_tiles + tpu - 1) / tpu;
+    const int lane = threadIdx.x & 31;
+    // ---- every CTA: the ranges of its runs (one warp per run)
+    const int64_t b = (int64_t)blockIdx.x * (kUnitThreads / 32) + (threadIdx.x >> 5);
+    if (b < B) {
+        double a = INFINITY, z = -INFINITY;
+        const int64_t g = b * tpu + lane;
+        if (lane < tpu && g < n_tiles) {
+            a = tile_lo_of(metric, lo, tile_lo + g);
+            z = tile_hi_of(metric, hi, tile_lo + g);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+            z = fmax(z, __shfl_xor_sync(0xffffffffu, z, o));
+        }
+        if (lane == 0) {
+            rmin[b] = a;
+            rmax[b] = z;
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // ---- the last CTA: the table
+    double vmin = INFINITY, vmax = -INFINITY;
+    for (int64_t i = threadIdx.x; i < B; i += kUnitThreads) {
+        vmin = fmin(vmin, __ldcg(rmin + i));
+        vmax = fmax(vmax, __ldcg(rmax + i));
+    }
+    vmin = Reduce(tmp.r).Reduce(vmin, [](double x, double y) { return fmin(x, y); });
+    __syncthreads();
+    vmax = Reduce(tmp.r).Reduce(vmax, [](double x, double y) { return fmax(x, y); });
+    if (threadIdx.x == 0) {
+        s_min = vmin;
+        s_max = vmax;
+        s_wide = 0;
+        *ticket = 0;  // ready for the next launch
+    }
+    __syncthreads();
+    // a run is wide when its range exceeds 4x the average run's share
+    const double limit = 4.0 * (s_max - s_min) / (double)B;
+    const int64_t per = (B + kUnitThreads - 1) / kUnitThreads;
+    const int64_t b0 = min(B, (int64_t)threadIdx.x * per), b1 = min(B, b0 + per);
+    auto tiles_of = [&](int64_t r) { return (int)(min(n_tiles, (r + 1) * tpu) - r * tpu); };
+    auto wide = [&](int64_t r) { return tpu > 1 && __ldcg(rmax + r) - __ldcg(rmin + r) > limit; };
+    int nw = 0;
+    for (int64_t r = b0; r < b1; ++r) nw += wide(r) ? 1 : 0;
+    if (nw) atomicAdd(&s_wide, nw);
+    __syncthreads();
+    // split only when the wide runs are the exception (a layout that is not
+    // norm-ordered has no narrow runs; single tiles would only add overhead)
+    const bool split = (int64_t)s_wide * 8 <= B;
+    int n_split = 0, n_reg = 0;
+    for (int64_t r = b0; r < b1; ++r) {
+        if (split && wide(r)) n_split += tiles_of(r);
+        else n_reg += 1;
+    }
+    int off_split, off_reg, tot_split;
+    Scan(tmp.s).ExclusiveSum(n_split, off_split, tot_split);
+    __syncthreads();
+    Scan(tmp.s).ExclusiveSum(n_reg, off_reg);
+    off_reg += tot_split;
+    for (int64_t r = b0; r < b1; ++r) {
+        if (split && wide(r)) {
+            for (int64_t g = r * tpu; g < min(n_tiles, (r + 1) * tpu); ++g) {
+                table[2 * off_split] = (int32_t)g;
+                table[2 * off_split + 1] = 1;
+                ++off_split;
+            }
+        } else {
+            table[2 * off_reg] = (int32_t)(r * tpu);
+            table[2 * off_reg + 1] = tiles_of(r);
+            ++off_reg;
+        }
+    }
+    if (threadIdx.x == kUnitThreads - 1) *count = off_reg;
+}
+
 }  // namespace
+
+cudaError_t launch_unit_table(int metric, const int32_t *grp_lo, const int32_t *grp_hi,
+                              int64_t tile_lo, int64_t n_tiles, int tpu, int32_t *table,
+                              int32_t *count, unsigned *ticket, double *scratch, cudaStream_t st) {
+    if (metric == 0 || n_tiles <= 0 || tpu < 1 || tpu > 32 || n_tiles > INT32_MAX)
+        return cudaErrorInvalidValue;
+    const int64_t B = (n_tiles + tpu - 1) / tpu;
+    const unsigned grid = (unsigned)((B + kUnitThreads / 32 - 1) / (kUnitThreads / 32));
+    unit_table_kernel<<<grid, kUnitThreads, 0, st>>>(metric, grp_lo, grp_hi, tile_lo, n_tiles, tpu,
+                                                     table, count, ticket, scratch, scratch + B);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_group_ranges(int metric, const int32_t *sqnorm, const float *norm, int64_t n,
                                 int32_t *lo, int32_t *hi, int64_t groups, cudaStream_t st) {

@@ -1371,6 +1371,118 @@ cudaError_t launch_estimate(const Entry *state, const int32_t *state_cnt, int32_
     return cudaGetLastError();
 }
 
+// Threshold estimate from a sampled pass (filter mode 4): per query, the
+// j-th largest of its nb bucket keys (order-preserving int32 "goodness",
+// qa_filter_tc.cu) by an MSB-first radix select, turned into the final pass's
+// threshold and the order key the check after it compares with.  The key is
+// a real row's goodness and at least j distinct rows reach it, so it plays the
+// role of the j-th best prefix score (estimate_kernel).  Angular goodness is
+// float(dot) / xn, so its score is approximate; the estimate is a heuristic
+// and exactness rests on the check (finalize_kernel), not on it.
+template <int M>
+__global__ void __launch_bounds__(256) est_select_kernel(
+    const int32_t *__restrict__ keys, int64_t ld, int64_t nb, int64_t j,
+    const int32_t *__restrict__ q_sqnorm, const float *__restrict__ q_norm,
+    int32_t *__restrict__ thr, unsigned long long *__restrict__ est) {
+    __shared__ unsigned hist[256];
+    __shared__ unsigned s_digit, s_want;
+    const int64_t q = blockIdx.x;
+    const int32_t *kq = keys + q * ld;
+    unsigned prefix = 0, mask = 0, want = (unsigned)j;  // rank from the top, 1-based
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        hist[threadIdx.x] = 0;
+        __syncthreads();
+        for (int64_t i = threadIdx.x; i < nb; i += 256) {
+            const unsigned u = (unsigned)__ldg(kq + i) ^ 0x80000000u;
+            if ((u & mask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            // lane l owns digits 255 - 8l .. 248 - 8l (descending)
+            const int lane = threadIdx.x;
+            unsigned c[8], tot = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                c[i] = hist[255 - 8 * lane - i];
+                tot += c[i];
+            }
+            unsigned incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const unsigned excl = incl - tot;
+            const unsigned hitm = __ballot_sync(0xffffffffu, incl >= want && excl < want);
+            if (hitm) {
+                const int src = __ffs(hitm) - 1;
+                if (lane == src) {
+                    unsigned acc = excl;
+                    int i = 0;
+                    while (acc + c[i] < want) acc += c[i++];
+                    s_digit = 255u - 8u * (unsigned)lane - (unsigned)i;
+                    s_want = want - acc;
+                }
+            } else if (lane == 0) {
+                s_digit = 0xffffffffu;  // fewer than `want` keys match
+            }
+        }
+        __syncthreads();
+        const unsigned dg = s_digit;
+        want = s_want;
+        __syncthreads();
+        if (dg == 0xffffffffu) {
+            if (threadIdx.x == 0) est[q] = ~0ull;  // thr keeps its pass-all init
+            return;
+        }
+        prefix |= dg << shift;
+        mask |= 255u << shift;
+    }
+    if (threadIdx.x != 0) return;
+    const int32_t g = (int32_t)(prefix ^ 0x80000000u);
+    if (g == INT32_MIN) {  // the j-th bucket saw no row
+        est[q] = ~0ull;
+        return;
+    }
+    Entry e;
+    e.id = 0;
+    e.row = 0;
+    int32_t qq = 0;
+    float qn = 1.0f;
+    if constexpr (M == kIP) {
+        e.skey = skey_from_int((int32_t)(0u - (uint32_t)g));  // score = -dot
+    } else if constexpr (M == kL2) {
+        qq = q_sqnorm[q];
+        e.skey = skey_from_int((int32_t)((uint32_t)qq - (uint32_t)g));  // qq + xx - 2 dot
+    } else {
+        qn = q_norm[q];
+        const int32_t fb = g < 0 ? (g ^ 0x7fffffff) : g;
+        e.skey = skey_from_double(1.0 - (double)__int_as_float(fb) / (double)qn);
+    }
+    thr[q] = threshold_of<M>(e, qq, qn);
+    est[q] = e.skey;
+}
+
+cudaError_t launch_est_select(const int32_t *keys, int64_t ld, int64_t nb, int64_t nq, int64_t j,
+                              int metric, const int32_t *q_sqnorm, const float *q_norm,
+                              int32_t *thr, unsigned long long *est, cudaStream_t st) {
+    if (nq == 0) return cudaSuccess;
+    if (nq > 0x7fffffff || j < 1) return cudaErrorInvalidValue;
+    const unsigned grid = (unsigned)nq;
+    switch (metric) {
+        case kIP:
+            est_select_kernel<kIP><<<grid, 256, 0, st>>>(keys, ld, nb, j, q_sqnorm, q_norm, thr, est);
+            break;
+        case kL2:
+            est_select_kernel<kL2><<<grid, 256, 0, st>>>(keys, ld, nb, j, q_sqnorm, q_norm, thr, est);
+            break;
+        default:
+            est_select_kernel<kAngular><<<grid, 256, 0, st>>>(keys, ld, nb, j, q_sqnorm, q_norm,
+                                                              thr, est);
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_check_estimate(const Entry *state, const int32_t *state_cnt,
                                   const unsigned long long *est, int64_t nq, int64_t k,
                                   int32_t *redo, int32_t *any_redo, cudaStream_t st) {

@@ -41,28 +41,26 @@ class Int8Index:
     @classmethod
     def from_params(cls, x: torch.Tensor, params: QuantizerParams, metric: Metric,
                     id_offset: int = 0, sort_rows: bool = True) -> "Int8Index":
-        """Encode ``x`` with ``params``.  The stored rows are ordered by code
-        norm (ids still report positions in ``x``), which keeps the scan's
-        per-unit filter bounds tight and its estimate prefix a stratified
-        sample."""
+        """Encode ``x`` with ``params``.  The stored rows are ordered for the
+        scan (ids still report positions in ``x``): narrow per-unit filter
+        bounds, and a threshold-estimate sample (every stride-th tile) that
+        spans the whole index."""
         device = x.device
         k, sb, se = (torch.from_numpy(np.array(a, dtype=np.float32)).to(device)
                      for a in (params.k, params.sb, params.se))
         codes = dev.encode(x, k, sb, se, params.bits)
         metric = Metric(metric)
         if sort_rows:
-            # The threshold estimate reads the first rows as a sample of the
-            # whole index, so clustered or sorted input must not reach it in
-            # caller order.  L2: norm bands after a stratified sample region
-            # (qa_layout.cu; tight per-unit bounds); angular: plain norm bands
-            # (narrow norms); inner product: a fixed pseudo-random order -- its
-            # bound does not use norms, and norm strata starve the prefix of
-            # the high-norm rows where the best dots live (2.5x the
-            # candidates and failed estimates on cfg4 in norm order).
+            # L2 / angular: interleaved norm blocks (qa_layout.cu) -- every
+            # 4096-row block is one narrow norm band, so work units have tight
+            # bounds and the strided estimate sample meets every band.  Inner
+            # product: a fixed pseudo-random order -- its bound does not use
+            # norms, and norm order clusters the high-norm rows where the best
+            # dots live (2.5x the candidates and failed estimates on cfg4).
             if metric == Metric.INNER_PRODUCT:
                 codes = codes.shuffled()
             else:
-                codes = codes.sorted_by_norm(stratify=metric == Metric.L2_SQUARED)
+                codes = codes.sorted_by_norm(stratify=False)
         return cls(params, metric, codes, k, sb, se, id_offset)
 
     def codes_in_input_order(self) -> np.ndarray:

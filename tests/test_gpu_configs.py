@@ -76,7 +76,7 @@ def test_cfg2_full_size_l2(oracle):
     np.testing.assert_array_equal(qc.to_host(), oracle.encode(Q, k_, sb, se, 8))
     sc, ids = index.search_codes(qc, 100)
     st = _lib.last_scan_stats()
-    assert st["rounds"] <= 4, st  # dense round, prefix pass, estimated final pass
+    assert st["rounds"] == 2, st  # the estimate pass, one pass over every row
     _check(oracle, Xc, qc.to_host(), sc, ids, 100, 1, 48)
 
 

@@ -423,30 +423,36 @@ def test_filter_bounds_hold_on_large_dots(oracle, metric):
 
 
 @pytest.mark.parametrize("metric", [0, 1, 2])
-@pytest.mark.parametrize("force_j1", [None, "1"])
-def test_two_level_estimate_exact(oracle, monkeypatch, metric, force_j1):
-    # Two-level estimate: round 0's j1-th best bounds the rest of the
-    # prefix, the prefix's j-th best bounds the rest of the index, and the
-    # final check needs the k-th at least as good as both.  j1 = 1 makes the
-    # first level fail for many queries (recompute path); exact either way.
+@pytest.mark.parametrize("force_j", [None, "1"])
+@pytest.mark.parametrize("layout", ["plain", "bands"])
+def test_sampled_estimate_exact(oracle, monkeypatch, metric, force_j, layout):
+    # The estimate pass (filter mode 4) reads every stride-th tile, keeps the
+    # best row per (query, bucket), and the j-th best bucket bounds one pass
+    # over every row; the check after it needs the k-th at least as good.
+    # j = 1 makes the estimate fail for most queries (recompute path); exact
+    # either way, on caller order and on the interleaved norm blocks.
     from paper_2110_08919_b200 import _lib
 
     monkeypatch.setenv("QA_B200_EST_ROWS", "8192")
-    if force_j1:
-        monkeypatch.setenv("QA_B200_EST1_J", force_j1)
+    if force_j:
+        monkeypatch.setenv("QA_B200_EST_J", force_j)
     rng = np.random.default_rng(500 + metric)
     X = _rand_codes(rng, 60_000, 64, -30, 31, nonzero=True)
     Q = _rand_codes(rng, 300, 64, -30, 31, nonzero=True)
-    db = dev.DeviceCodes.from_host(X).sorted_by_norm()
+    db = dev.DeviceCodes.from_host(X)
+    if layout == "bands":
+        db = db.sorted_by_norm(stratify=False)
     qs = dev.DeviceCodes.from_host(Q)
     sc, ids = dev.scan_topk(db, qs, 20, metric)
     st = _lib.last_scan_stats()
     osc, oids = _scan_oracle(oracle, X, Q, 20, metric)
     np.testing.assert_array_equal(ids.cpu().numpy(), oids)
     np.testing.assert_array_equal(sc.cpu().numpy(), osc)
-    assert st["rounds"] <= 3 + (3 * st["retries"] + 20)
-    if force_j1:
+    assert st["rounds"] <= 2 + (3 * st["retries"] + 20)
+    if force_j:
         assert st["retries"] >= 1
+    else:
+        assert st["rounds"] == 2 and st["retries"] == 0, st
 
 
 @pytest.mark.parametrize("metric", [0, 1, 2])
