@@ -71,7 +71,20 @@ __host__ __device__ constexpr bool exact_epi() {
     return M == kL2;
 #endif
 }
-constexpr int kThreads = 640;
+// MMA issuers: warp 1 plus warps 20.. (kMmaWarpsMax in all).  One warp issuing
+// every tile's MMAs was the critical path of short-K passes: its ~150
+// dependent SASS instructions per tile (waits, descriptor moves into uniform
+// registers, elect, 5 MMAs, 2 commits) take ~1000 cycles, four times the
+// tile's tensor time at K = 128 (ncu: no hot spot in that warp, every
+// instruction waiting on the one before it).  Tile T of a CTA is issued by
+// MMA warp T mod W, W dividing the accumulator count, so every accumulator
+// has one issuer and every barrier wait still sees consecutive phases.
+#ifndef QA_MMA_WARPS
+#define QA_MMA_WARPS 4
+#endif
+constexpr int kMmaWarpsMax = QA_MMA_WARPS;
+constexpr int kMmaWarpX = 20;    // first extra MMA warp
+constexpr int kThreads = 640 + 32 * (kMmaWarpsMax - 1);
 constexpr int kBiasWarp = 3;
 constexpr int kEpiWarp0 = 4;
 constexpr int kEpiThreads = 512;
@@ -90,8 +103,51 @@ __host__ __device__ constexpr int nacc() { return 512 / N < 8 ? 512 / N : 8; }
 // MMAs: each epilogue thread holds its 16 columns' bounds in registers and
 // compares directly.  The tensor pipe then runs 4 MMAs per tile instead of
 // 4 + reps (measured -20 % per tile with the bias MMAs removed).
+#ifndef QA_DIRECT_N
+#define QA_DIRECT_N 64
+#endif
 template <int N>
-__host__ __device__ constexpr bool direct_bounds() { return N == 64; }  // bias MMAs per tile at most (|bias| <= 4.1M)
+__host__ __device__ constexpr bool direct_bounds() { return N <= QA_DIRECT_N; }  // bias MMAs per tile at most (|bias| <= 4.1M)
+
+// Epilogue organisation of the filter pass proper (kKind 0) for N >= 128:
+// the 16 epilogue warps form G = min(accumulators, 4) groups; group g takes
+// the CTA's tiles T = g, g + G, ... (the accumulators a = g mod G), each of
+// its warps one TMEM lane quarter x N / (warps per quarter) columns, read 16
+// columns at a time with the next load in flight while the current values
+// are tested.  With every warp on every tile (the other kinds, and N = 64)
+// each warp paid the tile's fixed costs (barrier wait, release, loop) per 32
+// columns and the TMEM load latency was exposed once per tile; the groups
+// pay them once per 128 columns, overlap the load with the tests, and work
+// on G tiles at a time.
+#ifndef QA_EPI_GROUPS
+#define QA_EPI_GROUPS 1
+#endif
+template <int N, int kKind>
+__host__ __device__ constexpr bool grouped_epi() {
+    return QA_EPI_GROUPS != 0 && kKind == 0 && !direct_bounds<N>();
+}
+#ifndef QA_EPI_ACC_PER_GROUP
+#define QA_EPI_ACC_PER_GROUP 2
+#endif
+// A lane whose 8-column group holds a non-negative value parks the group
+// (8 values + a key) in its warp's buffer; the warp tests the parked values
+// one per lane once kHitDrain groups are waiting (and at the end of the work
+// unit).  Testing them in place ran the exact test one candidate at a time
+// with the other lanes idle -- a third of the epilogue's time for ~10
+// candidates per 16k-value tile.
+constexpr int kHitDrain = 8;
+constexpr int kHitCap = kHitDrain + 32;  // one more group from every lane
+template <int N>
+__host__ __device__ constexpr int hit_words() {
+    return direct_bounds<N>() ? 0 : 16 * kHitCap * 9;
+}
+template <int N>
+__host__ __device__ constexpr int epi_groups() {
+    // two accumulators per group: the MMAs of a group's next tile run while
+    // it tests the current one
+    constexpr int g = nacc<N>() / QA_EPI_ACC_PER_GROUP;
+    return g < 1 ? 1 : (g > 4 ? 4 : g);
+}
 
 // Instruction descriptor for kind::i8: D=S32 (bits 4-5 = 2), A/B signed
 // int8 (bits 7-9, 10-12 = 1), both K-major, N>>3 at 17, M>>4 at 24.
@@ -134,6 +190,7 @@ struct Params {
     int b_slots;            // 1 or 2 query-tile buffers
     int stage_cap;          // survivor staging entries per slot
     int norm_bulk;          // norm arrays 16-byte aligned (bulk-copyable)
+    int mma_warps;          // MMA issuer warps (divides the accumulator count)
     uint32_t idesc;         // MMA instruction descriptor (signed or unsigned bytes)
 };
 
@@ -209,7 +266,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int32_t *qcnt_all = exc_s + 2 * (N / 32);                       // [2][N] staged per query
     int32_t *qbase = qcnt_all + 2 * N;                              // [N] (flush warp)
     int32_t *bnd_all = qbase + N;                                   // [2][N] direct bounds
-    uint64_t *bars = (uint64_t *)(bnd_all + 2 * N);
+    // grouped epilogue: per-warp buffers of candidate 8-column groups
+    int32_t *hit_all = bnd_all + 2 * N;                             // [16][kHitCap][8 + 1]
+    uint64_t *bars = (uint64_t *)(hit_all + hit_words<N>());
     uint64_t *a_full = bars;
     uint64_t *a_empty = a_full + p.stages;
     uint64_t *b_full = a_empty + p.stages;
@@ -236,9 +295,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(b_full + s, 1);
-            mbar_init(b_empty + s, 1);
+            mbar_init(b_empty + s, p.mma_warps);        // every MMA warp's commit
             mbar_init(bias_full + s, 1);
-            mbar_init(bias_empty + s, 1 + kEpiWarps);  // MMA commit + epilogue warps
+            mbar_init(bias_empty + s, p.mma_warps + kEpiWarps);  // MMA commits + epilogue warps
             mbar_init(stage_full + s, kEpiWarps);
             mbar_init(stage_free + s, 1);               // flush warp
             mbar_init(norm_full + s, 1);
@@ -246,11 +305,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int s = 0; s < kNacc; ++s) {
             mbar_init(acc_full + s, 1);
-            mbar_init(acc_empty + s, kEpiWarps);
+            mbar_init(acc_empty + s, grouped_epi<N, kKind>() ? kEpiWarps / epi_groups<N>() : kEpiWarps);
         }
         for (int s = 0; s < kURing; ++s) {
             mbar_init(unit_full + s, 1);
-            mbar_init(unit_empty + s, kEpiWarps + 3);  // MMA, bias, flush, epilogue warps
+            mbar_init(unit_empty + s, kEpiWarps + 2 + p.mma_warps);  // MMA, bias, flush, epilogue warps
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -345,22 +404,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else if (warp == 1) {
-        // =============================== MMA issuer =====================
-        // The whole warp walks the pipeline (uniform control flow, no lanes
-        // parked at a warp barrier); lane 0 issues.  Descriptors are formed
-        // once: the start-address field is the low 14 bits (addr >> 4) and
-        // smem addresses stay below 256 KiB, so stepping a descriptor is a
-        // 64-bit add of (bytes >> 4).
+    } else if (warp == 1 || warp >= kMmaWarpX) {
+        // =============================== MMA issuers ====================
+        // MMA warp mw issues the CTA's tiles T = mw, mw + W, ... (T counts
+        // tiles across work units).  The whole warp walks the pipeline
+        // (uniform control flow, no lanes parked at a warp barrier); one
+        // elected lane issues.  Descriptors are formed once: the
+        // start-address field is the low 14 bits (addr >> 4) and smem
+        // addresses stay below 256 KiB, so stepping a descriptor is a 64-bit
+        // add of (bytes >> 4).
+        const int nw = p.mma_warps;
+        const int mw = warp == 1 ? 0 : warp - kMmaWarpX + 1;
+        if (mw < nw) {
         const uint32_t idesc = p.idesc;
         const uint64_t adesc0 = make_desc<SW>(smem_u32(sA));
         const uint64_t bdesc0 = make_desc<SW>(smem_u32(sB));
         const uint64_t abias_desc = make_desc<32>(smem_u32(sAbias));
         const uint64_t bbias_desc0 = make_desc<32>(smem_u32(sBbias));
-        int stage = 0;
-        uint32_t aph = 0;
-        int acc = 0;
-        uint32_t accph = 0;
+        // this warp's next tile: its A stage / phase and accumulator / phase
+        int stage = (mw * p.kchunks) % p.stages;
+        uint32_t aph = (uint32_t)((mw * p.kchunks) / p.stages) & 1;
+        int acc = mw % kNacc;
+        uint32_t accph = (uint32_t)(mw / kNacc) & 1;
+        const int skip = (nw - 1) * p.kchunks;  // stages of the other warps' tiles
+        int first = mw;  // this warp's first tile of the unit
         for (int it = 0;; ++it) {
             const int u = unit_take(it);
             if (u < 0) break;
@@ -377,7 +444,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t bdesc = bdesc0 + (uint64_t)(((uint32_t)bslot * b_bytes) >> 4);
             const uint64_t bbias_desc = bbias_desc0 + (uint64_t)((slot * N * kBiasK) >> 4);
             const int reps = reps_s[slot];  // written before bias_full
-            for (int ti = 0; ti < ntl; ++ti) {
+            int ti = first;
+            for (; ti < ntl; ti += nw) {
                 WSTAT(4, mbar_wait_spin(acc_empty + acc, accph ^ 1));
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + (uint32_t)(acc * N);
@@ -401,16 +469,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mma_bias_elect(tmem_d, abias_desc, bbias_desc, idesc);
                 mma_bias_commit_elect(tmem_d, abias_desc, bbias_desc, idesc,
                                       reps == 0 ? 0u : 1u, smem_u32(acc_full + acc));
-                if (++acc == kNacc) {
-                    acc = 0;
+                // on to this warp's next tile (nw tiles further)
+                stage += skip;
+                while (stage >= p.stages) {
+                    stage -= p.stages;
+                    aph ^= 1;
+                }
+                acc += nw;
+                if (acc >= kNacc) {
+                    acc -= kNacc;
                     accph ^= 1;
                 }
             }
+            first = ti - ntl;
+            // this warp's MMAs of the unit are done with the query tile and
+            // the bias tile (a warp without a tile in the unit arrives at once)
             if (lane == 0) {
                 tc_commit(b_empty + bslot);
                 tc_commit(bias_empty + slot);
             }
             __syncwarp();
+        }
         }
     } else if (warp == kBiasWarp) {
         // =============================== bias builder ===================
@@ -657,6 +736,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t tm_warp = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)col0;
         int acc = 0;
         uint32_t accph = 0;
+        int efirst = 0;  // grouped epilogue: this group's first tile of the unit
+        (void)efirst;
         for (int it = 0;; ++it) {
             const int u = unit_take(it);
             if (u < 0) break;
@@ -687,7 +768,133 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int32_t *unit_norm = norm_all + slot * kUnitRowsMax;
             int32_t wrow0 = unit_row0 + quarter * 32;
             const int ntl = (int)(tile1 - tile0);
-            if constexpr (lean) {
+            if constexpr (grouped_epi<N, kKind>()) {
+                // ---- filter pass, the hot loop (grouped, see epi_groups) ----
+                constexpr int kG = epi_groups<N>();
+                constexpr int kWPG = kEpiWarps / kG;      // warps per group
+                constexpr int kCW = N / (kWPG / 4);       // columns per warp
+                constexpr int kCh = 16;                   // columns per TMEM load
+                constexpr int kNCh = kCW / kCh;
+                static_assert(kNCh % 2 == 0, "chunks are taken in pairs");
+                const int rest = ew >> 2;                 // 0..3 within the lane quarter
+                const int grp = rest % kG;
+                const int gcol0 = (rest / kG) * kCW;      // first column of this warp
+                const uint32_t tm_g = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)gcol0;
+                if (it == 0) {
+                    acc = grp;  // group g owns accumulators g, g + G, ...
+                    accph = 0;
+                    efirst = grp;
+                }
+                uint32_t excw = 0;  // exceptional 32-column chunks of this warp
+                for (int ci = 0; ci < kCW / 32; ++ci)
+                    if (exc_s[slot * (N / 32) + (gcol0 + ci * 32) / 32]) excw |= 1u << ci;
+                int32_t *hvals = hit_all + ew * (kHitCap * 9);  // [kHitCap][8]
+                int32_t *hkeys = hvals + kHitCap * 8;           // [kHitCap]
+                const uint32_t hvals_addr = smem_u32(hvals);
+                const uint32_t lt_mask = (1u << lane) - 1u;
+                int hcnt = 0;  // parked groups (warp-uniform)
+                // the parked values, one per lane: exact test, survivors staged
+                auto drain = [&]() {
+                    __syncwarp();
+                    for (int i = lane; i < hcnt * 8; i += 32) {
+                        const uint32_t key = (uint32_t)hkeys[i >> 3];
+                        const int32_t vj = hvals[i];
+                        if (vj < 0 && !(key >> 31)) continue;
+                        const int qloc = (int)(key & 0xffu) + (i & 7);
+                        const int rowrel = (int)((key >> 8) & 0xfffu);
+                        const int32_t dot = (int32_t)((uint32_t)vj -
+                                                      (uint32_t)lds32(bias_addr + 4u * (uint32_t)qloc));
+                        if constexpr (kExactInEpilogue) {
+                            int32_t xx = 0;
+                            float inv_xn = 0.f;
+                            if constexpr (M != kIP) {
+                                const int32_t nb = unit_norm[rowrel];  // staged by the bias warp
+                                if constexpr (M == kL2) xx = nb;
+                                if constexpr (M == kAngular) inv_xn = __int_as_float(nb);  // 1/xn
+                            }
+                            const int32_t T = lds32(thr_addr + 4u * (uint32_t)qloc);
+                            if (!passes<M>(dot, T, xx, inv_xn)) continue;
+                        }
+                        const int e = atom_add_smem(stage_n_addr, 1);
+                        if (e < stage_cap) {
+                            // slot among the query's survivors: the flush warp's
+                            sts64(stage_addr + 8u * (uint32_t)e,
+                                  (uint32_t)qloc | ((uint32_t)rowrel << 20), (uint32_t)dot);
+                        } else {
+                            // staging full: direct append (slow, rare)
+                            const int32_t sl = atomicAdd(a.ccount + q0 + qloc, 1);
+                            if (sl < a.cap)
+                                a.cand[(q0 + qloc) * a.cap + sl] = Cand{unit_row0 + rowrel, dot};
+                        }
+                    }
+                    __syncwarp();
+                    hcnt = 0;
+                };
+                // park the lanes' candidate groups (warp-uniform control flow)
+                auto park8 = [&](const int32_t *c8, bool hit, int qc0, bool exc, int32_t row) {
+                    const unsigned m = __ballot_sync(0xffffffffu, hit);
+                    if (!m) return;
+                    if (hit) {
+                        const int pos = hcnt + __popc(m & lt_mask);
+                        const uint32_t va = hvals_addr + 32u * (uint32_t)pos;
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(va), "r"(c8[0]),
+                                     "r"(c8[1]), "r"(c8[2]), "r"(c8[3])
+                                     : "memory");
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(va + 16u),
+                                     "r"(c8[4]), "r"(c8[5]), "r"(c8[6]), "r"(c8[7])
+                                     : "memory");
+                        hkeys[pos] = (int32_t)((uint32_t)qc0 | ((uint32_t)(row - unit_row0) << 8) |
+                                               (exc ? 0x80000000u : 0u));
+                    }
+                    hcnt += __popc(m);
+                    if (hcnt >= kHitDrain) drain();
+                };
+                // one 16-column chunk: sign test of each 8-column group; the
+                // rare chunk with a candidate parks its groups
+                auto test16 = [&](const int32_t (&v)[kCh], int ch, int32_t row) {
+                    const int32_t g0 = (v[0] & v[1] & v[2]) & (v[3] & v[4] & v[5]) & (v[6] & v[7]);
+                    const int32_t g1 =
+                        (v[8] & v[9] & v[10]) & (v[11] & v[12] & v[13]) & (v[14] & v[15]);
+                    const bool exc = (excw >> (ch * kCh / 32)) & 1u;
+                    if (!__any_sync(0xffffffffu, (g0 & g1) >= 0 || exc)) return;
+                    const bool rowok = row < r_hi;
+                    const int qc0 = gcol0 + ch * kCh;
+                    park8(v, rowok && (g0 >= 0 || exc), qc0, exc, row);
+                    park8(v + 8, rowok && (g1 >= 0 || exc), qc0 + 8, exc, row);
+                };
+                int ti = efirst;
+                for (; ti < ntl; ti += kG) {
+                    const int32_t row = wrow0 + ti * kBlockM + lane;
+                    WSTAT(11, mbar_wait(acc_full + acc, accph));
+                    tc_fence_after();
+                    const uint32_t ta = tm_g + (uint32_t)(acc * N);
+                    int32_t va[kCh], vb[kCh];
+                    tmem_ld_cols<kCh>(ta, va);
+#pragma unroll
+                    for (int ch = 0; ch < kNCh; ch += 2) {
+                        tmem_wait_regs(va);
+                        tmem_ld_cols<kCh>(ta + (uint32_t)((ch + 1) * kCh), vb);
+                        test16(va, ch, row);
+                        tmem_wait_regs(vb);
+                        if (ch + 2 < kNCh) {
+                            tmem_ld_cols<kCh>(ta + (uint32_t)((ch + 2) * kCh), va);
+                        } else {
+                            // every column is in registers: hand the accumulator back
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(acc_empty + acc);
+                        }
+                        test16(vb, ch + 1, row);
+                    }
+                    acc += kG;
+                    if (acc >= kNacc) {
+                        acc -= kNacc;
+                        accph ^= 1;
+                    }
+                }
+                efirst = ti - ntl;
+                if (hcnt) drain();  // the unit's bias, norms and staging slot end here
+            } else if constexpr (lean) {
                 // ---- filter pass, the hot loop ----
                 // Fast path per tile: TMEM -> registers, one sign bit per
                 // 8-column group (AND-reduction), and the accumulator is
@@ -1132,14 +1339,33 @@ cudaError_t launch_t(const FilterArgs &a, cudaStream_t st) {
                          kBlockM * kBiasK + 2 * (size_t)N * kBiasK +
                          2 * (size_t)p.stage_cap * sizeof(Staged) +
                          (M == kIP || !exact_epi<M>() ? 0 : 2 * (size_t)kUnitRowsMax * sizeof(int32_t)) +
-                         (9 * N + 2 * (N / 32)) * sizeof(int32_t) + 512;
+                         (9 * N + 2 * (N / 32) + hit_words<N>()) * sizeof(int32_t) + 512;
+#ifdef QA_WAIT_STATS
+    const size_t budget = 227 * 1024 - 3072;  // the static wait counters (2 KiB with alignment)
+#else
     const size_t budget = 227 * 1024;
+#endif
     const size_t stage_bytes = (size_t)kBlockM * SW;
     // each stage also costs two 8-byte mbarriers
     if (fixed + 2 * (stage_bytes + 16) > budget) return cudaErrorNotSupported;
     int stages = (int)((budget - fixed) / (stage_bytes + 16));
     if (stages > kn.max_stages) stages = kn.max_stages;
     p.stages = stages;
+    {
+        // every accumulator gets one issuer (W divides the accumulator
+        // count), and a warp may run ahead of the others by a full set of
+        // accumulators: the A ring must hold those tiles for the stage
+        // barriers to see consecutive phases
+        int w = std::min(kMmaWarpsMax, nacc<N>());
+        while (w > 1 && (nacc<N>() % w != 0)) --w;
+        if (stages < nacc<N>() * p.kchunks) w = 1;
+        static const int force_w = [] {  // diagnostics: QA_B200_MMA_WARPS=1/2/4
+            const char *v = getenv("QA_B200_MMA_WARPS");
+            return v ? atoi(v) : 0;
+        }();
+        if (force_w >= 1 && force_w <= w && nacc<N>() % force_w == 0) w = force_w;
+        p.mma_warps = w;
+    }
     const size_t smem = fixed + (size_t)stages * (stage_bytes + 16);
     auto kern = a.mode == 0 ? filter_tc_kernel<SW, N, M, 0>
                             : (a.mode == 4 ? filter_tc_kernel<SW, N, M, 2> : filter_tc_kernel<SW, N, M, 1>);

@@ -228,6 +228,18 @@ __device__ __forceinline__ void tmem_wait() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// tcgen05.wait::ld that names the 16 destination registers of an earlier
+// tcgen05.ld as in-out operands: their consumers then depend on the wait
+// (with other loads in flight the compiler must not move a use above it).
+__device__ __forceinline__ void tmem_wait_regs(int32_t (&v)[16]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                   "+r"(v[6]), "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]),
+                   "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
+                 :
+                 : "memory");
+}
+
 // tcgen05.ld of C (16 or 32) consecutive accumulator columns of this warp's
 // 32 TMEM lanes; the registers are valid after tmem_wait().
 template <int C>
