@@ -84,8 +84,12 @@ __host__ __device__ constexpr bool exact_epi() {
 #endif
 constexpr int kMmaWarpsMax = QA_MMA_WARPS;
 constexpr int kMmaWarpX = 20;    // first extra MMA warp
-constexpr int kThreads = 640 + 32 * (kMmaWarpsMax - 1);
+// A second bias builder (the last warp) takes the odd work units: runs of
+// single-tile units (the unit table's wide-norm blocks) are shorter than one
+// builder's latency per unit (global loads, the norm copy, the digits).
+constexpr int kThreads = 640 + 32 * (kMmaWarpsMax - 1) + 32;
 constexpr int kBiasWarp = 3;
+constexpr int kBiasWarp2 = kThreads / 32 - 1;
 constexpr int kEpiWarp0 = 4;
 constexpr int kEpiThreads = 512;
 constexpr int kStageCapDefault = 2048;  // survivors staged in smem per work unit
@@ -309,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int s = 0; s < kURing; ++s) {
             mbar_init(unit_full + s, 1);
-            mbar_init(unit_empty + s, kEpiWarps + 2 + p.mma_warps);  // MMA, bias, flush, epilogue warps
+            mbar_init(unit_empty + s, kEpiWarps + 3 + p.mma_warps);  // MMA, 2 bias, flush, epilogue warps
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -404,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else if (warp == 1 || warp >= kMmaWarpX) {
+    } else if (warp == 1 || (warp >= kMmaWarpX && warp != kBiasWarp2)) {
         // =============================== MMA issuers ====================
         // MMA warp mw issues the CTA's tiles T = mw, mw + W, ... (T counts
         // tiles across work units).  The whole warp walks the pipeline
@@ -491,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
         }
         }
-    } else if (warp == kBiasWarp) {
+    } else if (warp == kBiasWarp || warp == kBiasWarp2) {
         // =============================== bias builder ===================
         // Per work unit and query column: the bound B_q (see header), the
         // digit sum S_q = ceil(-B_q / 127) clamped to [kSMin, kSMax] (a bias
@@ -501,10 +505,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // two units ahead of the MMA.
         constexpr int kQPL = N / 32;  // query columns per lane
         const bool filtered = (a.mode == 0 || a.mode == 3);
+        const int my_slot = warp == kBiasWarp ? 0 : 1;
         for (int it = 0;; ++it) {
             const int u = unit_take(it);
             if (u < 0) break;
             const int slot = it & 1;
+            if (slot != my_slot) continue;  // the other builder's unit
             const uint32_t ph = (it >> 1) & 1;
             int64_t t, b, tile0, tile1;
             unit_tb(p, u, t, b);
@@ -873,11 +879,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int ch = 0; ch < kNCh; ch += 2) {
                         tmem_wait_regs(va);
-                        tmem_ld_cols<kCh>(ta + (uint32_t)((ch + 1) * kCh), vb);
+                        tmem_ld16_before(ta + (uint32_t)((ch + 1) * kCh), vb, va[0]);
                         test16(va, ch, row);
                         tmem_wait_regs(vb);
                         if (ch + 2 < kNCh) {
-                            tmem_ld_cols<kCh>(ta + (uint32_t)((ch + 2) * kCh), va);
+                            tmem_ld16_before(ta + (uint32_t)((ch + 2) * kCh), va, vb[0]);
                         } else {
                             // every column is in registers: hand the accumulator back
                             tc_fence_before();
