@@ -79,6 +79,9 @@ __host__ __device__ constexpr bool exact_epi() {
 // instruction waiting on the one before it).  Tile T of a CTA is issued by
 // MMA warp T mod W, W dividing the accumulator count, so every accumulator
 // has one issuer and every barrier wait still sees consecutive phases.
+#ifndef QA_UNIT_LOOKAHEAD
+#define QA_UNIT_LOOKAHEAD 1
+#endif
 #ifndef QA_MMA_WARPS
 #define QA_MMA_WARPS 4
 #endif
@@ -198,32 +201,16 @@ struct Params {
     uint32_t idesc;         // MMA instruction descriptor (signed or unsigned bytes)
 };
 
-// Work unit u -> (query tile t, row block b).  Query tiles vary fastest, so
-// the CTAs working at the same time share row blocks (L2 reuse of the
-// streamed database tiles).  Units are handed out dynamically (a global
-// counter read by the producer, published through the unit-id ring): the
-// cost of a unit is dominated by its survivors, which concentrate in the
-// norm bands near the queries' -- a static round-robin left the slowest CTA
-// at 3.7x the fastest on cfg2.
-__device__ __forceinline__ void unit_tb(const Params &p, int64_t u, int64_t &t, int64_t &b) {
-    t = u % p.n_qtiles;
-    b = u / p.n_qtiles;
-}
-
-// Tiles [tile0, tile1) of row unit b (relative to r_lo): fixed-size units, or
-// the pass's unit table (launch_unit_table: wide-norm blocks split into
-// single tiles, listed first).
-__device__ __forceinline__ void unit_tiles(const Params &p, int64_t b, int64_t &tile0,
-                                           int64_t &tile1) {
-    if (p.a.unit_table) {
-        const int2 e = __ldg(reinterpret_cast<const int2 *>(p.a.unit_table) + b);
-        tile0 = e.x;
-        tile1 = (int64_t)e.x + e.y;
-    } else {
-        tile0 = b * p.tiles_per_unit;
-        tile1 = min(p.n_tiles, tile0 + p.tiles_per_unit);
-    }
-}
+// Work unit u -> (query tile t = u mod n_qtiles, row unit b = u / n_qtiles).
+// Query tiles vary fastest, so the CTAs working at the same time share row
+// blocks (L2 reuse of the streamed database tiles).  Row unit b covers fixed
+// runs of tiles_per_unit tiles, or the entry b of the pass's unit table
+// (launch_unit_table: wide-norm blocks split into single tiles, listed
+// first).  Units are handed out dynamically (a global counter read by the
+// producer, resolved and published through the unit ring): the cost of a unit
+// is dominated by its survivors, which concentrate in the norm bands near the
+// queries' -- a static round-robin left the slowest CTA at 3.7x the fastest
+// on cfg2.
 
 // kKind 0: the filter pass proper (mode 0); 1: the dense, masked-dense and
 // diagnostic passes (modes 1-3); 2: the sampled estimate (mode 4).  Separate
@@ -289,7 +276,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t *tmem_base_s = (uint32_t *)(unit_empty + kURing);
     int32_t *stage_n_all = (int32_t *)(tmem_base_s + 1);  // [2]
     int32_t *reps_s = stage_n_all + 2;  // [2] bias MMAs per tile of the unit
-    int32_t *uring = reps_s + 2;        // [kURing] unit ids (-1: no more work)
+    // [kURing] published work units {query tile, row unit, first tile, tiles}
+    // (x = -1: no more work), 16-byte aligned
+    unsigned char *uring_b = (unsigned char *)(reps_s + 2);
+    uring_b += (16u - (smem_u32(uring_b) & 15u)) & 15u;
+    int4 *uring = (int4 *)uring_b;
     constexpr int kEpiWarps = kEpiThreads / 32;
 
     if (threadIdx.x == 0) {
@@ -339,13 +330,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     // the it-th unit of this CTA (every consumer role walks the same
     // sequence); the slot is handed back as soon as the id is read
-    auto unit_take = [&](int it) -> int {
+    auto unit_take = [&](int it) -> int4 {
         const int s = it & (kURing - 1);
         mbar_wait(unit_full + s, (uint32_t)(it / kURing) & 1);
-        const int u = *(volatile int *)(uring + s);
+        int4 e;
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(e.x), "=r"(e.y), "=r"(e.z), "=r"(e.w)
+                     : "r"(smem_u32(uring + s))
+                     : "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(unit_empty + s);
-        return u;
+        return e;
     };
 
     if (warp == 0) {
@@ -353,33 +348,73 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t aph = 0;
-            // unit ids are handed out by a global counter (dynamic
-            // scheduling: survivors concentrate in a few norm bands, so
-            // units differ in cost by several x) and published to the other
-            // roles through a 4-slot ring, two units ahead
-            int fetched = 0;
-            bool done = false;
-            const int64_t n_units =
-                a.unit_table ? (int64_t)__ldg(a.unit_count) * p.n_qtiles : p.n_units;
-            auto fetch = [&]() {
-                if (done) return;
-                const int s = fetched & (kURing - 1);
-                WSTAT(14, mbar_wait_sleep(unit_empty + s, ((uint32_t)(fetched / kURing) & 1) ^ 1));
-                const unsigned v = atomicAdd(a.sched, 1u);
-                const int u = v < (unsigned)n_units ? (int)v : -1;
-                *(volatile int *)(uring + s) = u;
-                mbar_arrive(unit_full + s);
-                done = u < 0;
-                ++fetched;
+            // Units are handed out by a global counter (dynamic scheduling:
+            // survivors concentrate in a few norm bands, so units differ in
+            // cost by several x).  The producer resolves each unit (query
+            // tile, row unit, its tiles -- a table lookup for table passes)
+            // and publishes it to the other roles through a 4-slot ring, two
+            // units ahead.  The counter's atomic, the table load and the
+            // publication of consecutive units are pipelined (each waits one
+            // iteration for its predecessor): a run of single-tile units
+            // does not pay two global round trips per unit, and no consumer
+            // role touches global memory or 64-bit division for a unit.
+            const unsigned n_units = (unsigned)(
+                a.unit_table ? (int64_t)__ldg(a.unit_count) * p.n_qtiles : p.n_units);
+            const unsigned nqt = (unsigned)p.n_qtiles;
+            auto resolve = [&](unsigned v) -> int2 {
+                if (v >= n_units) return make_int2(0, 0);
+                const unsigned rb = v / nqt;
+                if (a.unit_table) return __ldg(reinterpret_cast<const int2 *>(a.unit_table) + rb);
+                const int64_t t0 = (int64_t)rb * p.tiles_per_unit;
+                return make_int2((int)t0, (int)(min(p.n_tiles, t0 + p.tiles_per_unit) - t0));
             };
-            fetch();
-            fetch();
+            auto publish = [&](int k, unsigned v, int2 e) {
+                const int s = k & (kURing - 1);
+                WSTAT(14, mbar_wait_sleep(unit_empty + s, ((uint32_t)(k / kURing) & 1) ^ 1));
+                const bool live = v < n_units;
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(uring + s)),
+                             "r"(live ? (int)(v % nqt) : -1), "r"((int)(v / nqt)), "r"(e.x), "r"(e.y)
+                             : "memory");
+                mbar_arrive(unit_full + s);
+            };
+            // Claims run two units ahead of the unit being loaded (a claimed
+            // unit is work no other CTA can take: deeper claims cost balance
+            // at the end of the pass) -- except through a run of single-tile
+            // units, where the claim and the table load of the next units
+            // stay in flight across iterations (vb: claimed, va/ea: claimed
+            // and being resolved).  Units are published in claim order.
+            static_assert(QA_UNIT_LOOKAHEAD == 1 || QA_UNIT_LOOKAHEAD == 2, "1 or 2 units ahead");
+            unsigned va = atomicAdd(a.sched, 1u), vb = 0;
+            int2 ea = resolve(va);
+            publish(0, va, ea);
+            if (QA_UNIT_LOOKAHEAD == 2) {
+                vb = atomicAdd(a.sched, 1u);
+                ea = resolve(vb);
+                publish(1, vb, ea);
+            }
+            bool have_a = false, have_b = false, deep = true;
             for (int it = 0;; ++it) {
-                fetch();
-                const int u = *(volatile int *)(uring + (it & (kURing - 1)));  // own write
-                if (u < 0) break;
-                int64_t t, b;
-                unit_tb(p, u, t, b);
+                int4 un;  // own publication (the slot is rewritten at it + 2 at the earliest)
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(un.x), "=r"(un.y), "=r"(un.z), "=r"(un.w)
+                             : "r"(smem_u32(uring + (it & (kURing - 1))))
+                             : "memory");
+                if (un.x < 0) break;
+                if (!have_a) {
+                    va = have_b ? vb : atomicAdd(a.sched, 1u);
+                    have_b = false;
+                    ea = resolve(va);
+                }
+                publish(it + QA_UNIT_LOOKAHEAD, va, ea);
+                deep = deep && va < n_units && ea.y <= 1;
+                have_a = have_b;
+                if (have_b) {
+                    va = vb;
+                    ea = resolve(vb);  // in flight until the next iteration's publish
+                }
+                have_b = deep;
+                if (deep) vb = atomicAdd(a.sched, 1u);  // in flight until the next iteration
+                const int64_t t = un.x;
                 // resident query tile for this unit
                 const int bslot = it % bslots;
                 const uint32_t bph = (uint32_t)(it / bslots) & 1;
@@ -390,8 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tma_load_2d(dstB + (size_t)c * N * SW, &tm_q, b_full + bslot, c * SW,
                                 (int32_t)(t * N));
                 // streamed database tiles
-                int64_t tile0, tile1;
-                unit_tiles(p, b, tile0, tile1);
+                const int64_t tile0 = un.z, tile1 = (int64_t)un.z + un.w;
                 const int64_t tstep = a.mode == 4 ? a.sample_stride : 1;  // sampled tiles
                 for (int64_t tile = tile0; tile < tile1; ++tile) {
                     const int32_t row0 = (int32_t)(a.r_lo + tile * tstep * kBlockM);
@@ -433,14 +467,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int skip = (nw - 1) * p.kchunks;  // stages of the other warps' tiles
         int first = mw;  // this warp's first tile of the unit
         for (int it = 0;; ++it) {
-            const int u = unit_take(it);
-            if (u < 0) break;
+            const int4 un = unit_take(it);
+            if (un.x < 0) break;
             const int slot = it & 1;
             const uint32_t ph = (it >> 1) & 1;
-            int64_t t, b;
-            unit_tb(p, u, t, b);
-            int64_t tile0, tile1;
-            unit_tiles(p, b, tile0, tile1);
+            const int64_t t = un.x, b = un.y, tile0 = un.z, tile1 = (int64_t)un.z + un.w;
+            (void)b, (void)t, (void)tile0, (void)tile1;
             const int ntl = (int)(tile1 - tile0);
             const int bslot = it % bslots;
             WSTAT(2, mbar_wait_spin(b_full + bslot, (uint32_t)(it / bslots) & 1));
@@ -507,14 +539,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool filtered = (a.mode == 0 || a.mode == 3);
         const int my_slot = warp == kBiasWarp ? 0 : 1;
         for (int it = 0;; ++it) {
-            const int u = unit_take(it);
-            if (u < 0) break;
+            const int4 un = unit_take(it);
+            if (un.x < 0) break;
             const int slot = it & 1;
             if (slot != my_slot) continue;  // the other builder's unit
             const uint32_t ph = (it >> 1) & 1;
-            int64_t t, b, tile0, tile1;
-            unit_tb(p, u, t, b);
-            unit_tiles(p, b, tile0, tile1);
+            const int64_t t = un.x, b = un.y, tile0 = un.z, tile1 = (int64_t)un.z + un.w;
+            (void)b, (void)t, (void)tile0, (void)tile1;
             const int64_t q0 = t * N;
             const int nqt = (int)min((int64_t)N, a.nq - q0);
             // all global reads of the unit issued together: thresholds of
@@ -680,13 +711,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // are copied.  The epilogue never waits on global atomics.
         constexpr int kQPL = N / 32;
         for (int it = 0;; ++it) {
-            const int u = unit_take(it);
-            if (u < 0) break;
+            const int4 un = unit_take(it);
+            if (un.x < 0) break;
             const int slot = it & 1;
             const uint32_t ph = (it >> 1) & 1;
-            int64_t t, b, tile0, tile1;
-            unit_tb(p, u, t, b);
-            unit_tiles(p, b, tile0, tile1);
+            const int64_t t = un.x, b = un.y, tile0 = un.z, tile1 = (int64_t)un.z + un.w;
+            (void)b, (void)t, (void)tile0, (void)tile1;
             const int64_t q0 = t * N;
             const int32_t unit_row0 = (int32_t)(a.r_lo + tile0 * kBlockM);
             WSTAT(8, mbar_wait_sleep(stage_full + slot, ph));
@@ -745,12 +775,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         int efirst = 0;  // grouped epilogue: this group's first tile of the unit
         (void)efirst;
         for (int it = 0;; ++it) {
-            const int u = unit_take(it);
-            if (u < 0) break;
+            const int4 un = unit_take(it);
+            if (un.x < 0) break;
             const int slot = it & 1;
             const uint32_t ph = (it >> 1) & 1;
-            int64_t t, b;
-            unit_tb(p, u, t, b);
+            const int64_t t = un.x, b = un.y, tile0 = un.z, tile1 = (int64_t)un.z + un.w;
+            (void)b, (void)t, (void)tile0, (void)tile1;
             const int64_t q0 = t * N;
             const int nqt = (int)min((int64_t)N, a.nq - q0);
             // this unit's bias, thresholds and exception flags; a free
@@ -760,8 +790,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             int32_t *stage_n = stage_n_all + slot;
             const uint32_t stage_n_addr = smem_u32(stage_n);
             const uint32_t stage_addr = smem_u32(stage_all + slot * stage_cap);
-            int64_t tile0, tile1;
-            unit_tiles(p, b, tile0, tile1);
             const uint32_t thr_addr = smem_u32(thr_all + slot * N);
             const uint32_t bias_addr = smem_u32(bias_s + slot * N);
             const int nch = max(0, min(kCB / kC, (nqt - col0 + kC - 1) / kC));
@@ -1278,7 +1306,11 @@ int64_t tiles_per_unit(int64_t n_tiles, int64_t n_qtiles, int mode, int sms) {
         while (tpu < want && tpu < 32) tpu *= 2;
         return tpu;
     }
-    const int64_t want = (n_tiles * n_qtiles) / ((int64_t)sms * 8);
+    static const int upc = [] {  // diagnostics: units per CTA aimed at
+        const char *v = getenv("QA_B200_UNITS_PER_CTA");
+        return v && atoi(v) > 0 ? atoi(v) : 8;
+    }();
+    const int64_t want = (n_tiles * n_qtiles) / ((int64_t)sms * upc);
     while (tpu * 2 <= want && tpu < 32) tpu *= 2;
     return tpu;
 }
