@@ -1394,7 +1394,11 @@ cudaError_t launch_t(const FilterArgs &a, cudaStream_t st) {
         // count), and a warp may run ahead of the others by a full set of
         // accumulators: the A ring must hold those tiles for the stage
         // barriers to see consecutive phases
-        int w = std::min(kMmaWarpsMax, nacc<N>());
+        // tensor cycles of one tile's MMAs (M128 x N x K32 takes N / 2): one
+        // issuer keeps up once they cover its ~1000-cycle issue sequence
+        // (cfg3, N = 256, K = 256: 78 % of peak with one issuer, 74 % with two)
+        const int tile_cycles = p.kchunks * (SW / 32) * (N / 2);
+        int w = tile_cycles >= 1024 ? 1 : std::min(kMmaWarpsMax, nacc<N>());
         while (w > 1 && (nacc<N>() % w != 0)) --w;
         if (stages < nacc<N>() * p.kchunks) w = 1;
         static const int force_w = [] {  // diagnostics: QA_B200_MMA_WARPS=1/2/4
