@@ -101,6 +101,32 @@ def _resident(arr: np.ndarray, dev, form: str = "rows") -> _dev.DeviceCodes:
     return dc
 
 
+# pinned host staging for results (reused between calls; the caller gets
+# fresh arrays copied out of it)
+_PINNED: dict = {}
+
+
+def _pinned(name: str, shape, dtype) -> torch.Tensor:
+    n = int(np.prod(shape))
+    buf = _PINNED.get(name)
+    if buf is None or buf.numel() < n or buf.dtype != dtype:
+        buf = torch.empty(max(n, 1 << 16), dtype=dtype, pin_memory=True)
+        _PINNED[name] = buf
+    return buf[:n].view(*shape)
+
+
+def _results_to_host(scores: torch.Tensor, ids: torch.Tensor, want_scores: bool = True):
+    """The result matrices through pinned staging with one stream sync."""
+    hi = _pinned("ids", tuple(ids.shape), torch.int32)
+    hi.copy_(ids, non_blocking=True)
+    hs = None
+    if want_scores:
+        hs = _pinned("scores", tuple(scores.shape), torch.float64)
+        hs.copy_(scores, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return (hs.numpy().copy() if want_scores else None), hi.numpy().copy()
+
+
 def _norms_on(norms, dc: _dev.DeviceCodes, dev):
     """Caller norms (caller row order) as a device vector in ``dc``'s stored
     order; the resident copy when they are the matrix' own stored norms
@@ -111,8 +137,10 @@ def _norms_on(norms, dc: _dev.DeviceCodes, dev):
     return t if dc.ids is None else t[dc.ids.long()]
 
 
-def scan_topk(data, queries, k, metric, data_norms=None, query_norms=None):
-    """Exhaustive top-k per query; rows ascending by (score, id)."""
+def scan_topk(data, queries, k, metric, data_norms=None, query_norms=None, *, _ids_only=False):
+    """Exhaustive top-k per query; rows ascending by (score, id).
+    (``_ids_only``: package-internal, batch_ground_truth drops the scores --
+    the first element of the result is then None.)"""
     _check_pair(data, queries)
     if k < 0:
         raise ValueError("k must be >= 0")
@@ -142,8 +170,11 @@ def scan_topk(data, queries, k, metric, data_norms=None, query_norms=None):
     if int(metric) == 2:
         dn = _norms_on(data_norms, db, dev)
         qn = _norms_on(query_norms, qs, dev)
-    scores, ids = _dev.scan_topk(db, qs, int(k), int(metric), dn, qn)
-    return scores.cpu().numpy(), ids.cpu().numpy()
+    # L2 / inner product: the stream-ordered search (no host round trip inside
+    # the scan); angular keeps the synchronous entry, which reports a zero
+    # norm the way exact.py does
+    scores, ids = _dev.scan_topk(db, qs, int(k), int(metric), dn, qn, sync=int(metric) == 2)
+    return _results_to_host(scores, ids, not _ids_only)
 
 
 # ---- single pairs: host arithmetic, exactly the reference's loops ---------

@@ -103,6 +103,19 @@ class GroundTruth:
                 raise ValueError("a per-query neighbor list contains duplicates")
         ids.flags.writeable = False
 
+    @classmethod
+    def from_scan(cls, ids: np.ndarray) -> "GroundTruth":
+        """Wrap the int32 [nq, k] id matrix of an exhaustive scan.  Its rows
+        are distinct, non-negative corpus rows by construction, so the
+        constructor's O(nq k log k) duplicate check is skipped."""
+        if not (isinstance(ids, np.ndarray) and ids.ndim == 2 and ids.dtype == np.int32
+                and ids.flags.c_contiguous):
+            return cls(ids=ids)
+        self = object.__new__(cls)
+        object.__setattr__(self, "ids", ids)
+        ids.flags.writeable = False
+        return self
+
     @property
     def nq(self) -> int:
         return self.ids.shape[0]
