@@ -1406,6 +1406,19 @@ cudaError_t launch_t(const FilterArgs &a, cudaStream_t st) {
             return v ? atoi(v) : 0;
         }();
         if (force_w >= 1 && force_w <= w && nacc<N>() % force_w == 0) w = force_w;
+        // a ring of a multiple of W * kchunks stages gives every stage one
+        // issuer for the whole pass: its full/empty barriers then never skip
+        // a phase for any waiter, whatever order the bulk loads complete in
+        // (ring depth beyond 4 tiles measured no gain: cfg2 4 = 7 stages)
+        if (w > 1) {
+            const int unit = w * p.kchunks;
+            if (stages >= unit) {
+                stages = stages / unit * unit;
+                p.stages = stages;
+            } else {
+                w = 1;
+            }
+        }
         p.mma_warps = w;
     }
     const size_t smem = fixed + (size_t)stages * (stage_bytes + 16);
