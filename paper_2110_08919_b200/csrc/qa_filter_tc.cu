@@ -119,13 +119,11 @@ __host__ __device__ constexpr bool direct_bounds() { return N <= QA_DIRECT_N; } 
 // Epilogue organisation of the filter pass proper (kKind 0) for N >= 128:
 // the 16 epilogue warps form G = min(accumulators, 4) groups; group g takes
 // the CTA's tiles T = g, g + G, ... (the accumulators a = g mod G), each of
-// its warps one TMEM lane quarter x N / (warps per quarter) columns, read 16
-// columns at a time with the next load in flight while the current values
-// are tested.  With every warp on every tile (the other kinds, and N = 64)
+// its warps one TMEM lane quarter x N / (warps per quarter) columns, read as
+// pairs of 16-column loads under one wait.  With every warp on every tile (the other kinds, and N = 64)
 // each warp paid the tile's fixed costs (barrier wait, release, loop) per 32
 // columns and the TMEM load latency was exposed once per tile; the groups
-// pay them once per 128 columns, overlap the load with the tests, and work
-// on G tiles at a time.
+// pay them once per 64 or 128 columns and work on G tiles at a time.
 #ifndef QA_EPI_GROUPS
 #define QA_EPI_GROUPS 1
 #endif
@@ -903,21 +901,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_fence_after();
                     const uint32_t ta = tm_g + (uint32_t)(acc * N);
                     int32_t va[kCh], vb[kCh];
-                    tmem_ld_cols<kCh>(ta, va);
+                    // the two loads of a pair go out back to back and one wait
+                    // covers both (ptxas sinks a load issued between the tests
+                    // below them, so a look-ahead load hid nothing)
 #pragma unroll
                     for (int ch = 0; ch < kNCh; ch += 2) {
+                        tmem_ld_cols<kCh>(ta + (uint32_t)(ch * kCh), va);
+                        tmem_ld_cols<kCh>(ta + (uint32_t)((ch + 1) * kCh), vb);
                         tmem_wait_regs(va);
-                        tmem_ld16_before(ta + (uint32_t)((ch + 1) * kCh), vb, va[0]);
-                        test16(va, ch, row);
                         tmem_wait_regs(vb);
-                        if (ch + 2 < kNCh) {
-                            tmem_ld16_before(ta + (uint32_t)((ch + 2) * kCh), va, vb[0]);
-                        } else {
+                        if (ch + 2 >= kNCh) {
                             // every column is in registers: hand the accumulator back
                             tc_fence_before();
                             __syncwarp();
                             if (lane == 0) mbar_arrive(acc_empty + acc);
                         }
+                        test16(va, ch, row);
                         test16(vb, ch + 1, row);
                     }
                     acc += kG;

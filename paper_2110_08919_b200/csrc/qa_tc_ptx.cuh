@@ -240,22 +240,6 @@ __device__ __forceinline__ void tmem_wait_regs(int32_t (&v)[16]) {
                  : "memory");
 }
 
-// tcgen05.ld of 16 columns that must issue BEFORE any later use of `dep` (a
-// register of the buffer about to be tested): without the false dependence
-// the compiler sinks the load below the tests of the other buffer and the
-// double buffering hides nothing.
-__device__ __forceinline__ void tmem_ld16_before(uint32_t taddr, int32_t (&v)[16], int32_t &dep) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32"
-        " {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15},"
-        " [%17];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "+r"(dep)
-        : "r"(taddr)
-        : "memory");
-}
-
 // tcgen05.ld of C (16 or 32) consecutive accumulator columns of this warp's
 // 32 TMEM lanes; the registers are valid after tmem_wait().
 template <int C>
