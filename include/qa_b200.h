@@ -93,6 +93,23 @@ int qa_encode_i8(const float *x, int64_t n, int64_t d, int64_t ldx,
 int qa_norms_i8(const int8_t *codes, int64_t n, int64_t d, int64_t ldc,
                 int32_t *sqnorm, float *norm, void *stream);
 
+/* ---- distances to listed rows (the service a graph traversal calls) ----
+ * out_scores[q, j] = the reference's pair score _pair_i(query q, row
+ * cand[q, j]) (_core.pyx:88-96) -- what HnswCore._dq / _dist_rows compute one
+ * pair at a time (_core.pyx:472-494): L2 -> (double)l2, IP -> -dot, angular ->
+ * 1 - dot / (qn * xn).  cand is int32 [nq, ldcand] (m used per row); an id
+ * outside [0, n) yields +inf (padding of ragged neighbour lists).
+ * row_of_id (int32 [n] or NULL) maps a caller id to its stored row when the
+ * database is kept in an index layout.  Code rows as produced by
+ * qa_encode_i8 (stride a multiple of 16, zero padded). */
+int qa_gather_scores_i8(const int8_t *db, int64_t n, int64_t d, int64_t ldd,
+                        const int32_t *db_sqnorm, const float *db_norm,
+                        const int32_t *row_of_id,
+                        const int8_t *q, int64_t nq, int64_t ldq,
+                        const int32_t *q_sqnorm, const float *q_norm,
+                        const int32_t *cand, int64_t m, int64_t ldcand, int metric,
+                        double *out_scores, void *stream);
+
 /* ---- exhaustive top-k (_core.pyx:301-365 scan_topk/_scan_i8) ----
  * db[n, ldd] and q[nq, ldq] are int8 codes with ldd, ldq == qa_code_stride(d)
  * (zero padded).  db_sqnorm/q_sqnorm (int32) are required for metric 1,

@@ -184,6 +184,25 @@ int64_t qo_scan_topk_i8(const int8_t *X, int64_t n, int64_t d, const int8_t *Q,
  * accumulation in j order; built with -ffp-contract=off so t*t and the adds
  * round separately exactly as the reference's C does (no FMA on x86-64
  * baseline). ------------------------------------------------------------ */
+/* Scores of listed (query, row) pairs: out[q, j] = pair_i8(Q[q], X[cand[q, j]])
+ * -- HnswCore._dq for an external int8 query (_core.pyx:483-494 -> _pair_i,
+ * 88-96); an id outside [0, n) gives +inf (padding of ragged lists). */
+void qo_pair_scores_i8(const int8_t *X, int64_t n, int64_t d, const int8_t *Q, int64_t nq,
+                       const int32_t *cand, int64_t m, int metric, const float *xn,
+                       const float *qn, double *out) {
+    for (int64_t q = 0; q < nq; ++q)
+        for (int64_t j = 0; j < m; ++j) {
+            const int32_t id = cand[q * m + j];
+            if (id < 0 || id >= n) {
+                out[q * m + j] = INFINITY;
+                continue;
+            }
+            out[q * m + j] = pair_i8(Q + q * d, X + (int64_t)id * d, d, metric,
+                                     metric == 2 ? (double)qn[q] : 0.0,
+                                     metric == 2 ? (double)xn[id] : 0.0);
+        }
+}
+
 static inline double pair_f32(const float *a, const float *b, int64_t d, int metric,
                               double na, double nb) {
     double acc = 0.0;

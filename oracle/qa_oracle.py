@@ -43,6 +43,8 @@ def lib():
         L.qo_minmax_f32.restype = None
         L.qo_scan_topk_i8.argtypes = [vp, i64, i64, vp, i64, i64, ctypes.c_int, vp, vp, vp, vp]
         L.qo_scan_topk_i8.restype = i64
+        L.qo_pair_scores_i8.argtypes = [vp, i64, i64, vp, i64, vp, i64, ctypes.c_int, vp, vp, vp]
+        L.qo_pair_scores_i8.restype = None
         L.qo_norms_f32.argtypes = [vp, i64, i64, vp]
         L.qo_norms_f32.restype = None
         L.qo_scan_topk_f32.argtypes = [vp, i64, i64, vp, i64, i64, ctypes.c_int, vp, vp, vp, vp]
@@ -98,6 +100,23 @@ def scan_topk_i8(X, Q, k, metric, xn=None, qn=None):
     lib().qo_scan_topk_i8(_ptr(X), n, d, _ptr(Q), nq, int(k), int(metric), _ptr(xn), _ptr(qn),
                           _ptr(od), _ptr(oi))
     return od, oi
+
+
+def pair_scores_i8(X, Q, cand, metric, xn=None, qn=None) -> np.ndarray:
+    """float64 [nq, m] scores of the listed (query, row id) pairs, the
+    reference's _pair_i per pair (_core.pyx:88-96, HnswCore._dq 483-494)."""
+    X = np.ascontiguousarray(X, dtype=np.int8)
+    Q = np.ascontiguousarray(Q, dtype=np.int8)
+    cand = np.ascontiguousarray(cand, dtype=np.int32)
+    nq, m = cand.shape
+    out = np.empty((nq, m), dtype=np.float64)
+    if metric == 2:
+        xn = np.ascontiguousarray(xn, dtype=np.float32)
+        qn = np.ascontiguousarray(qn, dtype=np.float32)
+    lib().qo_pair_scores_i8(_ptr(X), X.shape[0], X.shape[1], _ptr(Q), nq, _ptr(cand), m,
+                            int(metric), _ptr(xn) if metric == 2 else None,
+                            _ptr(qn) if metric == 2 else None, _ptr(out))
+    return out
 
 
 def norms_f32(x: np.ndarray) -> np.ndarray:

@@ -14,7 +14,10 @@ Surface (host numpy in, host numpy out, reference semantics):
 * ``dot(a, b)`` / ``l2sq(a, b)`` -- single pairs, _core.pyx:99-134 (through
   the same kernels with n = nq = 1; the batch paths are the hot ones);
 * ``quantize(values, k, sb, se, bits)`` -> int8 [n, d] -- the encode hook the
-  reference lacks (its quantizer.py:291-300 calls numpy directly).
+  reference lacks (its quantizer.py:291-300 calls numpy directly);
+* ``pair_scores(data, queries, cand, metric, ...)`` -> float64 [nq, m] -- the
+  batched form of ``HnswCore._dq`` (_core.pyx:483-494): distances from each
+  query to its listed candidate rows, for a host-side graph traversal.
 
 float32 inputs take the float64-exact path (``qa_scan_topk_f32`` /
 ``qa_norms_f32``, bit-exact with ``_scan_f32`` and the float32 ``norms``
@@ -175,6 +178,39 @@ def scan_topk(data, queries, k, metric, data_norms=None, query_norms=None, *, _i
     # norm the way exact.py does
     scores, ids = _dev.scan_topk(db, qs, int(k), int(metric), dn, qn, sync=int(metric) == 2)
     return _results_to_host(scores, ids, not _ids_only)
+
+
+def pair_scores(data, queries, cand, metric, data_norms=None, query_norms=None):
+    """Scores of listed pairs: float64 [nq, m], out[i, j] = the reference's
+    pair score of ``queries[i]`` and ``data[cand[i, j]]`` (_core.pyx:88-96).
+    This is the batched form of HnswCore._dq (_core.pyx:483-494): a host beam
+    search hands the neighbour lists of a whole query batch to the GPU per
+    hop.  ``cand`` int32 [nq, m]; ids outside [0, n) give +inf.  The frozen
+    corpus stays resident between calls like in ``scan_topk``."""
+    _check_pair(data, queries)
+    if data.dtype != np.int8:
+        raise ValueError("dtype must be int8")
+    cand = np.ascontiguousarray(cand, dtype=np.int32)
+    if cand.ndim != 2 or cand.shape[0] != queries.shape[0]:
+        raise ValueError("cand must be [nq, m]")
+    nq, m = cand.shape
+    if nq == 0 or m == 0 or data.shape[0] == 0:
+        return np.full((nq, m), np.inf, dtype=np.float64)
+    if int(metric) not in _FORM_OF_METRIC:
+        raise ValueError(f"unknown metric {metric}")
+    if int(metric) == 2 and (data_norms is None or query_norms is None
+                             or data_norms.shape[0] != data.shape[0]
+                             or query_norms.shape[0] != nq):
+        raise ValueError("angular metric needs data and query norms")
+    dev = _dev.default_device()
+    db = _resident(data, dev, "rows")
+    qs = _resident(queries, dev, "rows")
+    dn = qn = None
+    if int(metric) == 2:
+        dn = _norms_on(data_norms, db, dev)
+        qn = _norms_on(query_norms, qs, dev)
+    out = _dev.gather_scores(db, qs, torch.from_numpy(cand).to(dev), int(metric), dn, qn)
+    return out.cpu().numpy()
 
 
 # ---- single pairs: host arithmetic, exactly the reference's loops ---------

@@ -88,6 +88,8 @@ SIGNATURES = {
                              c_int, c_vp]),
     "qa_vecs_write": (c_int, [ctypes.c_char_p, c_int, c_vp, c_i64, c_i64, c_i64]),
     "qa_estimate_stats_f32": (c_int, [c_vp, c_i64, c_i64, c_i64] + [c_vp] * 9 + [c_vp]),
+    "qa_gather_scores_i8": (c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64,
+                                    c_vp, c_vp, c_vp, c_i64, c_i64, c_int, c_vp, c_vp]),
     "qa_merge_topk": (c_int, [c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "qa_debug_dots_i8": (c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_int, c_vp, c_vp]),
     "qa_last_scan_stats": (c_int, [ctypes.POINTER(ScanStats)]),

@@ -916,6 +916,29 @@ int qa_norms_i8(const int8_t *codes, int64_t n, int64_t d, int64_t ldc, int32_t 
     return QA_OK;
 }
 
+int qa_gather_scores_i8(const int8_t *db, int64_t n, int64_t d, int64_t ldd,
+                        const int32_t *db_sqnorm, const float *db_norm, const int32_t *row_of_id,
+                        const int8_t *q, int64_t nq, int64_t ldq, const int32_t *q_sqnorm,
+                        const float *q_norm, const int32_t *cand, int64_t m, int64_t ldcand,
+                        int metric, double *out_scores, void *stream) {
+    if (metric < 0 || metric > 2) return set_err(QA_EINVAL, "unknown metric %d", metric);
+    if (n < 0 || nq < 0 || d < 0 || m < 0) return set_err(QA_EINVAL, "negative shape");
+    if (ldd < d || ldq < d || ldcand < m) return set_err(QA_EINVAL, "bad stride");
+    if (nq == 0 || m == 0) return QA_OK;
+    if (ldd % 16 != 0 || ldq % 16 != 0 || ((uintptr_t)db % 16) != 0 || ((uintptr_t)q % 16) != 0)
+        return set_err(QA_EINVAL, "code rows must be 16-byte aligned (qa_code_stride)");
+    if (metric == kL2 && (!db_sqnorm || !q_sqnorm))
+        return set_err(QA_EINVAL, "the L2 metric needs the squared code norms");
+    if (metric == kAngular && (!db_norm || !q_norm))
+        return set_err(QA_EINVAL, "angular metric needs data and query norms");
+    if (metric == kL2 && d > 33025)
+        return set_err(QA_EUNSUPPORTED, "rows wider than the int32-safe range");
+    QA_TRY(launch_gather_scores(db, n, ldd, db_sqnorm, db_norm, row_of_id, q, nq, ldq, q_sqnorm,
+                                q_norm, cand, m, ldcand, metric, out_scores, (cudaStream_t)stream),
+           "gather scores");
+    return QA_OK;
+}
+
 int qa_scan_topk_i8(const int8_t *db, int64_t n, int64_t d, int64_t ldd, const int32_t *db_sqnorm,
                     const float *db_norm, const int32_t *row_ids, const int8_t *q, int64_t nq,
                     int64_t ldq,

@@ -212,6 +212,14 @@ cudaError_t launch_f32_select(const double *scores, int64_t lds, int64_t rows, i
                               cudaStream_t st);
 cudaError_t launch_f32_finalize(const double *st_s, const int32_t *st_i, int64_t nq, int64_t k,
                                 int64_t id_offset, double *out_s, int32_t *out_i, cudaStream_t st);
+// scores of listed (query, row id) pairs (qa_gather.cu)
+cudaError_t launch_gather_scores(const int8_t *db, int64_t n, int64_t ldd,
+                                 const int32_t *db_sqnorm, const float *db_norm,
+                                 const int32_t *row_of_id, const int8_t *q, int64_t nq,
+                                 int64_t ldq, const int32_t *q_sqnorm, const float *q_norm,
+                                 const int32_t *cand, int64_t m, int64_t ldcand, int metric,
+                                 double *out, cudaStream_t st);
+
 cudaError_t launch_norms_f32(const float *x, int64_t n, int64_t d, int64_t ldx, float *out,
                              cudaStream_t st);
 size_t f32_select_smem(int64_t k);

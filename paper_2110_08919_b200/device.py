@@ -217,6 +217,38 @@ def scan_topk(db: DeviceCodes, q: DeviceCodes, k: int, metric: int, db_norm=None
     return scores, ids
 
 
+def gather_scores(db: DeviceCodes, q: DeviceCodes, cand: torch.Tensor, metric: int, db_norm=None,
+                  q_norm=None, row_of_id: torch.Tensor | None = None) -> torch.Tensor:
+    """float64 [nq, m] scores of the listed pairs: out[i, j] = the reference's
+    pair score of query i and database row ``cand[i, j]`` (_core.pyx:88-96;
+    HnswCore._dq / _dist_rows, 472-494).  ``cand``: int32 [nq, m] device
+    tensor of caller ids; ids outside [0, n) (e.g. -1 padding of ragged
+    neighbour lists) give +inf.  ``row_of_id`` maps caller id -> stored row
+    for a database kept in an index layout (see ``inverse_ids``)."""
+    if db.d != q.d:
+        raise ValueError("dimension mismatch between data and queries")
+    if cand.dtype != torch.int32 or cand.dim() != 2 or cand.shape[0] != q.n or not cand.is_cuda:
+        raise ValueError(f"cand must be an int32 [{q.n}, m] CUDA tensor")
+    cand = cand if cand.stride(1) == 1 else cand.contiguous()
+    m = cand.shape[1]
+    out = torch.empty((q.n, m), dtype=torch.float64, device=db.device)
+    dn = db.norm if db_norm is None else db_norm
+    qn = q.norm if q_norm is None else q_norm
+    check(lib.qa_gather_scores_i8(_p(db.codes), db.n, db.d, db.ld, _p(db.sqnorm), _p(dn),
+                                  _p(row_of_id), _p(q.codes), q.n, q.ld, _p(q.sqnorm), _p(qn),
+                                  _p(cand), m, cand.stride(0), int(metric), _p(out), _stream()))
+    return out
+
+
+def inverse_ids(dc: DeviceCodes) -> torch.Tensor | None:
+    """caller id -> stored row of an index-layout DeviceCodes (None: identity)."""
+    if dc.ids is None:
+        return None
+    inv = torch.empty((dc.n,), dtype=torch.int32, device=dc.device)
+    inv[dc.ids.long()] = torch.arange(dc.n, dtype=torch.int32, device=dc.device)
+    return inv
+
+
 def _f32_matrix(x: torch.Tensor, what: str) -> torch.Tensor:
     if x.dtype != torch.float32 or x.dim() != 2 or not x.is_cuda:
         raise ValueError(f"{what} must be a float32 [n, d] CUDA tensor")

@@ -106,6 +106,37 @@ def test_oracle_equals_reference_kernel_on_fresh_instances(oracle):
         np.testing.assert_array_equal(a[0], b[0])
 
 
+def test_pair_scores_equal_reference_scores(oracle):
+    """The listed-pair scores (the batched HnswCore._dq, _core.pyx:483-494)
+    against the reference: its full scan (k = n) gives every row's score per
+    query, and its public dot / l2sq give the integer metrics per pair."""
+    core = oracle.ref_core()
+    if core is None:
+        pytest.skip("reference _core not built here (make -C oracle ref)")
+    rng = np.random.default_rng(77)
+    for i in range(12):
+        n, d, nq, m = int(rng.integers(2, 300)), int(rng.integers(1, 70)), 3, int(rng.integers(1, 20))
+        metric = i % 3
+        X = rng.integers(-128, 128, size=(n, d)).astype(np.int8)
+        Q = rng.integers(-128, 128, size=(nq, d)).astype(np.int8)
+        X[~X.any(axis=1), 0] = 1
+        Q[~Q.any(axis=1), 0] = 1
+        cand = rng.integers(-2, n + 2, size=(nq, m)).astype(np.int32)
+        xn, qn = core.norms(X), core.norms(Q)
+        got = oracle.pair_scores_i8(X, Q, cand, metric, xn, qn)
+        sc, ids = core.scan_topk(X, Q, n, metric, xn, qn)
+        for q in range(nq):
+            by_id = dict(zip(ids[q].tolist(), sc[q].tolist()))
+            for j in range(m):
+                c = int(cand[q, j])
+                want = by_id[c] if 0 <= c < n else np.inf
+                assert got[q, j] == want
+                if 0 <= c < n and metric == 0:
+                    assert got[q, j] == -core.dot(Q[q], X[c])
+                if 0 <= c < n and metric == 1:
+                    assert got[q, j] == core.l2sq(Q[q], X[c])
+
+
 # ----------------------------------------------- float32 path (_scan_f32) --
 
 def test_scan_f32_matches_reference_golden(oracle, golden_scan_f32):
