@@ -625,9 +625,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                           : (long long)ceilf(bf));
                     }
                     Bq[i] = B;
-                    const long long mag = B >= 0 ? B : -B;
-                    const long long per = (long long)kBiasA * kSMax;  // 516k
-                    if (mag <= per * kMaxBiasReps) need = max(need, (int)((mag + per - 1) / per));
+                    const uint32_t mag = (uint32_t)(B >= 0 ? B : -B);  // <= 2^32 - 2^28
+                    constexpr uint32_t per = (uint32_t)kBiasA * kSMax;  // 516k
+                    if (mag <= per * kMaxBiasReps) need = max(need, (int)((mag + per - 1u) / per));
                 }
             }
 #pragma unroll
@@ -657,8 +657,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     S = 0;  // dense / diagnostic passes: plain dots
                 } else if (q < nqt) {
                     // smallest S with reps*127*S >= -B
+                    // (|B| <= 2^32 - 2^20: one unsigned 32-bit division; the
+                    // builder's latency per unit is what short units wait for)
                     const long long nb = -Bq[i];
-                    long long s = nb >= 0 ? (nb + unit_a - 1) / unit_a : -((-nb) / unit_a);
+                    const uint32_t mag = (uint32_t)(nb >= 0 ? nb : -nb);
+                    const uint32_t ua = (uint32_t)unit_a;
+                    const uint32_t qd = mag / ua;
+                    long long s = nb >= 0 ? (long long)qd + (mag - qd * ua != 0u) : -(long long)qd;
                     if (s > kSMax) {
                         s = kSMax;
                         exc = true;
@@ -671,16 +676,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // spread S over 32 int8 digits: base + (j < rem)
                 const int base = (S >= 0) ? S / kBiasK : -((-S + kBiasK - 1) / kBiasK);
                 const int rem = S - base * kBiasK;  // 0 .. 31
-                const uint32_t b8 = (uint32_t)(base & 0xff);
-                const uint32_t b8p = (uint32_t)((base + 1) & 0xff);
+                const uint32_t w0 = (uint32_t)(base & 0xff) * 0x01010101u;
+                const uint32_t w1 = (uint32_t)((base + 1) & 0xff) * 0x01010101u;
+                uint32_t dg[kBiasK / 4];
 #pragma unroll
                 for (int w = 0; w < kBiasK / 4; ++w) {
-                    uint32_t word = 0;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        word |= ((4 * w + j) < rem ? b8p : b8) << (8 * j);
-                    digits_out[q * (kBiasK / 4) + w] = (int32_t)word;
+                    // bytes 4w + j < rem take base + 1
+                    const int mb = rem - 4 * w;
+                    const uint32_t sel = mb >= 4 ? 0xffffffffu : (mb <= 0 ? 0u : ((1u << (8 * mb)) - 1u));
+                    dg[w] = (w0 & ~sel) | (w1 & sel);
                 }
+                static_assert(kBiasK == 32, "two 16-byte stores per query");
+                uint4 *dq = reinterpret_cast<uint4 *>(digits_out + q * (kBiasK / 4));
+                dq[0] = make_uint4(dg[0], dg[1], dg[2], dg[3]);
+                dq[1] = make_uint4(dg[4], dg[5], dg[6], dg[7]);
                 const unsigned eb = __ballot_sync(0xffffffffu, exc);
                 if (lane == 0) exc_s[slot * (N / 32) + i] = eb != 0;
             }
