@@ -774,6 +774,247 @@ __global__ void __launch_bounds__(kRadixWarps * 32) select_radix_kernel(SelectAr
     }
 }
 
+// One CTA (4 warps) per query: the candidate gathers, the histogram passes
+// and the compaction of the radix select above spread over 128 threads; the
+// final 32R-wide sort and the state update stay with warp 0.  One warp per
+// query left 1024 warps on 148 SMs, each a serial chain of dependent global
+// loads and shared-memory passes (40 us per 1024-query batch of cfg2, as long
+// as a fifth of the filter pass it follows).
+constexpr int kRbThreads = 128;
+constexpr int kRbCap = 2048;  // keys per query buffer
+
+// block-wide: the k smallest of U[0, nu) (unique keys) moved to U[0, k) in
+// any order; returns an upper bound T of the k-th smallest with exactly k
+// keys <= T.  All threads call it; `red` is a 256-int scratch, `ctl` 8 ints.
+__device__ unsigned long long radix_keep_k_block(unsigned long long *U, int nu, int k, int *hist,
+                                                 unsigned long long *red64, int *ctl) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned long long kmin = ~0ull, kmax0 = 0;
+    for (int i = tid; i < nu; i += kRbThreads) {
+        const unsigned long long key = U[i];
+        kmin = key < kmin ? key : kmin;
+        kmax0 = key > kmax0 ? key : kmax0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a0 = __shfl_xor_sync(0xffffffffu, kmin, o);
+        const unsigned long long b0 = __shfl_xor_sync(0xffffffffu, kmax0, o);
+        kmin = a0 < kmin ? a0 : kmin;
+        kmax0 = b0 > kmax0 ? b0 : kmax0;
+    }
+    if (lane == 0) {
+        red64[warp] = kmin;
+        red64[4 + warp] = kmax0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kRbThreads / 32; ++w) {
+        kmin = red64[w] < kmin ? red64[w] : kmin;
+        kmax0 = red64[4 + w] > kmax0 ? red64[4 + w] : kmax0;
+    }
+    const int hi = 63 - __clzll((long long)(kmin ^ kmax0) | 1ll);  // highest differing bit
+    const int shift0 = (hi / 8) * 8;
+    unsigned long long mask = shift0 == 56 ? 0ull : ~0ull << (shift0 + 8);
+    unsigned long long prefix = kmin & mask;
+    int want = k;  // rank still to place among keys matching prefix
+    for (int shift = shift0; shift >= 0; shift -= 8) {
+        for (int b = tid; b < 256; b += kRbThreads) hist[b] = 0;
+        __syncthreads();
+        for (int i = tid; i < nu; i += kRbThreads) {
+            const unsigned long long key = U[i];
+            if ((key & mask) == prefix) atomicAdd(hist + (int)((key >> shift) & 255), 1);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            int h[8], sum = 0;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                h[b] = hist[lane * 8 + b];
+                sum += h[b];
+            }
+            int incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const int excl = incl - sum;
+            if (excl < want && incl >= want) {  // the lane whose bins hold rank `want`
+                int c = excl;
+                bool found = false;
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    if (!found && c + h[b] >= want) {
+                        found = true;
+                        ctl[0] = lane * 8 + b;
+                        ctl[1] = c;
+                        ctl[2] = h[b];
+                    }
+                    c += h[b];
+                }
+            }
+        }
+        __syncthreads();
+        const int d = ctl[0], below = ctl[1], eq = ctl[2];
+        want -= below;
+        prefix |= (unsigned long long)d << shift;
+        mask |= 255ull << shift;
+        __syncthreads();  // ctl and hist are rewritten by the next pass
+        if (eq == want) break;  // every key with this prefix is kept
+    }
+    const unsigned long long T = prefix | ~mask;  // keep keys <= T: exactly k of them
+    // every thread reads its keys, then (after a barrier) the kept ones are
+    // written back through a shared counter (the order does not matter)
+    constexpr int kPer = kRbCap / kRbThreads;
+    unsigned long long mine[kPer];
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+        const int i = e * kRbThreads + tid;
+        mine[e] = i < nu ? U[i] : ~0ull;
+    }
+    if (tid == 0) ctl[4] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+        const int i = e * kRbThreads + tid;
+        const bool keep = i < nu && mine[e] <= T;
+        const unsigned bb = __ballot_sync(0xffffffffu, keep);
+        int base = 0;
+        if (lane == 0 && bb) base = atomicAdd(ctl + 4, __popc(bb));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) U[base + __popc(bb & ((1u << lane) - 1))] = mine[e];
+    }
+    __syncthreads();
+    return T;
+}
+
+template <int M, int R>
+__global__ void __launch_bounds__(kRbThreads) select_radix_block_kernel(SelectArgs a) {
+    static_assert(M == kIP || M == kL2, "integer scores");
+    __shared__ unsigned long long U[kRbCap];
+    __shared__ int hist[256];
+    __shared__ unsigned long long red64[8];
+    __shared__ int ctl[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t q = blockIdx.x;
+    const int k = (int)a.k;
+    const int32_t total = a.ccount[q];
+    Entry *st = a.state + q * a.k;
+    const int scur = a.state_cnt[q];
+    const int32_t qq = (M == kL2) ? a.q_sqnorm[q] : 0;
+    int cur = scur;
+    if (total > 0) {
+        const int m = (int)min((int64_t)total, a.cap);
+        if (total > a.cap && tid == 0) {
+            a.overflow[q] = 1;
+            atomicExch(a.any_overflow, 1);
+        }
+        for (int i = tid; i < scur; i += kRbThreads) {
+            RKey64 r;
+            to_key<M>(st[i], r);
+            U[i] = r.k;
+        }
+        if (tid == 0) ctl[5] = scur;  // keys in U
+        if (tid == 0) ctl[6] = 0;     // valid candidates seen
+        __syncthreads();
+        unsigned long long kth = scur == k ? U[k - 1] : ~0ull;  // the state is sorted
+        const Cand *cd = a.cand + q * a.cap;
+        constexpr int kIlp = 4;
+        int nvalid = 0;
+        for (int pos = 0; pos < m;) {
+            // a round gathers what the buffer can take on top of its keys
+            int nu = ctl[5];
+            const int room = kRbCap - nu;
+            const int end = min(m, pos + room);
+            __syncthreads();  // ctl[5] read by everyone before it moves
+            for (int p0 = pos; p0 < end; p0 += kRbThreads * kIlp) {
+                Cand c[kIlp];
+#pragma unroll
+                for (int u = 0; u < kIlp; ++u) {
+                    const int i = p0 + u * kRbThreads + tid;
+                    c[u] = i < end ? cd[i] : Cand{-1, 0};
+                }
+                int32_t xx[kIlp], id[kIlp];
+#pragma unroll
+                for (int u = 0; u < kIlp; ++u) {
+                    const int32_t row = c[u].row >= 0 ? c[u].row : 0;
+                    xx[u] = (M == kL2) ? __ldg(a.db_sqnorm + row) : 0;
+                    id[u] = a.row_ids ? __ldg(a.row_ids + row) : row;
+                }
+#pragma unroll
+                for (int u = 0; u < kIlp; ++u) {
+                    const bool valid = c[u].row >= 0;
+                    unsigned long long key = 0;
+                    if (valid) {
+                        int32_t sc;
+                        if constexpr (M == kIP)
+                            sc = (int32_t)(0u - (uint32_t)c[u].dot);
+                        else
+                            sc = (int32_t)((uint32_t)qq + (uint32_t)xx[u] - 2u * (uint32_t)c[u].dot);
+                        key = (skey_from_int(sc) << 32) | (uint32_t)id[u];
+                    }
+                    const bool keep = valid && key <= kth;
+                    nvalid += valid ? 1 : 0;
+                    const unsigned bb = __ballot_sync(0xffffffffu, keep);
+                    int base = 0;
+                    if (lane == 0 && bb) base = atomicAdd(ctl + 5, __popc(bb));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (keep) U[base + __popc(bb & ((1u << lane) - 1))] = key;
+                }
+            }
+            pos = end;
+            __syncthreads();
+            nu = ctl[5];
+            if (nu > k) {
+                kth = radix_keep_k_block(U, nu, k, hist, red64, ctl);
+                if (tid == 0) ctl[5] = k;
+                __syncthreads();
+            }
+        }
+        cur = min(ctl[5], k);
+        // valid-candidate count (statistics)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nvalid += __shfl_xor_sync(0xffffffffu, nvalid, o);
+        if (lane == 0 && a.cand_count && nvalid) atomicAdd(a.cand_count, (unsigned long long)nvalid);
+    }
+    if (warp != 0) return;  // the sort and the state update: one warp
+    if (a.next_fill >= 0 && lane == 0) a.ccount_reset[q] = a.next_fill;
+    RKey64 t[R];
+    if (total > 0) {
+#pragma unroll
+        for (int e = 0; e < R; ++e) {
+            const int i = e * 32 + lane;
+            t[e].k = i < cur ? U[i] : ~0ull;
+        }
+        rsort(t);
+#pragma unroll
+        for (int e = 0; e < R; ++e) {
+            const int i = e * 32 + lane;
+            if (i < cur) st[i] = from_key(t[e]);
+        }
+        if (cur == k) {
+            const RKey64 v = rget(t, k - 1);
+            if (lane == 0) a.thr[q] = threshold_of<M>(from_key(v), qq, 1.0f);
+        }
+        if (lane == 0) a.state_cnt[q] = cur;
+    }
+    if (a.est_j > 0) {
+        // fused threshold estimate (see select_reg_kernel)
+        const int j = (int)a.est_j;
+        const int cnt = total > 0 ? cur : scur;
+        if (cnt < j) {
+            if (lane == 0 && !a.est_combine) a.est[q] = ~0ull;
+            return;
+        }
+        const Entry e = total > 0 ? from_key(rget(t, j - 1)) : a.state[q * a.k + j - 1];
+        if (lane == 0) {
+            a.thr[q] = threshold_of<M>(e, qq, 1.0f);
+            const unsigned long long prev = a.est[q];
+            a.est[q] = (a.est_combine && prev != ~0ull && prev < e.skey) ? prev : e.skey;
+        }
+    }
+}
+
 __global__ void reset_kernel(int32_t *p, int64_t n, int32_t v) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -1204,6 +1445,20 @@ cudaError_t launch_select_t(const SelectArgs &a, cudaStream_t st) {
     }();
     if constexpr (M != kAngular) {
         // large batches, integer scores: one warp per query, radix select
+        static const bool block_on = [] {
+            const char *v = getenv("QA_B200_SEL_BLOCK");  // diagnostics: 0 = one warp per query
+            return !(v && strcmp(v, "0") == 0);
+        }();
+        if (radix_on && block_on && a.k <= 128 && a.nq >= 256 && a.nq <= 65535 * 16) {
+            const unsigned grid = (unsigned)a.nq;
+            if (a.k <= 32)
+                select_radix_block_kernel<M, 1><<<grid, kRbThreads, 0, st>>>(a);
+            else if (a.k <= 64)
+                select_radix_block_kernel<M, 2><<<grid, kRbThreads, 0, st>>>(a);
+            else
+                select_radix_block_kernel<M, 4><<<grid, kRbThreads, 0, st>>>(a);
+            return cudaGetLastError();
+        }
         if (radix_on && a.k <= 128 && a.nq >= 256) {
             const unsigned grid = (unsigned)((a.nq + kRadixWarps - 1) / kRadixWarps);
             if (a.k <= 32)
