@@ -173,7 +173,8 @@ __device__ __forceinline__ double tile_hi_of(int metric, const int32_t *hi, int6
 __global__ void __launch_bounds__(kUnitThreads) unit_table_kernel(
     int metric, const int32_t *__restrict__ lo, const int32_t *__restrict__ hi, int64_t tile_lo,
     int64_t n_tiles, int tpu, int32_t *__restrict__ table, int32_t *__restrict__ count,
-    unsigned *__restrict__ ticket, double *__restrict__ rmin, double *__restrict__ rmax) {
+    unsigned *__restrict__ ticket, double *__restrict__ rmin, double *__restrict__ rmax,
+    int tail_pct, int tail_split) {
     using Reduce = cub::BlockReduce<double, kUnitThreads>;
     using Scan = cub::BlockScan<int, kUnitThreads>;
     __shared__ union {
@@ -239,10 +240,18 @@ __global__ void __launch_bounds__(kUnitThreads) unit_table_kernel(
     // split only when the wide runs are the exception (a layout that is not
     // norm-ordered has no narrow runs; single tiles would only add overhead)
     const bool split = (int64_t)s_wide * 8 <= B;
+    // the runs at the end of the table are cut into `tail_split` units each:
+    // units are handed out in table order, and a CTA that takes one of the
+    // last full runs ends a unit's length after the others (the slowest CTA
+    // of a cfg2 pass ended 10 % after the median)
+    const int64_t cut = B - (B * tail_pct) / 100;
+    auto parts_of = [&](int64_t r) {
+        return (r >= cut && tail_split > 1 && tiles_of(r) >= tail_split) ? tail_split : 1;
+    };
     int n_split = 0, n_reg = 0;
     for (int64_t r = b0; r < b1; ++r) {
         if (split && wide(r)) n_split += tiles_of(r);
-        else n_reg += 1;
+        else n_reg += parts_of(r);
     }
     int off_split, off_reg, tot_split;
     Scan(tmp.s).ExclusiveSum(n_split, off_split, tot_split);
@@ -257,9 +266,15 @@ __global__ void __launch_bounds__(kUnitThreads) unit_table_kernel(
                 ++off_split;
             }
         } else {
-            table[2 * off_reg] = (int32_t)(r * tpu);
-            table[2 * off_reg + 1] = tiles_of(r);
-            ++off_reg;
+            const int parts = parts_of(r), nt = tiles_of(r);
+            int t0 = 0;
+            for (int i = 0; i < parts; ++i) {
+                const int len = (nt - t0) / (parts - i);
+                table[2 * off_reg] = (int32_t)(r * tpu) + t0;
+                table[2 * off_reg + 1] = len;
+                t0 += len;
+                ++off_reg;
+            }
         }
     }
     if (threadIdx.x == kUnitThreads - 1) *count = off_reg;
@@ -274,8 +289,17 @@ cudaError_t launch_unit_table(int metric, const int32_t *grp_lo, const int32_t *
         return cudaErrorInvalidValue;
     const int64_t B = (n_tiles + tpu - 1) / tpu;
     const unsigned grid = (unsigned)((B + kUnitThreads / 32 - 1) / (kUnitThreads / 32));
+    static const int tail_pct = [] {  // diagnostics: share of the runs cut into smaller units
+        const char *v = getenv("QA_B200_TAIL_PCT");
+        return v ? atoi(v) : 10;
+    }();
+    static const int tail_split = [] {
+        const char *v = getenv("QA_B200_TAIL_SPLIT");
+        return v ? atoi(v) : 2;  // cfg2: the last 10 % halved +2.7 %; quarters or 20 % cost more than they save
+    }();
     unit_table_kernel<<<grid, kUnitThreads, 0, st>>>(metric, grp_lo, grp_hi, tile_lo, n_tiles, tpu,
-                                                     table, count, ticket, scratch, scratch + B);
+                                                     table, count, ticket, scratch, scratch + B,
+                                                     tail_pct, tail_split);
     return cudaGetLastError();
 }
 
