@@ -352,7 +352,8 @@ cudaError_t sampled_chunk(const ScanPlan &pl, int64_t n, int64_t d_alg, int64_t 
     // wide norm ranges (cfg2: the lowest 4096-row block spans 180x the median
     // block), their bound admits nearly every element to the exact test, and
     // one such unit outlasted the rest of the pass (538 -> 291 us per cfg2
-    // batch as single-tile units).  Angular tests survivors in the select,
+    // batch as single-tile units; 8-tile units since the epilogue parks its
+    // candidates: qa_layout.cu).  Angular tests survivors in the select,
     // not the epilogue: there the extra units cost more (cfg1 +16 %); so do
     // they for a handful of queries, whose exact tests are few (cfg4 batch
     // 1 / 8: +25 us, batch 64: -15 us).

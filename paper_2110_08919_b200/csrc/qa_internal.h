@@ -76,7 +76,7 @@ struct FilterArgs {
 // The work-unit table of a mode-0 pass over tiles [tile_lo, tile_lo + n_tiles)
 // (global 128-row tile indices): aligned runs of `tpu` tiles, except runs
 // whose norm range is wide (the index's sparse norm tails), which are split
-// into single tiles so each gets its own bound; the split units come first so
+// into short units (8 tiles) with tighter bounds; the split units come first so
 // their extra cost starts early.  table needs 2 * n_tiles ints, scratch
 // 2 * ceil(n_tiles / tpu) doubles; *ticket must be 0 (the kernel leaves it 0).
 cudaError_t launch_unit_table(int metric, const int32_t *grp_lo, const int32_t *grp_hi,

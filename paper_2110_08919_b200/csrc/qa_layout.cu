@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kUnitThreads) unit_table_kernel(
     int metric, const int32_t *__restrict__ lo, const int32_t *__restrict__ hi, int64_t tile_lo,
     int64_t n_tiles, int tpu, int32_t *__restrict__ table, int32_t *__restrict__ count,
     unsigned *__restrict__ ticket, double *__restrict__ rmin, double *__restrict__ rmax,
-    int tail_pct, int tail_split) {
+    int tail_pct, int tail_split, int wide_tiles) {
     using Reduce = cub::BlockReduce<double, kUnitThreads>;
     using Scan = cub::BlockScan<int, kUnitThreads>;
     __shared__ union {
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kUnitThreads) unit_table_kernel(
     };
     int n_split = 0, n_reg = 0;
     for (int64_t r = b0; r < b1; ++r) {
-        if (split && wide(r)) n_split += tiles_of(r);
+        if (split && wide(r)) n_split += (tiles_of(r) + wide_tiles - 1) / wide_tiles;
         else n_reg += parts_of(r);
     }
     int off_split, off_reg, tot_split;
@@ -260,9 +260,10 @@ __global__ void __launch_bounds__(kUnitThreads) unit_table_kernel(
     off_reg += tot_split;
     for (int64_t r = b0; r < b1; ++r) {
         if (split && wide(r)) {
-            for (int64_t g = r * tpu; g < min(n_tiles, (r + 1) * tpu); ++g) {
+            const int64_t g1 = min(n_tiles, (r + 1) * tpu);
+            for (int64_t g = r * tpu; g < g1; g += wide_tiles) {
                 table[2 * off_split] = (int32_t)g;
-                table[2 * off_split + 1] = 1;
+                table[2 * off_split + 1] = (int32_t)min((int64_t)wide_tiles, g1 - g);
                 ++off_split;
             }
         } else {
@@ -293,13 +294,20 @@ cudaError_t launch_unit_table(int metric, const int32_t *grp_lo, const int32_t *
         const char *v = getenv("QA_B200_TAIL_PCT");
         return v ? atoi(v) : 10;
     }();
+    static const int wide_tiles = [] {  // tiles per unit of a wide-norm run
+        const char *v = getenv("QA_B200_WIDE_TILES");
+        // cfg2: 8 (= 4) tiles +3.3 % over single tiles, 16 +2.5 %, whole runs
+        // -3.5 %: once a candidate costs little in the epilogue, a unit's
+        // fixed cost (its bias build) outweighs the tighter single-tile bound
+        return v && atoi(v) > 0 ? atoi(v) : 8;
+    }();
     static const int tail_split = [] {
         const char *v = getenv("QA_B200_TAIL_SPLIT");
         return v ? atoi(v) : 2;  // cfg2: the last 10 % halved +2.7 %; quarters or 20 % cost more than they save
     }();
     unit_table_kernel<<<grid, kUnitThreads, 0, st>>>(metric, grp_lo, grp_hi, tile_lo, n_tiles, tpu,
                                                      table, count, ticket, scratch, scratch + B,
-                                                     tail_pct, tail_split);
+                                                     tail_pct, tail_split, wide_tiles);
     return cudaGetLastError();
 }
 
