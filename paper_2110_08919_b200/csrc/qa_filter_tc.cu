@@ -1331,6 +1331,7 @@ int pick_tile_n(int64_t nq, int64_t kdim, int mode) {
         const char *v = getenv("QA_B200_TILE_N");
         return v ? atoi(v) : 0;
     }();
+    if (force_n == 256 && nmax >= 256 && nq > 128 && mode == 0) return 256;
     if (force_n == 128 && nmax >= 128) return 128;
     if (force_n == 64 && nmax >= 64) return 64;
     // 256-query tiles only when K is long enough for the MMA time per tile to
