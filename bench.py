@@ -307,6 +307,16 @@ def run_gpu(args):
         return sharded.sharded_search(lambda off: index.search_codes(qcodes[i], k), n, k)
 
     def device_step():
+        if world > 1:
+            # the all-gather of batch i overlaps the scan of batch i + 1
+            def local_for(i, a, b):
+                def local(_off):
+                    index.encode_queries(q_dev[a:b], out=qcodes[i])
+                    return index.search_codes(qcodes[i], k)
+                return local
+            sharded.sharded_search_batches([local_for(i, a, b) for i, (a, b) in enumerate(spans)],
+                                           n, k)
+            return
         for i, (a, b) in enumerate(spans):
             search_batch(i, q_dev[a:b])
 

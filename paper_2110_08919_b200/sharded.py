@@ -37,12 +37,22 @@ def gather_topk(scores: torch.Tensor, ids: torch.Tensor, group=None):
     Every rank must pass the same kin (ranks whose shard has fewer rows pad
     with +inf scores / INT32_MAX ids, which sort last)."""
     world = dist.get_world_size(group)
-    nq, kin = scores.shape
-    packed = torch.cat([scores.contiguous().view(torch.uint8).reshape(nq, kin * 8),
-                        ids.contiguous().view(torch.uint8).reshape(nq, kin * 4)], dim=1)
+    kin = scores.shape[1]
+    packed = _pack(scores, ids)
     parts = [torch.empty_like(packed) for _ in range(world)]
     dist.all_gather(parts, packed, group=group)
+    return _unpack(parts, kin)
+
+
+def _pack(scores: torch.Tensor, ids: torch.Tensor) -> torch.Tensor:
+    nq, kin = scores.shape
+    return torch.cat([scores.contiguous().view(torch.uint8).reshape(nq, kin * 8),
+                      ids.contiguous().view(torch.uint8).reshape(nq, kin * 4)], dim=1)
+
+
+def _unpack(parts, kin: int):
     allp = torch.stack(parts)  # [world, nq, kin * 12]
+    world, nq = allp.shape[0], allp.shape[1]
     s_all = allp[:, :, : kin * 8].contiguous().view(torch.float64).reshape(world, nq, kin)
     i_all = allp[:, :, kin * 8:].contiguous().view(torch.int32).reshape(world, nq, kin)
     return s_all, i_all
@@ -76,3 +86,40 @@ def sharded_search(local_search: Callable[[int], tuple], n_total: int, k: int,
     if merge is None:
         from .device import merge_topk as merge
     return merge(s_all, i_all, keff)
+
+
+def sharded_search_batches(local_searches, n_total: int, k: int, merge: Callable | None = None,
+                           group=None):
+    """``sharded_search`` for a sequence of query batches, pipelined: batch
+    i's all-gather is issued asynchronously and waited for only after batch
+    i + 1's local search has been launched, so the exchange (NCCL's own
+    stream) overlaps the next batch's scan.  ``local_searches``: one
+    ``id_offset -> (scores, ids)`` callable per batch.  Returns the list of
+    merged (scores, ids), equal to calling ``sharded_search`` per batch."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    lo, _ = shard_bounds(n_total, world, rank)
+    kin = min(k, -(-n_total // world))
+    keff = min(k, n_total)
+    if merge is None:
+        from .device import merge_topk as merge
+    results = []
+    pending = None  # (work, parts) of the previous batch
+
+    def finish(p):
+        work, parts = p
+        work.wait()
+        s_all, i_all = _unpack(parts, kin)
+        results.append(merge(s_all, i_all, keff))
+
+    for local_search in local_searches:
+        scores, ids = pad_topk(*local_search(lo), kin)
+        packed = _pack(scores, ids)
+        parts = [torch.empty_like(packed) for _ in range(world)]
+        work = dist.all_gather(parts, packed, group=group, async_op=True)
+        if pending is not None:
+            finish(pending)
+        pending = (work, parts)
+    if pending is not None:
+        finish(pending)
+    return results

@@ -77,6 +77,51 @@ def _worker(rank, world, port, X, Q, k, metric, out):
     dist.destroy_process_group()
 
 
+def _worker_batches(rank, world, port, X, Qs, k, metric, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2110_08919_b200 import sharded
+
+    lo, hi = sharded.shard_bounds(X.shape[0], world, rank)
+
+    def local_for(Q):
+        def local(id_offset):
+            s, i = _np_topk(X[lo:hi], Q, k, metric)
+            return torch.from_numpy(s), torch.from_numpy(i + id_offset)
+        return local
+
+    res = sharded.sharded_search_batches([local_for(Q) for Q in Qs], X.shape[0], k,
+                                         merge=_merge_host)
+    out[rank] = [(s.numpy(), i.numpy()) for s, i in res]
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_pipelined_batches_equal_full_scan(oracle, world):
+    """sharded_search_batches (the gather of batch i overlapped with the scan
+    of batch i + 1): every batch equals the single-process full scan."""
+    rng = np.random.default_rng(91 + world)
+    n, k, metric = 700, 40, 1
+    X = rng.integers(-4, 5, size=(n, 12)).astype(np.int8)
+    X[~X.any(axis=1), 0] = 1
+    Qs = []
+    for nq in (5, 1, 8, 3):  # ragged batches
+        Q = rng.integers(-4, 5, size=(nq, 12)).astype(np.int8)
+        Q[~Q.any(axis=1), 0] = 1
+        Qs.append(Q)
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.start_processes(_worker_batches, args=(world, _free_port(), X, Qs, k, metric, out),
+                       nprocs=world, join=True, start_method="fork")
+    for b, Q in enumerate(Qs):
+        want_s, want_i = oracle.scan_topk_i8(X, Q, k, metric, oracle.norms_i8(X), oracle.norms_i8(Q))
+        for rank in range(world):
+            s, i = out[rank][b]
+            np.testing.assert_array_equal(i, want_i)
+            np.testing.assert_array_equal(s, want_s)
+
+
 @pytest.mark.parametrize("metric", [0, 1, 2])
 @pytest.mark.parametrize("world,n,k", [(2, 1001, 50), (3, 1001, 50), (3, 100, 50)])
 def test_gloo_merge_equals_full_scan(oracle, metric, world, n, k):
