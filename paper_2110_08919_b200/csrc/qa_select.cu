@@ -1449,7 +1449,15 @@ cudaError_t launch_select_t(const SelectArgs &a, cudaStream_t st) {
             const char *v = getenv("QA_B200_SEL_BLOCK");  // diagnostics: 0 = one warp per query
             return !(v && strcmp(v, "0") == 0);
         }();
-        if (radix_on && block_on && a.k <= 128 && a.nq >= 256 && a.nq <= 65535 * 16) {
+        static const int64_t block_minq = [] {  // diagnostics: smallest batch for the CTA-per-query select
+            const char *v = getenv("QA_B200_SEL_BLOCK_MINQ");
+            return v ? (int64_t)atoll(v) : (int64_t)256;
+        }();
+        // small batches too once k > 32: the register select's 64/128-wide
+        // networks per candidate chunk cost more than the radix passes (cfg4
+        // k = 100: 0.27-0.33 -> 0.25-0.29 ms; k = 10 keeps the register select)
+        if (radix_on && block_on && a.k <= 128 && (a.nq >= block_minq || a.k > 32) &&
+            a.nq <= 65535 * 16) {
             const unsigned grid = (unsigned)a.nq;
             if (a.k <= 32)
                 select_radix_block_kernel<M, 1><<<grid, kRbThreads, 0, st>>>(a);
