@@ -780,7 +780,11 @@ __global__ void __launch_bounds__(kRadixWarps * 32) select_radix_kernel(SelectAr
 // query left 1024 warps on 148 SMs, each a serial chain of dependent global
 // loads and shared-memory passes (40 us per 1024-query batch of cfg2, as long
 // as a fifth of the filter pass it follows).
-constexpr int kRbThreads = 128;
+#ifndef QA_RB_THREADS
+#define QA_RB_THREADS 128
+#endif
+constexpr int kRbThreads = QA_RB_THREADS;
+constexpr int kRbWarps = kRbThreads / 32;
 constexpr int kRbCap = 2048;  // keys per query buffer
 
 // block-wide: the k smallest of U[0, nu) (unique keys) moved to U[0, k) in
@@ -804,13 +808,13 @@ __device__ unsigned long long radix_keep_k_block(unsigned long long *U, int nu, 
     }
     if (lane == 0) {
         red64[warp] = kmin;
-        red64[4 + warp] = kmax0;
+        red64[kRbWarps + warp] = kmax0;
     }
     __syncthreads();
 #pragma unroll
     for (int w = 0; w < kRbThreads / 32; ++w) {
         kmin = red64[w] < kmin ? red64[w] : kmin;
-        kmax0 = red64[4 + w] > kmax0 ? red64[4 + w] : kmax0;
+        kmax0 = red64[kRbWarps + w] > kmax0 ? red64[kRbWarps + w] : kmax0;
     }
     const int hi = 63 - __clzll((long long)(kmin ^ kmax0) | 1ll);  // highest differing bit
     const int shift0 = (hi / 8) * 8;
@@ -893,7 +897,7 @@ __global__ void __launch_bounds__(kRbThreads) select_radix_block_kernel(SelectAr
     static_assert(M == kIP || M == kL2, "integer scores");
     __shared__ unsigned long long U[kRbCap];
     __shared__ int hist[256];
-    __shared__ unsigned long long red64[8];
+    __shared__ unsigned long long red64[2 * kRbWarps];
     __shared__ int ctl[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t q = blockIdx.x;
