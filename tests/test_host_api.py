@@ -157,3 +157,23 @@ def test_acceptance_gate1_quantizer_order_range_reconstruction():
             q = qa.quantize_value(float(x), 0, p)
             assert abs(qa.dequantize_value(q, 0, p) - float(x)) <= width / (1 << bits)
     assert checked == 10_000
+
+
+def test_ground_truth_from_scan_matches_constructor():
+    """GroundTruth.from_scan (the scan's own id matrix: distinct rows by
+    construction) equals the checked constructor on valid input, freezes the
+    array, and falls back to the checked constructor for anything else."""
+    import numpy as np
+    import pytest
+
+    import paper_2110_08919_b200 as qa
+
+    ids = np.array([[3, 1, 2], [0, 2, 5]], dtype=np.int32)
+    a = qa.GroundTruth(ids=ids.copy())
+    b = qa.GroundTruth.from_scan(ids.copy())
+    assert a == b and b.nq == 2 and b.k == 3
+    assert not b.ids.flags.writeable
+    c = qa.GroundTruth.from_scan(ids.astype(np.int64))   # not int32: the checked path
+    assert c == a and c.ids.dtype == np.int32
+    with pytest.raises(ValueError):
+        qa.GroundTruth.from_scan(np.array([[1, 1]], dtype=np.int64))  # duplicates still caught there
